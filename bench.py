@@ -1,0 +1,390 @@
+#!/usr/bin/env python
+"""bench.py -- emulated FP64 TFLOP/s of the FP8 Ozaki-II DGEMM (arxiv 2603.10634) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl oz2|reference]
+
+Workload (BASELINE.json config 3, the headline): m = n = k = 16384 per GPU, paper
+generator a = (rand - 0.5) exp(randn * phi) with phi = 1, accurate mode,
+hybrid moduli, N = 13 (the smallest N whose normwise error is at cuBLAS-DGEMM level at
+k = 16384).  A step is one full oz2_dgemm (all six stages) on inputs
+resident in HBM; with --gpus G > 1 (torchrun, NCCL) every rank owns a 16384-row
+block of A and C and B is broadcast from rank 0 inside every step (weak scaling).
+
+Printed JSON line (rank 0): the contract keys plus
+  roofline      the dominant kernel (residue GEMMs, tcgen05 kind::f8f6f4), timed with
+                the library's CUDA-event phase timers on its launch stream, against the
+                FP8 dense peak = 2 x the measured cuBLAS bf16 sustained peak
+                (MEASURED_PEAKS.json x the nominal fp8/bf16 ratio 4.5/2.25)
+  e2e           the same metric through oz2_dgemm with pinned HOST buffers (H2D of A, B
+                and D2H of C inside the timed region)
+  cpu_baseline  the oracle (oracle/, pure Python + numpy) on a bounded sub-block
+  cublas        native torch.matmul float64 (cuBLAS DGEMM) on the same inputs
+  accuracy      normwise / max relative error of oz2 and of cuBLAS against the exact
+                product on sampled entries, and the moduli sweep (N = 12..16)
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "emulated FP64 TFLOP/s at n=16384 vs cuBLAS DGEMM; max rel err vs moduli count"
+UNIT = "TFLOP/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="oz2", choices=["oz2", "reference"])
+    ap.add_argument("--n", type=int, default=16384)
+    ap.add_argument("--moduli", type=int, default=13)
+    ap.add_argument("--phi", type=float, default=1.0)
+    ap.add_argument("--no-extras", action="store_true", help="skip e2e/cuBLAS/accuracy/sweep/cpu legs")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------------- utils
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sms.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per residue-GEMM launch from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_residue_gemm.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def two_prod_exact_dot(a, b):
+    """RN64 of the exact dot product (Dekker TwoProduct + fsum); accuracy probe only."""
+    import numpy as np
+    p = a * b
+    c = 134217729.0
+    ah = c * a
+    ah = ah - (ah - a)
+    al = a - ah
+    bh = c * b
+    bh = bh - (bh - b)
+    bl = b - bh
+    e = ((ah * bh - p) + ah * bl + al * bh) + al * bl
+    return math.fsum(np.concatenate([p, e]).tolist())
+
+
+# ---------------------------------------------------------------------------------- oz2 arm
+
+def run_oz2(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2603_10634_b200 as P
+    from synth import gen_device
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    n = k = args.n
+    m = args.n                                   # rows per rank (weak scaling)
+    N = args.moduli
+    A = gen_device(m, k, "phi", phi=args.phi, seed=1000 + rank, device="cuda")
+    B = gen_device(k, n, "phi", phi=args.phi, seed=7, device="cuda") if rank == 0 else \
+        torch.empty((n, k), dtype=torch.float64, device="cuda").t()
+    C = torch.empty((n, m), dtype=torch.float64, device="cuda").t()
+    stream = torch.cuda.current_stream()
+    P.oz2_set_stream(stream.cuda_stream)
+    ws_bytes = P.oz2_workspace_size("N", "N", m, n, k, N)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    P.oz2_set_workspace(ws.data_ptr(), ws.numel())
+
+    def step():
+        if world > 1:
+            dist.broadcast(B, src=0)
+        rc = P.oz2_dgemm("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0, C.data_ptr(), m, N)
+        if rc != 0:
+            raise RuntimeError(f"oz2_dgemm rc={rc}")
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local_rank)
+    P.oz2_set_timing(True)
+    phase_acc = {}
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.3)
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+        ph = P.oz2_get_timing()
+        for key, v in ph.items():
+            phase_acc.setdefault(key, []).append(v)
+    ev1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    P.oz2_set_timing(False)
+    elapsed = ev0.elapsed_time(ev1)                    # ms, this rank
+    t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = t.item()
+    ms_per_step = ms_total / args.steps
+    flops_rank = 2.0 * m * n * k
+    value = world * flops_rank * args.steps / (ms_total * 1e-3) / 1e12
+
+    phases = {key: statistics.median(v) for key, v in phase_acc.items()}
+    peaks, peak_kind = measured_peaks()
+    fp8_peak = 2.0 * peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    gemm_ms = statistics.mean(phase_acc["residue_gemm"])
+    gemm_flops = 3 * N * 2.0 * m * n * k
+    achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12
+    traffic = None
+    tr = ncu_traffic()
+    if tr and tr.get("m") == m and tr.get("num_moduli") == N:
+        traffic = tr.get("dram_bytes_per_launch")
+    roofline = {"kernel": "gemm_kernel<MODE_RESIDUE> (3N tcgen05 FP8 GEMMs + modular epilogue)",
+                "bound": "tensor", "achieved": round(achieved, 1), "peak": round(fp8_peak, 1),
+                "unit": "TFLOP/s", "frac": round(achieved / fp8_peak, 4), "traffic": traffic,
+                "peak_source": f"{peak_kind}: 2 x bf16_tflops_sustained (nominal fp8/bf16 = 4.5/2.25)",
+                "algorithmic_flops_per_launch": gemm_flops,
+                "share_of_step": round(gemm_ms / phases["total"], 4)}
+    launches_per_step = 10
+
+    out = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (paper generator (rand-0.5)*exp(randn*phi), seeded, on device)",
+        "config": {"workload": f"config3: m=n=k={args.n} per GPU, phi={args.phi}, N={N} hybrid moduli, accurate mode",
+                   "m_per_gpu": m, "n": n, "k": k, "num_moduli": N, "phi": args.phi,
+                   "l2": "no flush: A, B, C are 2 GiB each (>> 126 MB L2)",
+                   "parallelism": f"row-sharded A/C over {world} GPU(s), B broadcast (NCCL)" if world > 1 else "single GPU"},
+        "gpu_launches": launches_per_step * args.steps,
+        "phases_ms": {k_: round(v, 3) for k_, v in phases.items()},
+        "roofline": roofline,
+        "clocks": clocks,
+    }
+    if rank != 0 or args.no_extras:
+        return out, None
+
+    extras = {}
+    # ---- cuBLAS DGEMM on the same inputs
+    ref = torch.empty_like(C)
+    for _ in range(2):
+        torch.matmul(A, B, out=ref)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = max(3, min(args.steps, 10))
+    e0.record()
+    for _ in range(reps):
+        torch.matmul(A, B, out=ref)
+    e1.record()
+    torch.cuda.synchronize()
+    cub_ms = e0.elapsed_time(e1) / reps
+    extras["cublas"] = {"tflops": round(flops_rank / (cub_ms * 1e-3) / 1e12, 3), "ms": round(cub_ms, 3),
+                        "speedup_oz2_vs_cublas": round(value / world / (flops_rank / (cub_ms * 1e-3) / 1e12), 3)}
+
+    # ---- accuracy against the exact product on sampled entries, and the N sweep
+    rng = np.random.default_rng(0)
+    I = rng.choice(m, 8, replace=False)
+    J = rng.choice(n, 8, replace=False)
+    Ah = A[I, :].cpu().numpy()
+    Bh = B[:, J].cpu().numpy()
+    exact = np.array([[two_prod_exact_dot(Ah[a], Bh[:, b]) for b in range(len(J))] for a in range(len(I))])
+
+    def errs(Cs):
+        d = Cs - exact
+        return {"normwise": float(np.linalg.norm(d) / np.linalg.norm(exact)),
+                "max_rel": float(np.max(np.abs(d) / np.abs(exact)))}
+
+    step()
+    torch.cuda.synchronize()
+    acc = {"sample": "8 x 8 entries, exact dot products (TwoProduct + fsum)",
+           f"oz2_N{N}": errs(C[I][:, J].cpu().numpy()),
+           "cublas": errs(ref[I][:, J].cpu().numpy())}
+    sweep = {}
+    for NN in [12, 13, 14, 16]:
+        ws2 = P.oz2_workspace_size("N", "N", m, n, k, NN)
+        if ws2 > ws.numel():
+            continue
+        f = lambda: P.oz2_dgemm("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0, C.data_ptr(), m, NN)
+        f()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(3):
+            f()
+        e1.record()
+        torch.cuda.synchronize()
+        msN = e0.elapsed_time(e1) / 3
+        sweep[str(NN)] = {"tflops": round(flops_rank / (msN * 1e-3) / 1e12, 3), **errs(C[I][:, J].cpu().numpy())}
+    acc["moduli_sweep"] = sweep
+    extras["accuracy"] = acc
+
+    # ---- e2e: host (pinned) buffers through the same C ABI
+    Ahost = torch.empty((k, m), dtype=torch.float64, pin_memory=True).t()
+    Bhost = torch.empty((n, k), dtype=torch.float64, pin_memory=True).t()
+    Chost = torch.empty((n, m), dtype=torch.float64, pin_memory=True).t()
+    Ahost.copy_(A)
+    Bhost.copy_(B)
+    P.oz2_dgemm("N", "N", m, n, k, 1.0, Ahost.data_ptr(), m, Bhost.data_ptr(), k, 0.0, Chost.data_ptr(), m, N)
+    ereps = 3
+    t0 = time.perf_counter()
+    for _ in range(ereps):
+        rc = P.oz2_dgemm("N", "N", m, n, k, 1.0, Ahost.data_ptr(), m, Bhost.data_ptr(), k, 0.0,
+                         Chost.data_ptr(), m, N)
+        assert rc == 0
+    e2e_s = (time.perf_counter() - t0) / ereps
+    extras["e2e"] = {"value": round(flops_rank / e2e_s / 1e12, 3), "unit": UNIT,
+                     "h2d_bytes_per_step": 8 * (m * k + k * n), "d2h_bytes_per_step": 8 * m * n,
+                     "ms_per_step": round(e2e_s * 1e3, 3), "buffers": "pinned host"}
+    del Ahost, Bhost, Chost
+    return out, extras
+
+
+def cpu_baseline(args, sample_rows=16, seed_off=0):
+    """The oracle as it stands, on a bounded sub-block of the same workload: the full
+    pipeline on an (s x k) x (k x s) block of the m=n=k problem (per-block scaling,
+    i.e. the paper's blocked call)."""
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+    from oracle import scheme
+    from synth import gen_host
+    s = sample_rows
+    k = args.n
+    A = gen_host(s, k, "phi", phi=args.phi, seed=50 + seed_off)
+    B = gen_host(k, s, "phi", phi=args.phi, seed=60 + seed_off)
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        scheme.dgemm(A, B, args.moduli)
+        dt = time.perf_counter() - t0
+    return {"value": 2.0 * s * s * k / dt / 1e12, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{s} x {k} x {s} sub-block, N={args.moduli} (full oracle pipeline, exact ints/Fractions)",
+            "seconds": round(dt, 3)}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    for w in range(args.warmup):
+        cpu_baseline(args, sample_rows=2, seed_off=w)
+    vals = []
+    t0 = time.perf_counter()
+    for s_ in range(args.steps):
+        vals.append(cpu_baseline(args, sample_rows=2, seed_off=100 + s_))
+    total = time.perf_counter() - t0
+    flops = sum(2.0 * 2 * 2 * args.n for _ in vals)
+    value = flops / total / 1e12
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"config3 sub-blocks: 2 x {args.n} x 2 per step, N={args.moduli}, phi={args.phi}"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"2 x {args.n} x 2 sub-block per step (full oracle pipeline)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out, extras = run_oz2(args, rank, world, local_rank)
+    if rank == 0:
+        if extras:
+            out["e2e"] = extras.pop("e2e")
+            out.update(extras)
+        if world == 1 and not args.no_extras:
+            out["cpu_baseline"] = cpu_baseline(args)
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,187 @@
+/*
+ * oz2.h -- C ABI of liboz2.so: FP64 GEMM emulated with the Ozaki-II scheme on the
+ * FP8 (E4M3 in, FP32 accumulate) tensor cores of an NVIDIA B200 (sm_100a).
+ *
+ * Method: Uchino, Ozaki, Imamura, "Double-Precision Matrix Multiplication Emulation
+ * via Ozaki-II Scheme with FP8 Quantization" (arxiv 2603.10634).  Citations "P:n"
+ * are line numbers of that paper's LaTeX source; "Rn" are the readings
+ * of silent or ambiguous passages listed in DESIGN.md.
+ *
+ * Every entry point is extern "C", takes plain pointers and sizes, and returns an
+ * int status (0 = success, -i = argument i invalid in BLAS xerbla order, >0 =
+ * OZ2_ERR_* runtime failure) unless stated otherwise.  No C++ or torch types cross
+ * this boundary.
+ */
+#ifndef OZ2_H
+#define OZ2_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------------ */
+#define OZ2_SUCCESS            0
+#define OZ2_ERR_CUDA           1   /* a CUDA runtime call or kernel launch failed     */
+#define OZ2_ERR_ALLOC          2   /* device or pinned host allocation failed         */
+#define OZ2_ERR_WORKSPACE      3   /* caller-provided workspace smaller than needed   */
+#define OZ2_ERR_NOT_SUPPORTED  4   /* k > 65536, or no sm_100 device          */
+#define OZ2_ERR_NONFINITE      5   /* oz2_get_status(): A or B held NaN/Inf           */
+
+/* ---- the primary call -------------------------------------------------------- */
+
+/*
+ * C <- alpha * op(A) op(B) + beta * C, op(A) m x k, op(B) k x n, all FP64,
+ * column-major BLAS/cuBLAS conventions (reading R11: the paper states the problem
+ * as C ~ AB; alpha, beta, trans and ld follow DGEMM).
+ *
+ *   transa, transb  'N'/'n' (op(X) = X), 'T'/'t'/'C'/'c' (op(X) = X^T).
+ *   m, n, k         >= 0.  k <= 65536 (the paper's exactness assumption k <= 2^16,
+ *                   P:208 and eq. error-free-FP8-matmult); larger k
+ *                   returns OZ2_ERR_NOT_SUPPORTED.
+ *   A, lda          A is m x k (transa 'N', lda >= max(1,m)) or k x m (lda >= max(1,k)).
+ *   B, ldb          B is k x n (transb 'N', ldb >= max(1,k)) or n x k (ldb >= max(1,n)).
+ *   C, ldc          m x n, ldc >= max(1,m).  Read only when beta != 0.
+ *   num_moduli      N in [2, 33]: the first N moduli of the hybrid set
+ *                   {1089, 1024, 961, 841, 625, 529, 511, 509, ...} (eq. p_list_hybrid,
+ *                   P:306-316; P:526 assumes N < 34).  N = 12 is the paper's FP64
+ *                   configuration; N = 13 gives FP64-BLAS-level
+ *                   error at k = 16384.
+ *
+ * Pointers may be DEVICE memory (the fast path: everything is enqueued on the
+ * library's current stream, see oz2_set_stream, asynchronously; the caller keeps
+ * A, B, C alive until the stream work completes) or HOST memory (pageable or
+ * pinned; detected with cudaPointerGetAttributes): then A and B are copied to
+ * device staging buffers, the same device pipeline runs, C is copied back, and the
+ * call returns only after the stream has been synchronised.  All of A, B, C must be
+ * of the same kind.
+ *
+ * Algorithm (accurate mode; workflow P:501-524), all on the device:
+ *   1. mu'_i = 2^7/ufp(max_h |a_ih|), A-bar = RU_fp8(|diag(mu') A|); same for B   (eq. def:mu'nu')
+ *   2. C-bar' = A-bar B-bar on FP8 tensor cores; keep row/column maxima
+ *   3. log2 mu_i = log2 mu'_i + int(P' + delta log2 max_j c-bar_ij)               (eq. mu-computation)
+ *   4. A' = trunc(diag(mu) A), residues mod p_l, FP8 digit split
+ *   5. 3 exact FP8 GEMMs per modulus, reduced mod p_l in the epilogue             (eqs. 3matmult-notKaratsuba, C'-Karatsuba)
+ *   6. C' = mod(sum_l q_l P/p_l C'_l, P) and C = diag(mu)^-1 C' diag(nu)^-1        (eqs. CRT_finalreduction, inversescaling)
+ *
+ * Quick returns (BLAS): m == 0 or n == 0: nothing.  alpha == 0 or k == 0:
+ * C <- beta C (C not read when beta == 0).
+ * Non-finite entries in A or B: the call still returns 0 (no host sync on the fast
+ * path); the device status word is set and oz2_get_status() reports
+ * OZ2_ERR_NONFINITE (reading R12).
+ */
+int oz2_dgemm(char transa, char transb, int64_t m, int64_t n, int64_t k,
+              double alpha, const double* A, int64_t lda,
+              const double* B, int64_t ldb,
+              double beta, double* C, int64_t ldc, int num_moduli);
+
+/* ---- extended call: debug outputs and imported exponents ---------------------- */
+
+/*
+ * Every pointer field is optional (NULL = not wanted / not given) and must be
+ * DEVICE memory.  Outputs are written after the corresponding stage, in the layouts
+ * stated; sizes are the caller's responsibility.  Integer exponents are log2 of the
+ * power-of-two scaling factors (the paper stores them as INT16; we use int32).
+ */
+typedef struct oz2_options {
+    /* outputs */
+    int32_t* e_prime_a;     /* [m]  log2 mu'_i                 (eq. def:mu'nu')          */
+    int32_t* e_prime_b;     /* [n]  log2 nu'_j                                            */
+    uint8_t* abar;          /* [m][k] row-major E4M3 codes of A-bar (K contiguous)        */
+    uint8_t* bbar;          /* [n][k] row-major E4M3 codes of B-bar^T (K contiguous)      */
+    float*   rmax;          /* [m]  R_i = max_j C-bar'_ij                    */
+    float*   smax;          /* [n]  S_j = max_i C-bar'_ij                    */
+    int32_t* e_mu;          /* [m]  log2 mu_i                  (eq. mu-computation)       */
+    int32_t* e_nu;          /* [n]  log2 nu_j                  (eq. nu-computation)       */
+    uint8_t* digits_a;      /* [M_N][m][k] E4M3 digit planes of A, plane order: per
+                               modulus l, x = 1..2 (square) or 1..3 (non-square)          */
+    uint8_t* digits_b;      /* [M_N][n][k] same for B^T                                  */
+    int16_t* residues;      /* [N][n][m] C'_l (i fastest), symmetric range (R2)          */
+    /* inputs */
+    const int32_t* e_mu_in; /* [m]  if non-NULL together with e_nu_in: use these scaling */
+    const int32_t* e_nu_in; /* [n]  exponents and skip steps 1-3             */
+    int32_t reserved[8];    /* must be zero                                               */
+} oz2_options;
+
+int oz2_dgemm_ex(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                 double alpha, const double* A, int64_t lda,
+                 const double* B, int64_t ldb,
+                 double beta, double* C, int64_t ldc, int num_moduli,
+                 const oz2_options* opt);
+
+/* ---- runtime state (per host thread) ------------------------------------------ */
+
+/* Stream for subsequent calls from this host thread (cudaStream_t passed as void*;
+ * NULL = legacy default stream). */
+int oz2_set_stream(void* stream);
+
+/* Bytes of device workspace a call with these arguments needs (0 on invalid args). */
+size_t oz2_workspace_size(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                          int num_moduli);
+
+/* Caller-owned device workspace for subsequent calls from this host thread; the
+ * library keeps the pointer (not ownership) until replaced.  ptr == NULL reverts to
+ * a library-owned buffer that grows on demand.  Must stay valid until all work
+ * enqueued with it has completed. */
+int oz2_set_workspace(void* ptr, size_t bytes);
+
+/* Synchronises the current stream, returns the device status word of the last call
+ * on it (OZ2_SUCCESS or OZ2_ERR_NONFINITE) in *status and clears it. */
+int oz2_get_status(int32_t* status);
+
+/* Phase timers (CUDA events on the call's stream).  enable != 0 makes subsequent
+ * device-path calls of this host thread record events at the phase boundaries;
+ * oz2_get_timing synchronises on the last call's final event and writes up to n
+ * floats (ms): [0] prescale (row maxima + A-bar/B-bar cast), [1] bound GEMM,
+ * [2] scaling exponents, [3] residue/digit split, [4] residue GEMMs with the
+ * modular epilogue (the paper's "gemms" + "requant"), [5] CRT + inverse
+ * scaling ("dequant"), [6] total.  Returns OZ2_ERR_NOT_SUPPORTED if the last
+ * call recorded no timing. */
+int oz2_set_timing(int enable);
+int oz2_get_timing(float* ms_out, int n);
+
+/* Frees library-owned buffers and cached plans of this host thread. */
+int oz2_finalize(void);
+
+/* ---- host-only queries (no device needed) -------------------------------------- */
+
+/* The first num_moduli hybrid moduli (eq. p_list_hybrid). */
+int oz2_moduli(int num_moduli, int32_t* p_out);
+
+/* Constants of the plan for (num_moduli, k), for tests and reports. */
+typedef struct oz2_plan_info {
+    int32_t num_moduli;
+    int32_t num_planes;        /* M_N (eq. M)                                   */
+    int32_t num_limbs;         /* 32-bit limbs of the CRT integer arithmetic               */
+    int32_t num_squares;       /* square moduli among the first N (<= 6)                   */
+    float   p_prime;           /* P' = RD32((log2(P-1) - 1)/2)           */
+    float   delta;             /* delta = RD32(-1/(2 - 2^-21))           */
+    float   f_k;               /* RU32(1/(1 - k 2^-23)), reading R5  (eq. barCupper)       */
+    double  log2_P;            /* log2 P                                                   */
+    uint32_t P_limbs[12];      /* P, little-endian 32-bit limbs (num_limbs used)           */
+    uint32_t w_limbs[33][12];  /* w_l = q_l P/p_l (eq. CRT_finalreduction)                 */
+} oz2_plan_info;
+
+int oz2_plan_query(int num_moduli, int64_t k, oz2_plan_info* out);
+
+/* "oz2 <version> sm_100a" */
+const char* oz2_version(void);
+
+/* ---- diagnostics ---------------------------------------------------------------- */
+
+/*
+ * Raw FP8 GEMM on the same tcgen05 kernel: C32[i][j] = sum_h a[i][h] b[j][h] with
+ * E4M3 inputs and the tensor core's FP32 accumulation, for probing the
+ * exactness window (eq. error-free-FP8-matmult) and the bound-GEMM rounding (R5).
+ * a: [m][k] and b: [n][k] row-major E4M3 codes, device memory, k a multiple of 16;
+ * C32: [m][n] row-major float, device memory.  Enqueued on the current stream.
+ */
+int oz2_fp8_gemm_raw(const uint8_t* a, const uint8_t* b, float* C32,
+                     int64_t m, int64_t n, int64_t k);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OZ2_H */

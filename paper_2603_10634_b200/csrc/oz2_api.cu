@@ -1,0 +1,680 @@
+// oz2_api.cu -- the C ABI (include/oz2.h): argument checking, the host planner
+// (moduli, CRT constants, P', delta, f_k), workspace carving, TMA descriptors and the
+// launch sequence of the FP8 Ozaki-II pipeline.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "../../include/oz2.h"
+#include "oz2_internal.h"
+
+namespace oz2 {
+
+// =================================================================================
+// host planner: hybrid moduli (eq. p_list_hybrid) and CRT constants
+// (eq. CRT_finalreduction) with a small fixed-purpose bigint.
+
+using Big = std::vector<uint32_t>;   // little-endian 32-bit limbs
+
+static void big_trim(Big& a) { while (a.size() > 1 && a.back() == 0) a.pop_back(); }
+static void big_mul_small(Big& a, uint32_t s) {
+    uint64_t c = 0;
+    for (auto& x : a) { const uint64_t v = static_cast<uint64_t>(x) * s + c; x = static_cast<uint32_t>(v); c = v >> 32; }
+    if (c) a.push_back(static_cast<uint32_t>(c));
+}
+static uint32_t big_divmod_small(Big& a, uint32_t s) {
+    uint64_t r = 0;
+    for (size_t i = a.size(); i-- > 0;) {
+        const uint64_t cur = (r << 32) | a[i];
+        a[i] = static_cast<uint32_t>(cur / s);
+        r = cur % s;
+    }
+    big_trim(a);
+    return static_cast<uint32_t>(r);
+}
+static int big_bitlen(const Big& a) {
+    for (size_t i = a.size(); i-- > 0;)
+        if (a[i]) return static_cast<int>(i) * 32 + (32 - __builtin_clz(a[i]));
+    return 0;
+}
+static uint64_t big_top64(const Big& a, int& shift) {   // a ~= top * 2^shift, top < 2^64
+    const int nb = big_bitlen(a);
+    shift = nb > 64 ? nb - 64 : 0;
+    uint64_t top = 0;
+    for (int b = 63; b >= 0; --b) {
+        const int bit = shift + b;
+        if (bit >= nb) continue;
+        if ((a[bit >> 5] >> (bit & 31)) & 1u) top |= (1ull << b);
+    }
+    return top;
+}
+static int64_t inv_mod(int64_t a, int64_t p) {   // a^-1 mod p, gcd(a,p) = 1
+    int64_t t = 0, nt = 1, r = p, nr = a % p;
+    while (nr) { const int64_t q = r / nr; int64_t tmp = t - q * nt; t = nt; nt = tmp; tmp = r - q * nr; r = nr; nr = tmp; }
+    return t < 0 ? t + p : t;
+}
+static int gcd_i(int a, int b) { while (b) { const int t = a % b; a = b; b = t; } return a; }
+
+static std::vector<int> hybrid_moduli(int N) {
+    // squares s^2 > 513 (s <= 33) pairwise coprime, then greedy coprime from 513 down
+    std::vector<int> out;
+    for (int s = 33; s >= 2 && static_cast<int>(out.size()) < N; --s) {
+        const int p = s * s;
+        if (p <= 513) break;
+        bool ok = true;
+        for (int q : out) ok = ok && gcd_i(p, q) == 1;
+        if (ok) out.push_back(p);
+    }
+    for (int c = 513; c >= 2 && static_cast<int>(out.size()) < N; --c) {
+        bool ok = true;
+        for (int q : out) ok = ok && gcd_i(c, q) == 1;
+        if (ok) out.push_back(c);
+    }
+    return out;
+}
+static bool is_square_i(int p) { const int s = static_cast<int>(std::lround(std::sqrt(static_cast<double>(p)))); return s * s == p; }
+
+static float rd32(long double x) {
+    float f = static_cast<float>(x);
+    if (static_cast<long double>(f) > x) f = std::nextafterf(f, -INFINITY);
+    return f;
+}
+static float ru32(long double x) {
+    float f = static_cast<float>(x);
+    if (static_cast<long double>(f) < x) f = std::nextafterf(f, INFINITY);
+    return f;
+}
+
+struct Plan {
+    int N = 0, nsq = 0, M = 0, L = 0;
+    std::vector<int> p;
+    float p_prime = 0, delta = 0;
+    double log2P = 0;
+    CrtParams crt{};
+    DigitParams dig{};
+    GemmParams gemm_mod{};            // only .mod[] filled
+    std::vector<uint16_t> pow2tab;    // [N][kPow2Tab]
+    uint16_t* d_pow2tab = nullptr;    // device copy (per thread)
+    Big P;
+    std::vector<Big> w;
+};
+
+static Plan build_plan(int N) {
+    Plan pl;
+    pl.N = N;
+    pl.p = hybrid_moduli(N);
+    for (int p : pl.p) pl.nsq += is_square_i(p) ? 1 : 0;
+    pl.M = 2 * pl.nsq + 3 * (N - pl.nsq);
+    Big P{1};
+    for (int p : pl.p) big_mul_small(P, static_cast<uint32_t>(p));
+    pl.P = P;
+    const int nb = big_bitlen(P);
+    pl.L = (nb + 1 + 31) / 32;
+    // P' = RD32((log2(P-1) - 1)/2)
+    Big Pm1 = P;
+    for (auto& x : Pm1) { if (x--) break; }    // P - 1 (P > 0)
+    big_trim(Pm1);
+    int sh = 0;
+    const uint64_t top = big_top64(Pm1, sh);
+    const long double lg = static_cast<long double>(sh) + log2l(static_cast<long double>(top));
+    pl.p_prime = rd32((lg - 1.0L) / 2.0L);
+    pl.delta = rd32(-1.0L / (2.0L - ldexpl(1.0L, -21)));
+    int shP = 0;
+    const uint64_t topP = big_top64(P, shP);
+    pl.log2P = static_cast<double>(static_cast<long double>(shP) + log2l(static_cast<long double>(topP)));
+    // CRT constants
+    CrtParams& cp = pl.crt;
+    std::memset(&cp, 0, sizeof(cp));
+    cp.num_moduli = N;
+    for (int l = 0; l < N; ++l) {
+        const int p = pl.p[l];
+        Big Pp = P;
+        big_divmod_small(Pp, static_cast<uint32_t>(p));
+        Big tmp = Pp;
+        const uint32_t rem = big_divmod_small(tmp, static_cast<uint32_t>(p));
+        const int64_t q = inv_mod(rem, p);
+        Big w = Pp;
+        big_mul_small(w, static_cast<uint32_t>(q));
+        pl.w.push_back(w);
+        cp.p[l] = p;
+        cp.qp[l] = static_cast<double>(q) / static_cast<double>(p);
+        for (int t = 0; t < pl.L && t < static_cast<int>(w.size()); ++t) cp.w[l][t] = w[t];
+    }
+    for (int t = 0; t < pl.L && t < static_cast<int>(P.size()); ++t) cp.P[t] = P[t];
+    {   // np = 2^(32L) - P, halfP = P/2
+        uint64_t c = 1;
+        for (int t = 0; t < pl.L; ++t) {
+            const uint64_t s = static_cast<uint64_t>(~cp.P[t]) + c;
+            cp.np[t] = static_cast<uint32_t>(s);
+            c = s >> 32;
+        }
+        for (int t = 0; t < pl.L; ++t) {
+            const uint32_t hi = (t + 1 < pl.L) ? cp.P[t + 1] : 0u;
+            cp.halfP[t] = (cp.P[t] >> 1) | (hi << 31);
+        }
+    }
+    // digit split and epilogue constants
+    DigitParams& dp = pl.dig;
+    std::memset(&dp, 0, sizeof(dp));
+    dp.num_moduli = N;
+    dp.num_planes = pl.M;
+    int plane = 0;
+    for (int l = 0; l < N; ++l) {
+        const int p = pl.p[l];
+        ModDig& md = dp.mod[l];
+        md.p_d = p;
+        md.pinv_d = 1.0 / p;
+        md.p_f = static_cast<float>(p);
+        md.pinv_f = 1.0f / static_cast<float>(p);
+        md.square = is_square_i(p) ? 1 : 0;
+        const int s = md.square ? static_cast<int>(std::lround(std::sqrt(static_cast<double>(p)))) : 16;
+        md.s_f = static_cast<float>(s);
+        md.inv_s_f = 1.0f / static_cast<float>(s);
+        md.plane0 = plane;
+        ModEpi& me = pl.gemm_mod.mod[l];
+        me.p = static_cast<float>(p);
+        me.pinv = 1.0f / static_cast<float>(p);
+        if (md.square) {
+            // C'_l = mod(s A1 B2 + s A2 B1 + A2 B2, p)  (eq. 3matmult-notKaratsuba)
+            me.coef[0] = static_cast<float>(s); me.a_plane[0] = plane + 0; me.b_plane[0] = plane + 1;
+            me.coef[1] = static_cast<float>(s); me.a_plane[1] = plane + 1; me.b_plane[1] = plane + 0;
+            me.coef[2] = 1.0f;                  me.a_plane[2] = plane + 1; me.b_plane[2] = plane + 1;
+            plane += 2;
+        } else {
+            // A'B' = 256 C1 + C2 + 16 (C3 - C1 - C2)  (eq. C'-Karatsuba)
+            me.coef[0] = 240.0f; me.a_plane[0] = plane + 0; me.b_plane[0] = plane + 0;
+            me.coef[1] = -15.0f; me.a_plane[1] = plane + 1; me.b_plane[1] = plane + 1;
+            me.coef[2] = 16.0f;  me.a_plane[2] = plane + 2; me.b_plane[2] = plane + 2;
+            plane += 3;
+        }
+    }
+    pl.pow2tab.resize(static_cast<size_t>(N) * kPow2Tab);
+    for (int l = 0; l < N; ++l) {
+        uint32_t v = 1 % pl.p[l];
+        for (int e = 0; e < kPow2Tab; ++e) {
+            pl.pow2tab[static_cast<size_t>(l) * kPow2Tab + e] = static_cast<uint16_t>(v);
+            v = (v * 2) % static_cast<uint32_t>(pl.p[l]);
+        }
+    }
+    return pl;
+}
+
+static float f_k_of(int64_t k) {   // reading R5: RU32(1/(1 - k 2^-23))
+    return ru32(1.0L / (1.0L - static_cast<long double>(k) * ldexpl(1.0L, -23)));
+}
+
+// =================================================================================
+// per-thread runtime state
+
+struct ThreadState {
+    cudaStream_t stream = nullptr;
+    void* user_ws = nullptr;
+    size_t user_ws_bytes = 0;
+    void* own_ws = nullptr;
+    size_t own_ws_bytes = 0;
+    void* staging = nullptr;
+    size_t staging_bytes = 0;
+    int32_t* d_status = nullptr;
+    int device = -1;
+    int num_sms = 0;
+    std::map<int, std::unique_ptr<Plan>> plans;
+    bool timing = false;
+    bool timed_last = false;
+    cudaEvent_t ev[8] = {};
+    ~ThreadState() {}
+};
+static thread_local ThreadState g_ts;
+
+static std::mutex g_plan_mutex;
+static std::map<int, std::unique_ptr<Plan>> g_host_plans;   // host-only queries
+
+static const Plan& host_plan(int N) {
+    std::lock_guard<std::mutex> lk(g_plan_mutex);
+    auto it = g_host_plans.find(N);
+    if (it == g_host_plans.end()) it = g_host_plans.emplace(N, std::make_unique<Plan>(build_plan(N))).first;
+    return *it->second;
+}
+
+static int ensure_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return OZ2_ERR_CUDA;
+    if (g_ts.device != dev) {
+        int major = 0;
+        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return OZ2_ERR_CUDA;
+        if (major != 10) return OZ2_ERR_NOT_SUPPORTED;
+        if (cudaDeviceGetAttribute(&g_ts.num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return OZ2_ERR_CUDA;
+        g_ts.device = dev;
+        g_ts.plans.clear();
+        g_ts.d_status = nullptr;
+    }
+    if (!g_ts.d_status) {
+        if (cudaMalloc(&g_ts.d_status, sizeof(int32_t)) != cudaSuccess) return OZ2_ERR_ALLOC;
+        if (cudaMemset(g_ts.d_status, 0, sizeof(int32_t)) != cudaSuccess) return OZ2_ERR_CUDA;
+    }
+    return OZ2_SUCCESS;
+}
+
+static Plan* device_plan(int N, int* err) {
+    auto it = g_ts.plans.find(N);
+    if (it != g_ts.plans.end()) return it->second.get();
+    auto pl = std::make_unique<Plan>(build_plan(N));
+    const size_t bytes = pl->pow2tab.size() * sizeof(uint16_t);
+    if (cudaMalloc(&pl->d_pow2tab, bytes) != cudaSuccess) { *err = OZ2_ERR_ALLOC; return nullptr; }
+    if (cudaMemcpy(pl->d_pow2tab, pl->pow2tab.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+        *err = OZ2_ERR_CUDA;
+        return nullptr;
+    }
+    pl->dig.pow2tab = pl->d_pow2tab;
+    Plan* raw = pl.get();
+    g_ts.plans.emplace(N, std::move(pl));
+    return raw;
+}
+
+// =================================================================================
+// workspace layout
+
+static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+static inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+struct Layout {
+    int64_t m_pad, n_pad, k_pad;
+    int M;
+    size_t maxbits, eprime, rsmax, eexp, digA, digB, res, total;
+};
+
+static Layout make_layout(int64_t m, int64_t n, int64_t k, int N, int M) {
+    Layout L{};
+    L.m_pad = round_up(m, PAD_M);
+    L.n_pad = round_up(n, PAD_N);
+    L.k_pad = round_up(k, PAD_K);
+    L.M = M;
+    size_t off = 0;
+    const size_t mn = static_cast<size_t>(m + n);
+    L.maxbits = off; off = align_up(off + 8 * mn, 256);
+    L.eprime = off;  off = align_up(off + 4 * mn, 256);
+    L.rsmax = off;   off = align_up(off + 4 * mn, 256);
+    L.eexp = off;    off = align_up(off + 4 * mn, 256);
+    L.digA = off;    off = align_up(off + static_cast<size_t>(M) * L.m_pad * L.k_pad, 1024);
+    L.digB = off;    off = align_up(off + static_cast<size_t>(M) * L.n_pad * L.k_pad, 1024);
+    L.res = off;     off = align_up(off + 2ull * N * static_cast<size_t>(m) * static_cast<size_t>(n), 256);
+    L.total = off;
+    return L;
+}
+
+// =================================================================================
+// TMA descriptors (driver entry point fetched through the runtime; no -lcuda)
+
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                      const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                      const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                      CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled_t encode_fn() {
+    static PFN_encodeTiled_t fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+    }
+    return fn;
+}
+
+// 2D byte tensor [outer][inner] with row pitch `pitch` bytes, box inner x outer, 128B swizzle
+static bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                     uint64_t pitch, uint32_t box_inner, uint32_t box_outer) {
+    PFN_encodeTiled_t fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {pitch};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t es[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static void phase_mark(int i) {
+    if (!g_ts.timing) return;
+    if (!g_ts.ev[i]) cudaEventCreate(&g_ts.ev[i]);
+    cudaEventRecord(g_ts.ev[i], g_ts.stream);
+}
+
+#define OZ2_CK(x)                                   \
+    do {                                            \
+        if ((x) != cudaSuccess) return OZ2_ERR_CUDA; \
+    } while (0)
+
+// =================================================================================
+// the pipeline on device pointers
+
+static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_t k, double alpha,
+                      const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                      double* C, int64_t ldc, int N, const oz2_options* opt) {
+    cudaStream_t st = g_ts.stream;
+    int err = OZ2_SUCCESS;
+    Plan* pl = device_plan(N, &err);
+    if (!pl) return err;
+    const Layout L = make_layout(m, n, k, N, pl->M);
+    uint8_t* ws = nullptr;
+    if (g_ts.user_ws) {
+        if (g_ts.user_ws_bytes < L.total) return OZ2_ERR_WORKSPACE;
+        ws = static_cast<uint8_t*>(g_ts.user_ws);
+    } else {
+        if (g_ts.own_ws_bytes < L.total) {
+            if (g_ts.own_ws) { cudaStreamSynchronize(st); cudaFree(g_ts.own_ws); g_ts.own_ws = nullptr; g_ts.own_ws_bytes = 0; }
+            if (cudaMalloc(&g_ts.own_ws, L.total) != cudaSuccess) return OZ2_ERR_ALLOC;
+            g_ts.own_ws_bytes = L.total;
+        }
+        ws = static_cast<uint8_t*>(g_ts.own_ws);
+    }
+    auto* maxbits = reinterpret_cast<unsigned long long*>(ws + L.maxbits);
+    auto* eprime = reinterpret_cast<int32_t*>(ws + L.eprime);
+    auto* rsmax = reinterpret_cast<uint32_t*>(ws + L.rsmax);
+    auto* eexp = reinterpret_cast<int32_t*>(ws + L.eexp);
+    uint8_t* digA = ws + L.digA;
+    uint8_t* digB = ws + L.digB;
+    auto* res = reinterpret_cast<int16_t*>(ws + L.res);
+    uint8_t* abar = digA;      // A-bar / B-bar live in the first digit plane until step 4
+    uint8_t* bbar = digB;
+    int32_t* e_mu = eexp;
+    int32_t* e_nu = eexp + m;
+
+    const bool imported = opt && opt->e_mu_in && opt->e_nu_in;
+    g_ts.timed_last = false;
+    phase_mark(0);
+    OZ2_CK(cudaMemsetAsync(g_ts.d_status, 0, sizeof(int32_t), st));
+    if (!imported) {
+        // ---- step 1: prescale (eq. def:mu'nu')
+        OZ2_CK(cudaMemsetAsync(maxbits, 0, 8 * static_cast<size_t>(m + n), st));
+        OZ2_CK(cudaMemsetAsync(rsmax, 0, 4 * static_cast<size_t>(m + n), st));
+        OZ2_CK(launch_rowmax(A, m, k, lda, a_kmajor, maxbits, st));
+        OZ2_CK(launch_rowmax(B, n, k, ldb, b_kmajor, maxbits + m, st));
+        OZ2_CK(launch_cast(A, m, k, lda, a_kmajor, maxbits, eprime, abar, L.m_pad, L.k_pad, g_ts.d_status, st));
+        OZ2_CK(launch_cast(B, n, k, ldb, b_kmajor, maxbits + m, eprime + m, bbar, L.n_pad, L.k_pad, g_ts.d_status, st));
+        if (opt && opt->e_prime_a) OZ2_CK(cudaMemcpyAsync(opt->e_prime_a, eprime, 4 * m, cudaMemcpyDeviceToDevice, st));
+        if (opt && opt->e_prime_b) OZ2_CK(cudaMemcpyAsync(opt->e_prime_b, eprime + m, 4 * n, cudaMemcpyDeviceToDevice, st));
+        if (opt && opt->abar && k)
+            OZ2_CK(cudaMemcpy2DAsync(opt->abar, k, abar, L.k_pad, k, m, cudaMemcpyDeviceToDevice, st));
+        if (opt && opt->bbar && k)
+            OZ2_CK(cudaMemcpy2DAsync(opt->bbar, k, bbar, L.k_pad, k, n, cudaMemcpyDeviceToDevice, st));
+        // ---- step 2: bound GEMM C-bar' = A-bar B-bar, row/column maxima
+        phase_mark(1);
+        {
+            CUtensorMap ta, tb;
+            if (!make_map(&ta, abar, L.k_pad, L.m_pad, L.k_pad, BK, BM)) return OZ2_ERR_CUDA;
+            if (!make_map(&tb, bbar, L.k_pad, L.n_pad, L.k_pad, BK, BN)) return OZ2_ERR_CUDA;
+            GemmParams gp;
+            std::memset(&gp, 0, sizeof(gp));
+            gp.m = static_cast<int>(m); gp.n = static_cast<int>(n);
+            gp.num_k_blocks = static_cast<int>(L.k_pad / BK);
+            gp.m_tiles = static_cast<int>(L.m_pad / BM); gp.n_tiles = static_cast<int>(L.n_pad / BN);
+            gp.rows_per_plane_a = static_cast<int>(L.m_pad); gp.rows_per_plane_b = static_cast<int>(L.n_pad);
+            gp.rmax = rsmax; gp.smax = rsmax + m;
+            OZ2_CK(launch_gemm(MODE_BOUND, ta, tb, gp, g_ts.num_sms, st));
+        }
+        if (opt && opt->rmax) OZ2_CK(cudaMemcpyAsync(opt->rmax, rsmax, 4 * m, cudaMemcpyDeviceToDevice, st));
+        if (opt && opt->smax) OZ2_CK(cudaMemcpyAsync(opt->smax, rsmax + m, 4 * n, cudaMemcpyDeviceToDevice, st));
+        // ---- step 3: scaling exponents (eq. mu-computation / nu-computation)
+        phase_mark(2);
+        ExpParams ep{pl->p_prime, pl->delta, f_k_of(k)};
+        OZ2_CK(launch_exps(maxbits, eprime, rsmax, m + n, ep, eexp, st));
+    } else {
+        phase_mark(1);
+        phase_mark(2);
+        OZ2_CK(cudaMemcpyAsync(e_mu, opt->e_mu_in, 4 * m, cudaMemcpyDeviceToDevice, st));
+        OZ2_CK(cudaMemcpyAsync(e_nu, opt->e_nu_in, 4 * n, cudaMemcpyDeviceToDevice, st));
+    }
+    if (opt && opt->e_mu) OZ2_CK(cudaMemcpyAsync(opt->e_mu, e_mu, 4 * m, cudaMemcpyDeviceToDevice, st));
+    if (opt && opt->e_nu) OZ2_CK(cudaMemcpyAsync(opt->e_nu, e_nu, 4 * n, cudaMemcpyDeviceToDevice, st));
+
+    // ---- step 4: integers, residues, FP8 digits
+    phase_mark(3);
+    OZ2_CK(launch_digits(A, m, k, lda, a_kmajor, e_mu, pl->dig, digA, L.m_pad, L.k_pad, st));
+    OZ2_CK(launch_digits(B, n, k, ldb, b_kmajor, e_nu, pl->dig, digB, L.n_pad, L.k_pad, st));
+    if (opt && opt->digits_a && k)
+        for (int x = 0; x < pl->M; ++x)
+            OZ2_CK(cudaMemcpy2DAsync(opt->digits_a + static_cast<size_t>(x) * m * k, k,
+                                     digA + static_cast<size_t>(x) * L.m_pad * L.k_pad, L.k_pad, k, m,
+                                     cudaMemcpyDeviceToDevice, st));
+    if (opt && opt->digits_b && k)
+        for (int x = 0; x < pl->M; ++x)
+            OZ2_CK(cudaMemcpy2DAsync(opt->digits_b + static_cast<size_t>(x) * n * k, k,
+                                     digB + static_cast<size_t>(x) * L.n_pad * L.k_pad, L.k_pad, k, n,
+                                     cudaMemcpyDeviceToDevice, st));
+    // ---- step 5: 3N exact FP8 GEMMs with the modular epilogue
+    phase_mark(4);
+    {
+        CUtensorMap ta, tb;
+        if (!make_map(&ta, digA, L.k_pad, static_cast<uint64_t>(pl->M) * L.m_pad, L.k_pad, BK, BM)) return OZ2_ERR_CUDA;
+        if (!make_map(&tb, digB, L.k_pad, static_cast<uint64_t>(pl->M) * L.n_pad, L.k_pad, BK, BN)) return OZ2_ERR_CUDA;
+        GemmParams gp = pl->gemm_mod;
+        gp.m = static_cast<int>(m); gp.n = static_cast<int>(n);
+        gp.num_k_blocks = static_cast<int>(L.k_pad / BK);
+        gp.m_tiles = static_cast<int>(L.m_pad / BM); gp.n_tiles = static_cast<int>(L.n_pad / BN);
+        gp.rows_per_plane_a = static_cast<int>(L.m_pad); gp.rows_per_plane_b = static_cast<int>(L.n_pad);
+        gp.num_moduli = N;
+        gp.residues = res;
+        OZ2_CK(launch_gemm(MODE_RESIDUE, ta, tb, gp, g_ts.num_sms, st));
+    }
+    if (opt && opt->residues)
+        OZ2_CK(cudaMemcpyAsync(opt->residues, res, 2ull * N * m * n, cudaMemcpyDeviceToDevice, st));
+    // ---- step 6: CRT + inverse scaling (eqs. CRT_finalreduction, inversescaling)
+    phase_mark(5);
+    OZ2_CK(launch_crt(pl->L, res, m, n, pl->crt, e_mu, e_nu, alpha, beta, C, ldc, st));
+    phase_mark(6);
+    g_ts.timed_last = g_ts.timing;
+    return OZ2_SUCCESS;
+}
+
+static bool is_device_ptr(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+static bool trans_ok(char t) {
+    return t == 'N' || t == 'n' || t == 'T' || t == 't' || t == 'C' || t == 'c';
+}
+static bool is_n(char t) { return t == 'N' || t == 'n'; }
+
+int dgemm_impl(char transa, char transb, int64_t m, int64_t n, int64_t k, double alpha,
+               const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+               int64_t ldc, int N, const oz2_options* opt) {
+    // BLAS argument checks (xerbla order)
+    if (!trans_ok(transa)) return -1;
+    if (!trans_ok(transb)) return -2;
+    if (m < 0) return -3;
+    if (n < 0) return -4;
+    if (k < 0) return -5;
+    const int64_t rowsA = is_n(transa) ? m : k;
+    const int64_t rowsB = is_n(transb) ? k : n;
+    if (lda < (rowsA > 1 ? rowsA : 1)) return -8;
+    if (ldb < (rowsB > 1 ? rowsB : 1)) return -10;
+    if (ldc < (m > 1 ? m : 1)) return -13;
+    if (N < 2 || N > kMaxModuli) return -14;
+    if (opt) for (int i = 0; i < 8; ++i) if (opt->reserved[i]) return -15;
+    if (m == 0 || n == 0) return OZ2_SUCCESS;
+    int e = ensure_device();
+    if (e) return e;
+    if (k > 65536) return OZ2_ERR_NOT_SUPPORTED;
+    if (m > (1ll << 30) || n > (1ll << 30)) return OZ2_ERR_NOT_SUPPORTED;
+    cudaStream_t st = g_ts.stream;
+    const bool quick = (alpha == 0.0 || k == 0);
+    const bool dev = is_device_ptr(C);
+    if (!quick && (dev != is_device_ptr(A) || dev != is_device_ptr(B))) return OZ2_ERR_NOT_SUPPORTED;
+    if (dev) {
+        if (quick) { OZ2_CK(launch_scale(C, m, n, ldc, beta, st)); return OZ2_SUCCESS; }
+        return run_device(!is_n(transa), is_n(transb), m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, N, opt);
+    }
+    // host buffers: stage through device memory, run, copy back, synchronise
+    const int64_t colsA = is_n(transa) ? k : m;
+    const int64_t colsB = is_n(transb) ? n : k;
+    const size_t bA = align_up(8ull * rowsA * colsA, 256), bB = align_up(8ull * rowsB * colsB, 256);
+    const size_t bC = align_up(8ull * m * n, 256);
+    const size_t need = bA + bB + bC;
+    if (g_ts.staging_bytes < need) {
+        if (g_ts.staging) { cudaStreamSynchronize(st); cudaFree(g_ts.staging); g_ts.staging = nullptr; g_ts.staging_bytes = 0; }
+        if (cudaMalloc(&g_ts.staging, need) != cudaSuccess) return OZ2_ERR_ALLOC;
+        g_ts.staging_bytes = need;
+    }
+    double* dA = static_cast<double*>(g_ts.staging);
+    double* dB = reinterpret_cast<double*>(static_cast<uint8_t*>(g_ts.staging) + bA);
+    double* dC = reinterpret_cast<double*>(static_cast<uint8_t*>(g_ts.staging) + bA + bB);
+    if (!quick) {
+        OZ2_CK(cudaMemcpy2DAsync(dA, 8 * rowsA, A, 8 * lda, 8 * rowsA, colsA, cudaMemcpyHostToDevice, st));
+        OZ2_CK(cudaMemcpy2DAsync(dB, 8 * rowsB, B, 8 * ldb, 8 * rowsB, colsB, cudaMemcpyHostToDevice, st));
+    }
+    if (beta != 0.0) OZ2_CK(cudaMemcpy2DAsync(dC, 8 * m, C, 8 * ldc, 8 * m, n, cudaMemcpyHostToDevice, st));
+    int rc = OZ2_SUCCESS;
+    if (quick) rc = launch_scale(dC, m, n, m, beta, st) == cudaSuccess ? OZ2_SUCCESS : OZ2_ERR_CUDA;
+    else rc = run_device(!is_n(transa), is_n(transb), m, n, k, alpha, dA, rowsA, dB, rowsB, beta, dC, m, N, opt);
+    if (rc) return rc;
+    OZ2_CK(cudaMemcpy2DAsync(C, 8 * ldc, dC, 8 * m, 8 * m, n, cudaMemcpyDeviceToHost, st));
+    OZ2_CK(cudaStreamSynchronize(st));
+    return OZ2_SUCCESS;
+}
+
+}  // namespace oz2
+
+using namespace oz2;
+
+// =================================================================================
+// C ABI
+
+extern "C" {
+
+int oz2_dgemm(char transa, char transb, int64_t m, int64_t n, int64_t k, double alpha,
+              const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+              int64_t ldc, int num_moduli) {
+    return dgemm_impl(transa, transb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, num_moduli, nullptr);
+}
+
+int oz2_dgemm_ex(char transa, char transb, int64_t m, int64_t n, int64_t k, double alpha,
+                 const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+                 int64_t ldc, int num_moduli, const oz2_options* opt) {
+    return dgemm_impl(transa, transb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, num_moduli, opt);
+}
+
+int oz2_set_stream(void* stream) {
+    g_ts.stream = static_cast<cudaStream_t>(stream);
+    return OZ2_SUCCESS;
+}
+
+size_t oz2_workspace_size(char transa, char transb, int64_t m, int64_t n, int64_t k, int num_moduli) {
+    if (!trans_ok(transa) || !trans_ok(transb) || m < 0 || n < 0 || k < 0) return 0;
+    if (num_moduli < 2 || num_moduli > kMaxModuli) return 0;
+    const Plan& pl = host_plan(num_moduli);
+    return make_layout(m, n, k, num_moduli, pl.M).total;
+}
+
+int oz2_set_workspace(void* ptr, size_t bytes) {
+    g_ts.user_ws = ptr;
+    g_ts.user_ws_bytes = ptr ? bytes : 0;
+    return OZ2_SUCCESS;
+}
+
+int oz2_get_status(int32_t* status) {
+    if (!status) return -1;
+    int e = ensure_device();
+    if (e) return e;
+    int32_t h = 0;
+    OZ2_CK(cudaStreamSynchronize(g_ts.stream));
+    OZ2_CK(cudaMemcpy(&h, g_ts.d_status, sizeof(h), cudaMemcpyDeviceToHost));
+    OZ2_CK(cudaMemset(g_ts.d_status, 0, sizeof(int32_t)));
+    *status = h ? OZ2_ERR_NONFINITE : OZ2_SUCCESS;
+    return OZ2_SUCCESS;
+}
+
+int oz2_set_timing(int enable) {
+    g_ts.timing = enable != 0;
+    return OZ2_SUCCESS;
+}
+
+int oz2_get_timing(float* ms_out, int n) {
+    if (!ms_out) return -1;
+    if (!g_ts.timed_last) return OZ2_ERR_NOT_SUPPORTED;
+    if (cudaEventSynchronize(g_ts.ev[6]) != cudaSuccess) return OZ2_ERR_CUDA;
+    float v[7];
+    for (int i = 0; i < 6; ++i)
+        if (cudaEventElapsedTime(&v[i], g_ts.ev[i], g_ts.ev[i + 1]) != cudaSuccess) return OZ2_ERR_CUDA;
+    if (cudaEventElapsedTime(&v[6], g_ts.ev[0], g_ts.ev[6]) != cudaSuccess) return OZ2_ERR_CUDA;
+    for (int i = 0; i < n && i < 7; ++i) ms_out[i] = v[i];
+    return OZ2_SUCCESS;
+}
+
+int oz2_finalize(void) {
+    if (g_ts.stream) cudaStreamSynchronize(g_ts.stream);
+    if (g_ts.own_ws) cudaFree(g_ts.own_ws);
+    if (g_ts.staging) cudaFree(g_ts.staging);
+    if (g_ts.d_status) cudaFree(g_ts.d_status);
+    for (auto& kv : g_ts.plans) if (kv.second->d_pow2tab) cudaFree(kv.second->d_pow2tab);
+    g_ts.plans.clear();
+    g_ts.own_ws = nullptr; g_ts.own_ws_bytes = 0;
+    g_ts.staging = nullptr; g_ts.staging_bytes = 0;
+    g_ts.d_status = nullptr;
+    g_ts.device = -1;
+    return OZ2_SUCCESS;
+}
+
+int oz2_moduli(int num_moduli, int32_t* p_out) {
+    if (num_moduli < 2 || num_moduli > kMaxModuli) return -1;
+    if (!p_out) return -2;
+    const Plan& pl = host_plan(num_moduli);
+    for (int l = 0; l < num_moduli; ++l) p_out[l] = pl.p[l];
+    return OZ2_SUCCESS;
+}
+
+int oz2_plan_query(int num_moduli, int64_t k, oz2_plan_info* out) {
+    if (num_moduli < 2 || num_moduli > kMaxModuli) return -1;
+    if (k < 0) return -2;
+    if (!out) return -3;
+    const Plan& pl = host_plan(num_moduli);
+    std::memset(out, 0, sizeof(*out));
+    out->num_moduli = num_moduli;
+    out->num_planes = pl.M;
+    out->num_limbs = pl.L;
+    out->num_squares = pl.nsq;
+    out->p_prime = pl.p_prime;
+    out->delta = pl.delta;
+    out->f_k = f_k_of(k);
+    out->log2_P = pl.log2P;
+    for (int t = 0; t < pl.L && t < 12; ++t) out->P_limbs[t] = pl.crt.P[t];
+    for (int l = 0; l < num_moduli; ++l)
+        for (int t = 0; t < pl.L && t < 12; ++t) out->w_limbs[l][t] = pl.crt.w[l][t];
+    return OZ2_SUCCESS;
+}
+
+const char* oz2_version(void) { return "oz2 0.1.0 sm_100a"; }
+
+int oz2_fp8_gemm_raw(const uint8_t* a, const uint8_t* b, float* C32, int64_t m, int64_t n, int64_t k) {
+    if (m < 0) return -4;
+    if (n < 0) return -5;
+    if (k < 0 || (k % 16) != 0) return -6;
+    if (m == 0 || n == 0) return OZ2_SUCCESS;
+    int e = ensure_device();
+    if (e) return e;
+    if (k == 0) { OZ2_CK(cudaMemsetAsync(C32, 0, 4ull * m * n, g_ts.stream)); return OZ2_SUCCESS; }
+    if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15u) return OZ2_ERR_NOT_SUPPORTED;
+    CUtensorMap ta, tb;
+    if (!make_map(&ta, a, k, m, k, BK, BM)) return OZ2_ERR_CUDA;
+    if (!make_map(&tb, b, k, n, k, BK, BN)) return OZ2_ERR_CUDA;
+    GemmParams gp;
+    std::memset(&gp, 0, sizeof(gp));
+    gp.m = static_cast<int>(m); gp.n = static_cast<int>(n);
+    gp.num_k_blocks = static_cast<int>((k + BK - 1) / BK);
+    gp.m_tiles = static_cast<int>((m + BM - 1) / BM); gp.n_tiles = static_cast<int>((n + BN - 1) / BN);
+    gp.c32 = C32;
+    OZ2_CK(launch_gemm(MODE_RAW, ta, tb, gp, g_ts.num_sms, g_ts.stream));
+    return OZ2_SUCCESS;
+}
+
+}  // extern "C"

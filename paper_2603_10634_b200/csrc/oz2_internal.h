@@ -1,0 +1,101 @@
+// oz2_internal.h -- shared between the host planner/launcher (oz2_api.cu) and the
+// kernels.  Plain structs passed to kernels by value (they live in the constant
+// parameter bank, so uniform reads are broadcasts).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace oz2 {
+
+constexpr int kMaxModuli = 33;   // N < 34
+constexpr int kMaxLimbs = 12;
+constexpr int kPow2Tab = 1024;   // 2^E mod p for E in [0, 1024)
+
+// ---- GEMM (tcgen05) ------------------------------------------------------------
+constexpr int BM = 128;          // rows of A per CTA tile (TMEM lanes)
+constexpr int BN = 256;          // rows of B^T per CTA tile (TMEM columns per slot)
+constexpr int BK = 128;          // bytes (= E4M3 elements) of K per pipeline stage
+constexpr int STAGES = 4;
+constexpr int SMEM_A_STAGE = BM * BK;   // 16 KiB
+constexpr int SMEM_B_STAGE = BN * BK;   // 32 KiB
+constexpr int GEMM_THREADS = 320;       // warp0 TMA, warp1 MMA, warps 2..9 epilogue
+constexpr int GEMM_SMEM = STAGES * (SMEM_A_STAGE + SMEM_B_STAGE) + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int PAD_M = 256;       // row padding of operand planes (tile multiple)
+constexpr int PAD_N = 256;
+constexpr int PAD_K = 128;
+
+enum GemmMode : int { MODE_RESIDUE = 0, MODE_BOUND = 1, MODE_RAW = 2 };
+
+struct ModEpi {          // per modulus, residue-GEMM epilogue
+    float p, pinv;
+    float coef[3];       // square: (s, s, 1); non-square: (240, -15, 16)
+    int a_plane[3];      // digit-plane index of the A operand of product x
+    int b_plane[3];
+};
+
+struct GemmParams {
+    int m, n;                    // true sizes (store masks)
+    int num_k_blocks;
+    int m_tiles, n_tiles;
+    int rows_per_plane_a;        // m_pad
+    int rows_per_plane_b;        // n_pad
+    int num_moduli;
+    int16_t* residues;           // [N][n][m]
+    uint32_t* rmax;              // [m] float bits (bound)
+    uint32_t* smax;              // [n]
+    float* c32;                  // raw: [m][n]
+    ModEpi mod[kMaxModuli];
+};
+
+// ---- residue / digit split ------------------------------------------------------
+struct ModDig {
+    double p_d, pinv_d;
+    float p_f, pinv_f, s_f, inv_s_f;
+    int square;
+    int plane0;                  // first digit plane of this modulus
+};
+
+struct DigitParams {
+    int num_moduli;
+    int num_planes;
+    const uint16_t* pow2tab;     // [N][kPow2Tab]
+    ModDig mod[kMaxModuli];
+};
+
+// ---- CRT ------------------------------------------------------------------------
+struct CrtParams {
+    int num_moduli;
+    int p[kMaxModuli];
+    double qp[kMaxModuli];                       // q_l / p_l
+    uint32_t w[kMaxModuli][kMaxLimbs];           // w_l mod 2^(32L)
+    uint32_t np[kMaxLimbs];                      // 2^(32L) - P
+    uint32_t P[kMaxLimbs];
+    uint32_t halfP[kMaxLimbs];                   // P / 2 (P is even: 1024 | P)
+};
+
+// ---- exponents ------------------------------------------------------------------
+struct ExpParams {
+    float p_prime, delta, f_k;
+};
+
+// launchers (defined in the .cu files)
+cudaError_t launch_rowmax(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
+                          unsigned long long* maxbits, cudaStream_t st);
+cudaError_t launch_cast(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
+                        const unsigned long long* maxbits, int32_t* eprime, uint8_t* xbar,
+                        int64_t rows_pad, int64_t k_pad, int32_t* status, cudaStream_t st);
+cudaError_t launch_exps(const unsigned long long* maxbits, const int32_t* eprime,
+                        const uint32_t* rsmax, int64_t count, ExpParams ep, int32_t* e_out,
+                        cudaStream_t st);
+cudaError_t launch_digits(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
+                          const int32_t* e, const DigitParams& dp, uint8_t* planes,
+                          int64_t rows_pad, int64_t k_pad, cudaStream_t st);
+cudaError_t launch_gemm(int mode, const CUtensorMap& ta, const CUtensorMap& tb,
+                        const GemmParams& gp, int num_sms, cudaStream_t st);
+cudaError_t launch_crt(int limbs, const int16_t* res, int64_t m, int64_t n, const CrtParams& cp,
+                       const int32_t* e_mu, const int32_t* e_nu, double alpha, double beta,
+                       double* C, int64_t ldc, cudaStream_t st);
+cudaError_t launch_scale(double* C, int64_t m, int64_t n, int64_t ldc, double beta, cudaStream_t st);
+
+}  // namespace oz2

@@ -1,0 +1,338 @@
+// prep_kernels.cu -- the HBM-bound conversion kernels of the FP8 Ozaki-II pipeline.
+//
+//   k_rowmax  max_h |x_rh| per operand row (for mu', nu'; eq. def:mu'nu')
+//   k_cast    e'_r = 7 - floor(log2 max) and X-bar = RU_fp8(|x| 2^e')
+//   k_exps    log2 mu = log2 mu' + int(P' + delta log2 RU(f_k R))      (eq. mu-computation)
+//   k_digits  X' = trunc(2^e x), residues mod p_l, FP8 digit split
+//
+// An operand is seen as `rows` rows of length k (A: rows = i; B: rows = j of B^T).
+// Element (r, h) lives at X[r + h*ld] (MN-major: A with transa='N', B with 'T') or
+// X[h + r*ld] (K-major: A 'T', B 'N').  Outputs are K-major byte planes
+// [rows_pad][k_pad] (the tcgen05 operand layout), zero in the padding.
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "oz2_internal.h"
+#include "oz2_ptx.cuh"
+
+namespace oz2 {
+
+// ---------------------------------------------------------------------------------
+// row maxima of |x| as binary64 bit patterns (non-negative doubles order like their
+// bits; NaN/Inf patterns sort above every finite value and are flagged in k_cast)
+
+template <bool KMAJOR>
+__global__ void __launch_bounds__(256) k_rowmax(const double* __restrict__ X, int64_t rows,
+                                                int64_t k, int64_t ld,
+                                                unsigned long long* __restrict__ maxbits) {
+    if (!KMAJOR) {
+        // thread per row, block strip of k; coalesced across the rows
+        const int64_t r = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+        const int64_t h0 = static_cast<int64_t>(blockIdx.y) * 512;
+        const int64_t h1 = min(k, h0 + 512);
+        if (r >= rows) return;
+        unsigned long long mx = 0;
+        const double* p = X + r + h0 * ld;
+#pragma unroll 8
+        for (int64_t h = h0; h < h1; ++h, p += ld) {
+            const unsigned long long b = __double_as_longlong(fabs(__ldg(p)));
+            mx = b > mx ? b : mx;
+        }
+        if (mx) atomicMax(maxbits + r, mx);
+    } else {
+        // warp per row, lanes stride along k
+        const int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+        if (r >= rows) return;
+        const double* p = X + r * ld;
+        unsigned long long mx = 0;
+        int64_t h = threadIdx.x & 31;
+        for (; h + 96 < k; h += 128) {
+            const double a0 = __ldg(p + h), a1 = __ldg(p + h + 32), a2 = __ldg(p + h + 64),
+                         a3 = __ldg(p + h + 96);
+            unsigned long long b0 = __double_as_longlong(fabs(a0)), b1 = __double_as_longlong(fabs(a1));
+            unsigned long long b2 = __double_as_longlong(fabs(a2)), b3 = __double_as_longlong(fabs(a3));
+            b0 = b0 > b1 ? b0 : b1;
+            b2 = b2 > b3 ? b2 : b3;
+            b0 = b0 > b2 ? b0 : b2;
+            mx = mx > b0 ? mx : b0;
+        }
+        for (; h < k; h += 32) {
+            const unsigned long long b = __double_as_longlong(fabs(__ldg(p + h)));
+            mx = mx > b ? mx : b;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long v = __shfl_xor_sync(0xffffffffu, mx, o);
+            mx = mx > v ? mx : v;
+        }
+        if ((threadIdx.x & 31) == 0 && mx) atomicMax(maxbits + r, mx);
+    }
+}
+
+// floor(log2 x) of a positive finite binary64 given as bits
+__device__ __forceinline__ int ilog2_bits(unsigned long long b) {
+    const int ef = static_cast<int>(b >> 52);
+    if (ef > 0) return ef - 1023;
+    const unsigned long long mant = b & 0xFFFFFFFFFFFFFull;
+    return (63 - __clzll(static_cast<long long>(mant))) - 1074;
+}
+
+__device__ __forceinline__ int eprime_of(unsigned long long mb) {
+    // log2 mu' = 7 - floor(log2 max|x|) (eq. def:mu'nu'); zero row -> 0 (reading R3)
+    if (mb == 0ull || mb >= 0x7FF0000000000000ull) return 0;
+    return 7 - ilog2_bits(mb);
+}
+
+// ---------------------------------------------------------------------------------
+// Tile loader shared by k_cast and k_digits: a 32-row x 128-h tile of doubles in
+// shared memory (zero outside [0,rows) x [0,k)), loaded coalesced for both layouts.
+
+constexpr int TR = 32;     // rows per tile
+constexpr int TH = 128;    // k per tile
+constexpr int TP = TH + 1; // padded shared row (doubles)
+
+template <bool KMAJOR>
+__device__ __forceinline__ void load_tile(const double* __restrict__ X, int64_t rows, int64_t k,
+                                          int64_t ld, int64_t r0, int64_t h0, double* tile) {
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    if (!KMAJOR) {
+        // each warp reads 32 consecutive rows for 16 values of h (256 B per request)
+#pragma unroll 4
+        for (int j = 0; j < TH / 8; ++j) {
+            const int hh = w * (TH / 8) + j;
+            const int64_t r = r0 + lane, h = h0 + hh;
+            double v = 0.0;
+            if (r < rows && h < k) v = __ldg(X + r + h * ld);
+            tile[lane * TP + hh] = v;
+        }
+    } else {
+        // each warp reads 4 rows, 128 consecutive h per row (1 KiB per row)
+#pragma unroll
+        for (int j = 0; j < TR / 8; ++j) {
+            const int rr = w * (TR / 8) + j;
+            const int64_t r = r0 + rr;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int hh = q * 32 + lane;
+                const int64_t h = h0 + hh;
+                double v = 0.0;
+                if (r < rows && h < k) v = __ldg(X + h + r * ld);
+                tile[rr * TP + hh] = v;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// k_cast: e' and X-bar = RU_fp8(|x| 2^e')
+
+template <bool KMAJOR>
+__global__ void __launch_bounds__(256) k_cast(const double* __restrict__ X, int64_t rows, int64_t k,
+                                              int64_t ld, const unsigned long long* __restrict__ maxbits,
+                                              int32_t* __restrict__ eprime, uint8_t* __restrict__ xbar,
+                                              int64_t k_pad, int32_t* __restrict__ status) {
+    __shared__ double tile[TR * TP];
+    const int64_t h0 = static_cast<int64_t>(blockIdx.x) * TH;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.y) * TR;
+    load_tile<KMAJOR>(X, rows, k, ld, r0, h0, tile);
+    __syncthreads();
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    if (blockIdx.x == 0 && t < TR) {
+        const int64_t r = r0 + t;
+        if (r < rows) {
+            const unsigned long long mb = maxbits[r];
+            eprime[r] = eprime_of(mb);
+            if (mb >= 0x7FF0000000000000ull) atomicOr(status, 1);
+        }
+    }
+    // warp w handles rows w, w+8, w+16, w+24; lane covers 4 consecutive h
+#pragma unroll
+    for (int j = 0; j < TR / 8; ++j) {
+        const int rr = w + 8 * j;
+        const int64_t r = r0 + rr;
+        const int e = (r < rows) ? eprime_of(maxbits[r]) : 0;
+        uint32_t word = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double x = tile[rr * TP + lane * 4 + q];
+            uint32_t c = 0;
+            if (x != 0.0) {
+                c = fp8_ru_code(ldexp(fabs(x), e));
+                c = c ? c : 1u;               // an underflowed nonzero still rounds up to 2^-9
+            }
+            word |= c << (8 * q);
+        }
+        *reinterpret_cast<uint32_t*>(xbar + r * k_pad + h0 + lane * 4) = word;
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// k_exps: scaling exponents from the bound maxima (eq. mu-computation)
+
+__global__ void k_exps(const unsigned long long* __restrict__ maxbits,
+                       const int32_t* __restrict__ eprime, const uint32_t* __restrict__ rsmax,
+                       int64_t count, ExpParams ep, int32_t* __restrict__ e_out) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= count) return;
+    const unsigned long long mb = maxbits[r];
+    if (mb == 0ull) { e_out[r] = 0; return; }               // zero row (R3)
+    const float R = __uint_as_float(rsmax[r]);
+    if (!(R > 0.0f)) { e_out[r] = eprime[r]; return; }       // no nonzero product
+    const float cbar = __fmul_ru(ep.f_k, R);                 // RU(f_k C-bar') (eq. barCupper, R5)
+    const float x1 = __double2float_rd(log2(static_cast<double>(cbar)));   // R7
+    const float x2 = __fmul_rd(ep.delta, x1);
+    const float x3 = __fadd_rd(ep.p_prime, x2);
+    e_out[r] = eprime[r] + static_cast<int>(floorf(x3));   // int() = floor (R8)
+}
+
+// ---------------------------------------------------------------------------------
+// k_digits: X' = trunc(2^e x) (exact), r_l = mod(X', p_l), FP8 digits
+
+template <bool KMAJOR>
+__global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, int64_t rows,
+                                                int64_t k, int64_t ld,
+                                                const int32_t* __restrict__ e_scale,
+                                                const __grid_constant__ DigitParams dp,
+                                                uint8_t* __restrict__ planes, int64_t rows_pad,
+                                                int64_t k_pad) {
+    __shared__ double tile[TR * TP];
+    const int64_t h0 = static_cast<int64_t>(blockIdx.x) * TH;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.y) * TR;
+    load_tile<KMAJOR>(X, rows, k, ld, r0, h0, tile);
+    __syncthreads();
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int64_t plane_stride = rows_pad * k_pad;
+#pragma unroll 1
+    for (int j = 0; j < TR / 8; ++j) {
+        const int rr = w + 8 * j;
+        const int64_t r = r0 + rr;
+        const int e = (r < rows) ? e_scale[r] : 0;
+        // |X'| = M 2^E with M < 2^53 an integer (E = 0 below 2^53), sign separately
+        double M[4];
+        int E[4];
+        bool neg[4];
+        bool anyE = false;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double y = trunc(ldexp(tile[rr * TP + lane * 4 + q], e));   // eq. def:A'
+            neg[q] = y < 0.0;
+            double ay = fabs(y);
+            int ee = 0;
+            if (ay >= 9007199254740992.0) {            // 2^53
+                ee = ilogb(ay) - 52;
+                ay = ldexp(ay, -ee);
+                anyE = true;
+            }
+            M[q] = ay;
+            E[q] = ee;
+        }
+        const bool warpE = __any_sync(0xffffffffu, anyE);
+        uint8_t* out = planes + r * k_pad + h0 + lane * 4;
+#pragma unroll 1
+        for (int l = 0; l < dp.num_moduli; ++l) {
+            const ModDig md = dp.mod[l];
+            float res[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double qq = rint(M[q] * md.pinv_d);
+                float rf = static_cast<float>(fma(-qq, md.p_d, M[q]));   // exact, |rf| <= p/2+1
+                if (warpE) {
+                    const float tw = static_cast<float>(__ldg(dp.pow2tab + l * kPow2Tab + min(E[q], kPow2Tab - 1)));
+                    rf *= tw;                                        // exact (< 2^20)
+                    rf = fmaf(-rintf(rf * md.pinv_f), md.p_f, rf);
+                }
+                if (neg[q]) rf = -rf;
+                // symmetric range [-floor(p/2), ceil(p/2)-1] (R2)
+                if (2.0f * rf >= md.p_f) rf -= md.p_f;
+                else if (2.0f * rf < -md.p_f) rf += md.p_f;
+                res[q] = rf;
+            }
+            if (md.square) {
+                // D1 = round(r/s) ties-to-even, D2 = r - s D1 (R9)
+                uint32_t w1 = 0, w2 = 0;
+#pragma unroll
+                for (int q = 0; q < 4; q += 2) {
+                    const float a1 = rintf(res[q] * md.inv_s_f), b1 = rintf(res[q + 1] * md.inv_s_f);
+                    const float a2 = fmaf(-a1, md.s_f, res[q]), b2 = fmaf(-b1, md.s_f, res[q + 1]);
+                    w1 |= static_cast<uint32_t>(cvt_e4m3x2(a1 + 0.0f, b1 + 0.0f)) << (8 * q);
+                    w2 |= static_cast<uint32_t>(cvt_e4m3x2(a2 + 0.0f, b2 + 0.0f)) << (8 * q);
+                }
+                *reinterpret_cast<uint32_t*>(out + (md.plane0 + 0) * plane_stride) = w1;
+                *reinterpret_cast<uint32_t*>(out + (md.plane0 + 1) * plane_stride) = w2;
+            } else {
+                // D1 = sign(r) ceil(|r|/16), D2 = r - 16 D1, D3 = D1 + D2
+                uint32_t w1 = 0, w2 = 0, w3 = 0;
+#pragma unroll
+                for (int q = 0; q < 4; q += 2) {
+                    const float a1 = copysignf(ceilf(fabsf(res[q]) * 0.0625f), res[q]);
+                    const float b1 = copysignf(ceilf(fabsf(res[q + 1]) * 0.0625f), res[q + 1]);
+                    const float a2 = fmaf(-16.0f, a1, res[q]), b2 = fmaf(-16.0f, b1, res[q + 1]);
+                    const float a3 = a1 + a2, b3 = b1 + b2;
+                    w1 |= static_cast<uint32_t>(cvt_e4m3x2(a1 + 0.0f, b1 + 0.0f)) << (8 * q);
+                    w2 |= static_cast<uint32_t>(cvt_e4m3x2(a2 + 0.0f, b2 + 0.0f)) << (8 * q);
+                    w3 |= static_cast<uint32_t>(cvt_e4m3x2(a3 + 0.0f, b3 + 0.0f)) << (8 * q);
+                }
+                *reinterpret_cast<uint32_t*>(out + (md.plane0 + 0) * plane_stride) = w1;
+                *reinterpret_cast<uint32_t*>(out + (md.plane0 + 1) * plane_stride) = w2;
+                *reinterpret_cast<uint32_t*>(out + (md.plane0 + 2) * plane_stride) = w3;
+            }
+        }
+    }
+}
+
+__global__ void k_scale(double* C, int64_t m, int64_t n, int64_t ldc, double beta) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (int64_t j = blockIdx.y; j < n; j += gridDim.y) {
+        if (i < m) C[i + j * ldc] = (beta == 0.0) ? 0.0 : beta * C[i + j * ldc];
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// launchers
+
+cudaError_t launch_rowmax(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
+                          unsigned long long* maxbits, cudaStream_t st) {
+    if (rows == 0 || k == 0) return cudaSuccess;
+    if (!kmajor) {
+        dim3 grid(static_cast<unsigned>((rows + 255) / 256), static_cast<unsigned>((k + 511) / 512));
+        k_rowmax<false><<<grid, 256, 0, st>>>(X, rows, k, ld, maxbits);
+    } else {
+        dim3 grid(static_cast<unsigned>((rows + 7) / 8));
+        k_rowmax<true><<<grid, 256, 0, st>>>(X, rows, k, ld, maxbits);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cast(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
+                        const unsigned long long* maxbits, int32_t* eprime, uint8_t* xbar,
+                        int64_t rows_pad, int64_t k_pad, int32_t* status, cudaStream_t st) {
+    dim3 grid(static_cast<unsigned>(k_pad / TH), static_cast<unsigned>(rows_pad / TR));
+    if (kmajor) k_cast<true><<<grid, 256, 0, st>>>(X, rows, k, ld, maxbits, eprime, xbar, k_pad, status);
+    else k_cast<false><<<grid, 256, 0, st>>>(X, rows, k, ld, maxbits, eprime, xbar, k_pad, status);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_exps(const unsigned long long* maxbits, const int32_t* eprime,
+                        const uint32_t* rsmax, int64_t count, ExpParams ep, int32_t* e_out,
+                        cudaStream_t st) {
+    if (count == 0) return cudaSuccess;
+    k_exps<<<static_cast<unsigned>((count + 255) / 256), 256, 0, st>>>(maxbits, eprime, rsmax, count, ep, e_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_digits(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
+                          const int32_t* e, const DigitParams& dp, uint8_t* planes,
+                          int64_t rows_pad, int64_t k_pad, cudaStream_t st) {
+    dim3 grid(static_cast<unsigned>(k_pad / TH), static_cast<unsigned>(rows_pad / TR));
+    if (kmajor) k_digits<true><<<grid, 256, 0, st>>>(X, rows, k, ld, e, dp, planes, rows_pad, k_pad);
+    else k_digits<false><<<grid, 256, 0, st>>>(X, rows, k, ld, e, dp, planes, rows_pad, k_pad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scale(double* C, int64_t m, int64_t n, int64_t ldc, double beta, cudaStream_t st) {
+    if (m == 0 || n == 0) return cudaSuccess;
+    dim3 grid(static_cast<unsigned>((m + 255) / 256), static_cast<unsigned>(n < 65535 ? n : 65535));
+    k_scale<<<grid, 256, 0, st>>>(C, m, n, ldc, beta);
+    return cudaGetLastError();
+}
+
+}  // namespace oz2

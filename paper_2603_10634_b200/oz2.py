@@ -1,0 +1,225 @@
+"""Python binding of liboz2.so (include/oz2.h) -- argument marshalling only.
+
+Every step of the emulation runs in the library's CUDA kernels; this module only
+loads the shared library with ctypes, declares the C signatures and converts
+arguments.  There is no CPU fallback: if liboz2.so is missing or no sm_100 device
+is present the calls fail loudly.
+"""
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liboz2.so")
+
+OZ2_SUCCESS = 0
+OZ2_ERR_CUDA = 1
+OZ2_ERR_ALLOC = 2
+OZ2_ERR_WORKSPACE = 3
+OZ2_ERR_NOT_SUPPORTED = 4
+OZ2_ERR_NONFINITE = 5
+
+_c_int64 = ctypes.c_int64
+_vp = ctypes.c_void_p
+
+
+class oz2_options(ctypes.Structure):
+    _fields_ = [
+        ("e_prime_a", _vp), ("e_prime_b", _vp), ("abar", _vp), ("bbar", _vp),
+        ("rmax", _vp), ("smax", _vp), ("e_mu", _vp), ("e_nu", _vp),
+        ("digits_a", _vp), ("digits_b", _vp), ("residues", _vp),
+        ("e_mu_in", _vp), ("e_nu_in", _vp),
+        ("reserved", ctypes.c_int32 * 8),
+    ]
+
+
+class oz2_plan_info(ctypes.Structure):
+    _fields_ = [
+        ("num_moduli", ctypes.c_int32), ("num_planes", ctypes.c_int32),
+        ("num_limbs", ctypes.c_int32), ("num_squares", ctypes.c_int32),
+        ("p_prime", ctypes.c_float), ("delta", ctypes.c_float), ("f_k", ctypes.c_float),
+        ("log2_P", ctypes.c_double),
+        ("P_limbs", ctypes.c_uint32 * 12),
+        ("w_limbs", (ctypes.c_uint32 * 12) * 33),
+    ]
+
+
+# (name, restype, argtypes) -- the full exported surface of include/oz2.h
+SIGNATURES = [
+    ("oz2_dgemm", ctypes.c_int,
+     [ctypes.c_char, ctypes.c_char, _c_int64, _c_int64, _c_int64, ctypes.c_double, _vp, _c_int64,
+      _vp, _c_int64, ctypes.c_double, _vp, _c_int64, ctypes.c_int]),
+    ("oz2_dgemm_ex", ctypes.c_int,
+     [ctypes.c_char, ctypes.c_char, _c_int64, _c_int64, _c_int64, ctypes.c_double, _vp, _c_int64,
+      _vp, _c_int64, ctypes.c_double, _vp, _c_int64, ctypes.c_int, ctypes.POINTER(oz2_options)]),
+    ("oz2_set_stream", ctypes.c_int, [_vp]),
+    ("oz2_workspace_size", ctypes.c_size_t,
+     [ctypes.c_char, ctypes.c_char, _c_int64, _c_int64, _c_int64, ctypes.c_int]),
+    ("oz2_set_workspace", ctypes.c_int, [_vp, ctypes.c_size_t]),
+    ("oz2_get_status", ctypes.c_int, [ctypes.POINTER(ctypes.c_int32)]),
+    ("oz2_set_timing", ctypes.c_int, [ctypes.c_int]),
+    ("oz2_get_timing", ctypes.c_int, [ctypes.POINTER(ctypes.c_float), ctypes.c_int]),
+    ("oz2_finalize", ctypes.c_int, []),
+    ("oz2_moduli", ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int32)]),
+    ("oz2_plan_query", ctypes.c_int, [ctypes.c_int, _c_int64, ctypes.POINTER(oz2_plan_info)]),
+    ("oz2_version", ctypes.c_char_p, []),
+    ("oz2_fp8_gemm_raw", ctypes.c_int, [_vp, _vp, _vp, _c_int64, _c_int64, _c_int64]),
+]
+
+_lib = None
+
+
+def lib():
+    """The loaded liboz2.so (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} not found: build it with `python -m paper_2603_10634_b200._build` "
+                "(or __graft_entry__.build()); there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _ch(t):
+    return t.encode() if isinstance(t, str) else t
+
+
+def _check(rc, what):
+    if rc != OZ2_SUCCESS:
+        raise RuntimeError(f"{what} failed with status {rc}")
+    return rc
+
+
+# ---- 1:1 wrappers of the C ABI (pointers are ints) ---------------------------------
+
+def oz2_dgemm(transa, transb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, num_moduli):
+    return lib().oz2_dgemm(_ch(transa), _ch(transb), m, n, k, alpha, A, lda, B, ldb, beta, C, ldc,
+                           num_moduli)
+
+
+def oz2_dgemm_ex(transa, transb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, num_moduli, opt):
+    return lib().oz2_dgemm_ex(_ch(transa), _ch(transb), m, n, k, alpha, A, lda, B, ldb, beta, C,
+                              ldc, num_moduli, ctypes.byref(opt) if opt is not None else None)
+
+
+def oz2_set_stream(stream):
+    return lib().oz2_set_stream(stream)
+
+
+def oz2_workspace_size(transa, transb, m, n, k, num_moduli):
+    return lib().oz2_workspace_size(_ch(transa), _ch(transb), m, n, k, num_moduli)
+
+
+def oz2_set_workspace(ptr, nbytes):
+    return lib().oz2_set_workspace(ptr, nbytes)
+
+
+def oz2_get_status():
+    s = ctypes.c_int32(0)
+    _check(lib().oz2_get_status(ctypes.byref(s)), "oz2_get_status")
+    return s.value
+
+
+def oz2_set_timing(enable):
+    return lib().oz2_set_timing(1 if enable else 0)
+
+
+PHASES = ["prescale", "bound_gemm", "exponents", "digits", "residue_gemm", "crt", "total"]
+
+
+def oz2_get_timing():
+    """Per-phase ms of the last timed call (see include/oz2.h), as a dict."""
+    buf = (ctypes.c_float * 7)()
+    _check(lib().oz2_get_timing(buf, 7), "oz2_get_timing")
+    return dict(zip(PHASES, list(buf)))
+
+
+def oz2_finalize():
+    return lib().oz2_finalize()
+
+
+def oz2_moduli(num_moduli):
+    out = (ctypes.c_int32 * num_moduli)()
+    _check(lib().oz2_moduli(num_moduli, out), "oz2_moduli")
+    return list(out)
+
+
+def oz2_plan_query(num_moduli, k):
+    info = oz2_plan_info()
+    _check(lib().oz2_plan_query(num_moduli, k, ctypes.byref(info)), "oz2_plan_query")
+    return info
+
+
+def oz2_version():
+    return lib().oz2_version().decode()
+
+
+def oz2_fp8_gemm_raw(a, b, C32, m, n, k):
+    return lib().oz2_fp8_gemm_raw(a, b, C32, m, n, k)
+
+
+# ---- torch convenience (still only marshalling) ----------------------------------
+
+_ws = {}
+
+
+def _bind_stream_and_workspace(torch, device, nbytes):
+    """Point the library at torch's current stream and a torch-owned workspace."""
+    stream = torch.cuda.current_stream(device)
+    oz2_set_stream(stream.cuda_stream)
+    key = (device.index if device.index is not None else torch.cuda.current_device())
+    buf = _ws.get(key)
+    if buf is None or buf.numel() < nbytes:
+        _ws[key] = None
+        buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        _ws[key] = buf
+    oz2_set_workspace(buf.data_ptr(), buf.numel())
+
+
+def _colmajor(X):
+    """(tensor, trans, ld) with op(stored) == X for a 2-D float64 CUDA tensor."""
+    r, c = X.shape
+    s0, s1 = X.stride()
+    if s0 == 1 and s1 >= max(1, r):
+        return X, "N", s1
+    if s1 == 1 and s0 >= max(1, c):
+        return X, "T", s0
+    X = X.t().contiguous().t()
+    return X, "N", X.stride(1)
+
+
+def dgemm(A, B, alpha=1.0, beta=0.0, C=None, num_moduli=13):
+    """C <- alpha A @ B + beta C on torch float64 CUDA tensors via oz2_dgemm.
+
+    Any 2-D strided layout is accepted; the result is column-major (Fortran order)."""
+    import torch
+    assert A.dtype == torch.float64 and B.dtype == torch.float64
+    m, k = A.shape
+    k2, n = B.shape
+    assert k == k2
+    if C is None:
+        C = torch.empty((n, m), dtype=torch.float64, device=A.device).t()
+        beta = 0.0
+    A_, ta, lda = _colmajor(A)
+    B_, tb, ldb = _colmajor(B)
+    if C.stride(0) == 1:
+        C_, ldc = C, max(1, C.stride(1))
+        ws = oz2_workspace_size(ta, tb, m, n, k, num_moduli)
+        _bind_stream_and_workspace(torch, A.device, ws)
+        _check(oz2_dgemm(ta, tb, m, n, k, alpha, A_.data_ptr(), lda, B_.data_ptr(), ldb, beta,
+                         C_.data_ptr(), ldc, num_moduli), "oz2_dgemm")
+        return C
+    # row-major C: compute C^T = B^T A^T into the column-major view of C^T
+    Ct = C.t()
+    tb2 = "T" if tb == "N" else "N"
+    ta2 = "T" if ta == "N" else "N"
+    ws = oz2_workspace_size(tb2, ta2, n, m, k, num_moduli)
+    _bind_stream_and_workspace(torch, A.device, ws)
+    _check(oz2_dgemm(tb2, ta2, n, m, k, alpha, B_.data_ptr(), ldb, A_.data_ptr(), lda, beta,
+                     Ct.data_ptr(), max(1, Ct.stride(1)), num_moduli), "oz2_dgemm")
+    return C

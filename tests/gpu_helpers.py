@@ -1,0 +1,82 @@
+"""Helpers for the -m gpu tests: run the C-ABI pipeline on device buffers built from
+host (numpy) inputs and fetch its debug outputs."""
+import numpy as np
+
+import paper_2603_10634_b200 as oz2
+
+
+def torch():
+    import torch as t
+    return t
+
+
+def to_dev(x: np.ndarray):
+    t = torch()
+    return t.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def store(X: np.ndarray, trans: str):
+    """Column-major storage of op^-1(X): returns (flat device tensor, ld, rows, cols)."""
+    S = X if trans == "N" else X.T
+    rows, cols = S.shape
+    flat = np.asfortranarray(S).ravel(order="F")
+    return to_dev(flat), max(1, rows)
+
+
+def run(A, B, N, transa="N", transb="N", alpha=1.0, beta=0.0, C0=None, e_mu_in=None,
+        e_nu_in=None, want_digits=False, ldc_pad=0):
+    """Full pipeline through oz2_dgemm_ex; returns dict of host numpy outputs."""
+    t = torch()
+    m, k = A.shape
+    n = B.shape[1]
+    dA, lda = store(A, transa)
+    dB, ldb = store(B, transb)
+    ldc = max(1, m + ldc_pad)
+    Cst = np.zeros((ldc, n))
+    if C0 is not None:
+        Cst[:m, :] = C0
+    dC = to_dev(np.asfortranarray(Cst).ravel(order="F"))
+    dev = "cuda"
+    out = {
+        "e_prime_a": t.zeros(m, dtype=t.int32, device=dev),
+        "e_prime_b": t.zeros(n, dtype=t.int32, device=dev),
+        "abar": t.zeros(max(1, m * k), dtype=t.uint8, device=dev),
+        "bbar": t.zeros(max(1, n * k), dtype=t.uint8, device=dev),
+        "rmax": t.zeros(m, dtype=t.float32, device=dev),
+        "smax": t.zeros(n, dtype=t.float32, device=dev),
+        "e_mu": t.zeros(m, dtype=t.int32, device=dev),
+        "e_nu": t.zeros(n, dtype=t.int32, device=dev),
+        "residues": t.zeros(N * m * n, dtype=t.int16, device=dev),
+    }
+    M = oz2.oz2_plan_query(N, k).num_planes
+    if want_digits:
+        out["digits_a"] = t.zeros(M * m * k, dtype=t.uint8, device=dev)
+        out["digits_b"] = t.zeros(M * n * k, dtype=t.uint8, device=dev)
+    opt = oz2.oz2_options()
+    for key, v in out.items():
+        setattr(opt, key, v.data_ptr())
+    keep = []
+    if e_mu_in is not None:
+        a = t.tensor(np.asarray(e_mu_in, dtype=np.int32), device=dev)
+        b = t.tensor(np.asarray(e_nu_in, dtype=np.int32), device=dev)
+        keep += [a, b]
+        opt.e_mu_in = a.data_ptr()
+        opt.e_nu_in = b.data_ptr()
+    oz2.oz2_set_stream(t.cuda.current_stream().cuda_stream)
+    oz2.oz2_set_workspace(None, 0)
+    rc = oz2.oz2_dgemm_ex(transa, transb, m, n, k, alpha, dA.data_ptr(), lda, dB.data_ptr(), ldb,
+                          beta, dC.data_ptr(), ldc, N, opt)
+    assert rc == 0, rc
+    t.cuda.synchronize()
+    res = {key: v.cpu().numpy() for key, v in out.items()}
+    res["abar"] = res["abar"][: m * k].reshape(m, k)
+    res["bbar"] = res["bbar"][: n * k].reshape(n, k)
+    res["residues"] = res["residues"].reshape(N, n, m).transpose(0, 2, 1)   # [l][i][j]
+    if want_digits:
+        res["digits_a"] = res["digits_a"].reshape(M, m, k)
+        res["digits_b"] = res["digits_b"].reshape(M, n, k)
+    Cfull = dC.cpu().numpy().reshape(n, ldc).T
+    res["C"] = Cfull[:m, :]
+    res["C_pad"] = Cfull[m:, :]
+    res["status"] = oz2.oz2_get_status()
+    return res

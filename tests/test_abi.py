@@ -1,0 +1,88 @@
+"""The C-ABI library loads, exports every symbol include/oz2.h declares, and its
+host-only planner agrees with the oracle (no device needed, no compute calls)."""
+import os
+import re
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "oz2.h")
+
+
+def _declared():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(oz2_[a-z0-9_]+)\s*\(", txt)))
+
+
+@pytest.fixture(scope="module")
+def oz2mod():
+    import paper_2603_10634_b200 as P
+    P.lib()
+    return P
+
+
+def test_header_symbols_exported(oz2mod):
+    names = _declared()
+    assert "oz2_dgemm" in names and len(names) >= 10
+    out = subprocess.run(["nm", "-D", "--defined-only", oz2mod.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (oz2_[a-z0-9_]+)", out))
+    assert set(names) <= exported, set(names) - exported
+    bound = {s[0] for s in oz2mod.SIGNATURES}
+    assert set(names) == bound            # the binding covers exactly the header surface
+    for n in names:
+        assert hasattr(oz2mod.lib(), n)
+
+
+def test_built_for_sm100a(oz2mod):
+    out = subprocess.run(["cuobjdump", "--list-elf", oz2mod.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", oz2mod.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UTCQMMA" in sass          # tcgen05.mma kind::f8f6f4
+    assert "UTMALDG" in sass          # TMA loads
+    assert "LDTM" in sass             # tcgen05.ld
+    assert "HMMA" not in sass and "QGMMA" not in sass
+
+
+def test_version(oz2mod):
+    assert "sm_100a" in oz2mod.oz2_version()
+
+
+def test_moduli_match_oracle(oz2mod):
+    from oracle import moduli as mod
+    for N in [2, 6, 7, 12, 13, 14, 20, 33]:
+        assert oz2mod.oz2_moduli(N) == mod.hybrid_moduli(N)
+
+
+def test_plan_constants_match_oracle(oz2mod):
+    from fractions import Fraction
+    from oracle import fp32, models, moduli as mod, scheme
+    for N in [2, 6, 12, 13, 14, 16, 20, 33]:
+        for k in [1, 64, 4096, 8192, 16384, 65536]:
+            info = oz2mod.oz2_plan_query(N, k)
+            plan = mod.crt_plan(mod.hybrid_moduli(N))
+            assert info.num_planes == models.M_N(N)
+            assert info.num_squares == min(N, 6)
+            assert Fraction(info.p_prime) == mod.p_prime(plan.P)
+            assert Fraction(info.delta) == mod.delta()
+            assert Fraction(info.f_k) == scheme.safety_factor(k)
+            L = info.num_limbs
+            assert 2 ** (32 * L - 1) > plan.P          # two's complement holds (-P, P)
+            assert sum(info.P_limbs[t] << (32 * t) for t in range(L)) == plan.P
+            for l, w in enumerate(plan.w):
+                assert sum(info.w_limbs[l][t] << (32 * t) for t in range(L)) == w
+
+
+def test_argument_errors_before_device(oz2mod):
+    # BLAS xerbla order; returned before any device work
+    assert oz2mod.oz2_dgemm("X", "N", 1, 1, 1, 1.0, 0, 1, 0, 1, 0.0, 0, 1, 12) == -1
+    assert oz2mod.oz2_dgemm("N", "Q", 1, 1, 1, 1.0, 0, 1, 0, 1, 0.0, 0, 1, 12) == -2
+    assert oz2mod.oz2_dgemm("N", "N", -1, 1, 1, 1.0, 0, 1, 0, 1, 0.0, 0, 1, 12) == -3
+    assert oz2mod.oz2_dgemm("N", "N", 4, 1, 1, 1.0, 0, 3, 0, 1, 0.0, 0, 4, 12) == -8
+    assert oz2mod.oz2_dgemm("N", "N", 4, 1, 5, 1.0, 0, 4, 0, 4, 0.0, 0, 4, 12) == -10
+    assert oz2mod.oz2_dgemm("N", "N", 4, 1, 1, 1.0, 0, 4, 0, 1, 0.0, 0, 3, 12) == -13
+    assert oz2mod.oz2_dgemm("N", "N", 4, 1, 1, 1.0, 0, 4, 0, 1, 0.0, 0, 4, 1) == -14
+    assert oz2mod.oz2_dgemm("N", "N", 0, 0, 0, 1.0, 0, 1, 0, 1, 0.0, 0, 1, 12) == 0   # quick return
+    assert oz2mod.oz2_workspace_size("N", "N", 64, 64, 64, 14) > 0

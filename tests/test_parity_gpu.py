@@ -1,0 +1,258 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element.
+
+Bars:
+  * e', A-bar, B-bar, digit planes, residues C'_l: bit-exact (integer/byte work);
+  * R, S: sound (f_k R >= exact max) and within the R5 rounding budget;
+  * e_mu, e_nu: equal to the oracle's (both take the FP32 round-down decisions of
+    P:379-380); any row where the tensor core's FP32 rounding of C-bar' moves the
+    floor is validated instead (several exponents are correct, reading R13);
+  * C: bit-exact to the oracle wherever the exponents agree (the CRT is exact and the
+    final rounding is RNE on both sides), hence normwise <= 1e-15 (north_star).
+"""
+import math
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from oracle import exact, fp8, fp32, moduli as mod, scheme
+from synth import gen_host
+
+
+@pytest.fixture(scope="module")
+def dev():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2603_10634_b200 as P
+    P.lib()
+    return P
+
+
+_LUT = np.array([fp8.encode_int(v) for v in range(-16, 17)], dtype=np.uint8)
+
+
+def _codes_e4m3(vals):
+    """Exact E4M3 codes of integers in [-16, 16] (oracle codec, vectorised by a table)."""
+    v = np.asarray(vals, dtype=np.int64)
+    assert v.min(initial=0) >= -16 and v.max(initial=0) <= 16
+    return _LUT[v + 16]
+
+
+# ------------------------------------------------------------------ raw FP8 GEMM probes
+
+def _raw(dev, a_codes, b_codes):
+    import torch
+    m, k = a_codes.shape
+    n = b_codes.shape[0]
+    a = torch.from_numpy(np.ascontiguousarray(a_codes)).cuda()
+    b = torch.from_numpy(np.ascontiguousarray(b_codes)).cuda()
+    c = torch.zeros(m * n, dtype=torch.float32, device="cuda")
+    dev.oz2_set_stream(torch.cuda.current_stream().cuda_stream)
+    assert dev.oz2_fp8_gemm_raw(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k) == 0
+    torch.cuda.synchronize()
+    return c.cpu().numpy().reshape(m, n)
+
+
+def test_fp8_exactness_window_extremes(dev):
+    """All-16 digits at k = 2^16 give exactly 2^24 (eq. error-free-FP8-matmult)."""
+    k = 65536
+    a = np.full((128, k), fp8.encode_int(16), dtype=np.uint8)
+    a[1::2] = fp8.encode_int(-16)
+    b = np.full((256, k), fp8.encode_int(16), dtype=np.uint8)
+    c = _raw(dev, a, b)
+    assert np.all(c[0::2] == 2.0 ** 24) and np.all(c[1::2] == -(2.0 ** 24))
+
+
+@pytest.mark.parametrize("k", [32, 4096, 65536])
+def test_fp8_random_digits_exact(dev, k):
+    """Random integer digits in [-16, 16]: the FP32 accumulation is exact."""
+    rng = np.random.default_rng(k)
+    m, n = 192, 300                       # ragged: 2 x 2 tiles
+    A = rng.integers(-16, 17, size=(m, k))
+    B = rng.integers(-16, 17, size=(n, k))
+    c = _raw(dev, _codes_e4m3(A), _codes_e4m3(B))
+    want = scheme.exact_int_matmul(A, B.T)
+    assert np.array_equal(c.astype(np.int64), want)
+
+
+def test_fp8_bound_rounding_within_R5(dev):
+    """Non-negative FP8 values across the exponent range (like A-bar B-bar): the
+    tensor-core FP32 result underestimates the exact sum by < k 2^-23 (reading R5)."""
+    rng = np.random.default_rng(7)
+    k = 16384
+    m, n = 128, 256
+    codes_a = rng.integers(0x01, 0x79, size=(m, k)).astype(np.uint8)
+    codes_b = rng.integers(0x01, 0x79, size=(n, k)).astype(np.uint8)
+    c = _raw(dev, codes_a, codes_b)
+    exactv = scheme.exact_int_matmul(scheme.fp8_scaled_int(codes_a), scheme.fp8_scaled_int(codes_b).T)
+    ex = exactv.astype(np.float64) / 2.0 ** 18
+    rel = (ex - c.astype(np.float64)) / ex
+    assert rel.max() < k * 2.0 ** -23
+    assert np.abs(rel).max() < k * 2.0 ** -23
+
+
+# ------------------------------------------------------------------ full pipeline parity
+
+def _compare(res, ref, A, B, N):
+    m, n = A.shape[0], B.shape[1]
+    assert res["e_prime_a"].tolist() == ref.e_prime_A
+    assert res["e_prime_b"].tolist() == ref.e_prime_B
+    assert np.array_equal(res["abar"], ref.Abar)
+    assert np.array_equal(res["bbar"], ref.BbarT)
+    # R, S: sound and close (tensor-core rounding, R5/R6)
+    k = A.shape[1]
+    Cx = scheme.bound_product_exact(ref.Abar, ref.BbarT).astype(np.float64) / 2.0 ** 18
+    for i in range(m):
+        exact_max = Cx[i].max() if n else 0.0
+        g = float(res["rmax"][i])
+        assert g <= exact_max * (1 + 2.0 ** -23) and g >= exact_max * (1 - k * 2.0 ** -23)
+    for j in range(n):
+        exact_max = Cx[:, j].max() if m else 0.0
+        g = float(res["smax"][j])
+        assert g <= exact_max * (1 + 2.0 ** -23) and g >= exact_max * (1 - k * 2.0 ** -23)
+    rows_ok = [res["e_mu"][i] == ref.e_mu[i] for i in range(m)]
+    cols_ok = [res["e_nu"][j] == ref.e_nu[j] for j in range(n)]
+    # exponents may differ only where the oracle's own FP32 model rounds differently
+    for i in range(m):
+        if not rows_ok[i]:
+            Pp, dlt = ref.Pp, ref.delta
+            lo = scheme.scaling_offset(Fraction(float(Cx[i].max())) * (1 - Fraction(k, 2 ** 23)), k, Pp, dlt)
+            hi = scheme.scaling_offset(Fraction(float(Cx[i].max())), k, Pp, dlt)
+            assert hi <= res["e_mu"][i] - ref.e_prime_A[i] <= lo
+    for j in range(n):
+        if not cols_ok[j]:
+            Pp, dlt = ref.Pp, ref.delta
+            lo = scheme.scaling_offset(Fraction(float(Cx[:, j].max())) * (1 - Fraction(k, 2 ** 23)), k, Pp, dlt)
+            hi = scheme.scaling_offset(Fraction(float(Cx[:, j].max())), k, Pp, dlt)
+            assert hi <= res["e_nu"][j] - ref.e_prime_B[j] <= lo
+    assert sum(rows_ok) >= m - 1 and sum(cols_ok) >= n - 1
+    for l in range(N):
+        for i in range(m):
+            if not rows_ok[i]:
+                continue
+            want = ref.residues[l][i]
+            got = res["residues"][l][i]
+            mask = np.array(cols_ok)
+            assert np.array_equal(got[mask], want[mask]), (l, i)
+    mask = np.outer(rows_ok, cols_ok)
+    assert np.array_equal(res["C"][mask], ref.C[mask])
+    return mask
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_config1_64cubed_N14(dev, seed):
+    """BASELINE config 1: m=n=k=64, 14 moduli, uniform [-1,1]: bit-exact residues."""
+    from gpu_helpers import run
+    A = gen_host(64, 64, "uniform", seed=seed)
+    B = gen_host(64, 64, "uniform", seed=100 + seed)
+    ref = scheme.dgemm(A, B, 14, want_digits=True)
+    res = run(A, B, 14, want_digits=True)
+    mask = _compare(res, ref, A, B, 14)
+    assert mask.all()
+    # digit planes (same tie rule R9) bit-exact
+    planes_a = [pl for (da, db) in ref.extra["digits"] for pl in da]
+    planes_b = [pl for (da, db) in ref.extra["digits"] for pl in db]
+    for x, pl in enumerate(planes_a):
+        assert np.array_equal(res["digits_a"][x], _codes_e4m3(pl)), x
+    for x, pl in enumerate(planes_b):
+        assert np.array_equal(res["digits_b"][x], _codes_e4m3(pl)), x
+    assert res["status"] == 0
+
+
+@pytest.mark.parametrize("transa,transb", [("N", "N"), ("T", "N"), ("N", "T"), ("T", "T")])
+@pytest.mark.parametrize("N,phi", [(12, 1.0), (13, 4.0), (7, 0.5)])
+def test_ragged_layouts(dev, transa, transb, N, phi):
+    """Several tiles and ragged tails in m, n and k, all four op() combinations."""
+    from gpu_helpers import run
+    m, k, n = 200, 300, 290
+    A = gen_host(m, k, "phi", phi=phi, seed=3)
+    B = gen_host(k, n, "phi", phi=phi, seed=4)
+    A[5, :] = 0.0
+    B[:, 7] = 0.0
+    ref = scheme.dgemm(A, B, N)
+    res = run(A, B, N, transa, transb, ldc_pad=3)
+    mask = _compare(res, ref, A, B, N)
+    assert mask.mean() > 0.98
+    assert np.all(res["C_pad"] == 0.0)           # ldc padding untouched
+    rel = np.linalg.norm(res["C"] - ref.C) / np.linalg.norm(ref.C)
+    assert rel <= 1e-15
+
+
+@pytest.mark.parametrize("N", [2, 6, 12, 16, 20])
+def test_imported_exponents_bit_exact(dev, N):
+    """Oracle exponents fed to the GPU (oracle -> GPU only): every residue and every
+    output element bit-exact, including huge |A'| (>= 2^63 for N >= 14)."""
+    from gpu_helpers import run
+    m, k, n = 130, 257, 260
+    A = gen_host(m, k, "phi", phi=2.0, seed=5)
+    B = gen_host(k, n, "phi", phi=2.0, seed=6)
+    ref = scheme.dgemm(A, B, N)
+    res = run(A, B, N, e_mu_in=ref.e_mu, e_nu_in=ref.e_nu)
+    for l in range(N):
+        assert np.array_equal(res["residues"][l], ref.residues[l]), l
+    assert np.array_equal(res["C"], ref.C)
+
+
+def test_alpha_beta_and_quick_returns(dev):
+    from gpu_helpers import run
+    m, k, n = 70, 90, 80
+    A = gen_host(m, k, "phi", phi=1.0, seed=8)
+    B = gen_host(k, n, "phi", phi=1.0, seed=9)
+    C0 = gen_host(m, n, "uniform", seed=10)
+    ref = scheme.dgemm(A, B, 12, alpha=-1.5, beta=0.25, C=C0)
+    res = run(A, B, 12, alpha=-1.5, beta=0.25, C0=C0)
+    assert np.array_equal(res["C"], ref.C)
+    res0 = run(A, B, 12, alpha=0.0, beta=2.0, C0=C0)
+    assert np.array_equal(res0["C"], 2.0 * C0)
+    Ak = np.zeros((m, 0))
+    Bk = np.zeros((0, n))
+    resk = run(Ak, Bk, 12, alpha=1.0, beta=0.0, C0=C0)
+    assert np.all(resk["C"] == 0.0)
+
+
+def test_identity_and_integer_exact(dev):
+    from gpu_helpers import run
+    I = np.eye(40)
+    assert np.array_equal(run(I, I, 12)["C"], I)
+    A = gen_host(16, 64, "int", seed=1)
+    B = gen_host(64, 16, "int", seed=2)
+    want = (A.astype(object).dot(B.astype(object))).astype(np.float64)
+    assert np.array_equal(run(A, B, 12)["C"], want)
+
+
+def test_nonfinite_status(dev):
+    from gpu_helpers import run
+    A = gen_host(20, 30, "uniform", seed=1)
+    B = gen_host(30, 10, "uniform", seed=2)
+    A[3, 4] = np.nan
+    res = run(A, B, 12)
+    assert res["status"] == dev.OZ2_ERR_NONFINITE
+
+
+def test_host_pointer_path(dev):
+    """Host (numpy) buffers through the same C ABI give the same bits as device ones."""
+    from gpu_helpers import run
+    m, k, n = 150, 200, 170
+    A = np.asfortranarray(gen_host(m, k, "phi", phi=1.0, seed=11))
+    B = np.asfortranarray(gen_host(k, n, "phi", phi=1.0, seed=12))
+    C = np.asfortranarray(np.zeros((m, n)))
+    rc = dev.oz2_dgemm("N", "N", m, n, k, 1.0, A.ctypes.data, m, B.ctypes.data, k, 0.0, C.ctypes.data, m, 13)
+    assert rc == 0
+    assert np.array_equal(C, run(A, B, 13)["C"])
+
+
+def test_torch_wrapper_layouts(dev):
+    import torch
+    A = torch.from_numpy(gen_host(100, 120, "phi", phi=1.0, seed=13, order="C")).cuda()
+    B = torch.from_numpy(gen_host(120, 90, "phi", phi=1.0, seed=14, order="C")).cuda()
+    C1 = dev.dgemm(A, B, num_moduli=13)
+    C2 = dev.dgemm(A.t().contiguous().t(), B.t().contiguous().t(), num_moduli=13)
+    ref = A @ B
+    assert torch.equal(C1, C2)
+    assert (torch.linalg.norm(C1 - ref) / torch.linalg.norm(ref)).item() < 1e-14
+    C3 = torch.zeros(100, 90, dtype=torch.float64, device="cuda")     # row-major C
+    dev.dgemm(A, B, C=C3, num_moduli=13)
+    assert (torch.linalg.norm(C3 - ref) / torch.linalg.norm(ref)).item() < 1e-14
