@@ -1,13 +1,21 @@
 // gemm_kernel.cu -- the FP8 (E4M3 x E4M3 -> FP32) GEMMs of the FP8 Ozaki-II scheme on
-// 5th-generation tensor cores (tcgen05.mma kind::f8f6f4), one persistent CTA per SM.
+// 5th-generation tensor cores (tcgen05.mma kind::f8f6f4), persistent, one CTA per SM.
 //
-// Roles (320 threads):
-//   warp 0      TMA producer: A tile 128 x 128 B and B tile 256 x 128 B per stage,
-//               128-byte swizzle, 4-stage mbarrier ring
-//   warp 1      TMEM allocator + single-thread MMA issuer: 4 x (M=128, N=256, K=32)
-//               MMAs per stage into one of two 256-column FP32 accumulators in TMEM
-//   warps 2..9  epilogue: tcgen05.ld 32 lanes x 32 columns, each warp owns a TMEM lane
-//               quadrant (warp % 4) and one 128-column half of the tile
+// CG = 1: one CTA computes a 128 x 256 tile (UMMA M=128, N=256).
+// CG = 2: a cluster of two CTAs on one TPC computes a 256 x 256 tile with
+//         tcgen05.mma.cta_group::2 (UMMA M=256, N=256) issued by the leader CTA: each
+//         CTA stages its own 128 rows of A and half (128 rows) of B^T, the tensor core
+//         reads both halves, and each CTA's TMEM receives its 128 rows x 256 columns.
+//         Per SM this halves the B bytes moved from L2 and read from shared memory.
+//
+// Roles (320 threads per CTA):
+//   warp 0      TMA producer (K-major operand tiles, 128-byte swizzle, NSTAGE-deep ring)
+//   warp 1      TMEM allocator + single-thread MMA issuer (leader CTA only for CG = 2):
+//               4 x K=32 MMAs per 128-byte K stage into one of two 256-column FP32
+//               accumulators in TMEM (double buffer: the epilogue of product g overlaps
+//               the MMAs of product g+1)
+//   warps 2..9  epilogue: tcgen05.ld 32 lanes x 32 columns; warp w reads TMEM lane
+//               quadrant w % 4 and one 128-column half of the tile
 //
 // Modes:
 //   MODE_RESIDUE  for every tile and every modulus l the three exact products of
@@ -15,19 +23,30 @@
 //                 or eq. C'-Karatsuba P:241-246 (non-square: A^x B^x, x = 1..3 with
 //                 weights 256-16, 1-16, 16) run back to back; the epilogue reduces
 //                 each FP32 accumulator mod p (exact: entries are integers <= 2^24,
-//                 eq. error-free-FP8-matmult) and accumulates the weighted partial in
-//                 registers; after the third product it writes C'_l = mod(.., p) as
-//                 int16 [l][j][i].  The FP32 products never leave TMEM.
+//                 eq. error-free-FP8-matmult), accumulates the weighted partial in
+//                 registers (binary16 pairs, exact below 2048) and after the third
+//                 product stores C'_l = mod(.., p) as int16 [l][j][i].  The FP32
+//                 products never leave TMEM.
 //   MODE_BOUND    C-bar' = A-bar B-bar; the epilogue keeps only the row and
 //                 column maxima (atomicMax on non-negative float bits).
 //   MODE_RAW      diagnostic: writes the FP32 accumulator.
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 #include "oz2_internal.h"
 #include "oz2_ptx.cuh"
-#include <cuda_fp16.h>
 
 namespace oz2 {
+
+template <int CG>
+struct GemmCfg {
+    static constexpr int TILE_M = BM * CG;            // output rows per (cluster) tile
+    static constexpr int B_ROWS = BN / CG;            // B^T rows staged per CTA
+    static constexpr int A_STAGE = BM * BK;
+    static constexpr int B_STAGE = B_ROWS * BK;
+    static constexpr int NSTAGE = CG == 1 ? STAGES : STAGES2;
+    static constexpr int SMEM = NSTAGE * (A_STAGE + B_STAGE) + 1024 + 256;
+};
 
 __device__ __forceinline__ void tile_coords(int t, int m_tiles, int n_tiles, int& tm, int& tn) {
     // groups of 16 tile-rows swept column by column: concurrently running CTAs share
@@ -41,80 +60,175 @@ __device__ __forceinline__ void tile_coords(int t, int m_tiles, int n_tiles, int
     tn = in / gm;
 }
 
-template <int MODE>
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// 2-SM TMA: bytes land in this CTA's smem, completion is counted on the leader's barrier
+__device__ __forceinline__ void tma_load_2d_cg2(const CUtensorMap* m, uint32_t leader_bar, void* smem,
+                                                int32_t c0, int32_t c1, uint64_t cache_hint) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;"
+        ::"r"(smem_u32(smem)), "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar),
+          "r"(c0), "r"(c1), "l"(cache_hint)
+        : "memory");
+}
+__device__ __forceinline__ void mma_f8f6f4_cg2(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                               uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
+}
+// arrive on the barrier at the same smem offset in both CTAs of the pair
+__device__ __forceinline__ void mma_commit_cg2(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .b16 msk;\n\tmov.b16 msk, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], msk;\n\t}"
+        ::"r"(smem_u32(bar)) : "memory");
+}
+template <int CG>
+__device__ __forceinline__ void tmem_alloc_cg(uint32_t* dst_smem, uint32_t ncols) {
+    if (CG == 1) {
+        tmem_alloc(dst_smem, ncols);
+    } else {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                     ::"r"(smem_u32(dst_smem)), "r"(ncols) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+}
+template <int CG>
+__device__ __forceinline__ void tmem_dealloc_cg(uint32_t taddr, uint32_t ncols) {
+    if (CG == 1) tmem_dealloc(taddr, ncols);
+    else asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+template <int MODE, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
             const __grid_constant__ GemmParams P) {
+    using Cfg = GemmCfg<CG>;
+    constexpr int NS = Cfg::NSTAGE;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
-    uint8_t* sB = smem + STAGES * SMEM_A_STAGE;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * SMEM_B_STAGE);
-    uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;
+    uint8_t* sB = smem + NS * Cfg::A_STAGE;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + NS * Cfg::B_STAGE);
+    uint64_t* empty = full + NS;
+    uint64_t* tfull = empty + NS;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const uint32_t warp = warp_id_uniform();
     const uint32_t lane = lane_id();
+    const uint32_t rank = (CG == 2) ? cluster_rank() : 0u;
+    const bool leader = rank == 0;
 
     if (warp == 0) {
         if (elect_one()) {
             tma_prefetch_desc(&tmA);
             tma_prefetch_desc(&tmB);
-            for (int s = 0; s < STAGES; ++s) {
-                mbar_init(&full[s], 1);
+            for (int s = 0; s < NS; ++s) {
+                mbar_init(&full[s], CG);          // CG = 2: leader expect_tx + peer arrive
                 mbar_init(&empty[s], 1);
             }
             for (int s = 0; s < 2; ++s) {
                 mbar_init(&tfull[s], 1);
-                mbar_init(&tempty[s], 8);
+                mbar_init(&tempty[s], 8 * CG);    // every epilogue warp of the pair
             }
             fence_mbar_init();
         }
         __syncwarp();
     } else if (warp == 1) {
-        tmem_alloc(tmem_slot, 512);
+        tmem_alloc_cg<CG>(tmem_slot, 512);
     }
     tc_fence_before();
-    __syncthreads();
+    if (CG == 2) cluster_sync_all();
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     const int num_tiles = P.m_tiles * P.n_tiles;
     const int prods = (MODE == MODE_RESIDUE) ? 3 * P.num_moduli : 1;
     const int nkb = P.num_k_blocks;
+    const int unit = blockIdx.x / CG;            // tile-processing unit (CTA or CTA pair)
+    const int units = gridDim.x / CG;
 
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
         if (elect_one()) {
             uint32_t stage = 0, phase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            long long g = 0;                         // throttle chunks started by this unit
+            const long long nunits = units;
+            const int kc = P.sync_chunk > 0 ? P.sync_chunk : nkb;   // k-blocks per chunk
+            const long long chunks_per_prod = (nkb + kc - 1) / kc;
+            const uint32_t full0 = smem_u32(&full[0]) & 0xFEFFFFFFu;   // leader's barrier (CG=2)
+            for (int tile = unit; tile < num_tiles; tile += units) {
                 int tm, tn;
                 tile_coords(tile, P.m_tiles, P.n_tiles, tm, tn);
                 for (int pr = 0; pr < prods; ++pr) {
-                    int a_row = tm * BM, b_row = tn * BN;
+                    int a_row = tm * Cfg::TILE_M + static_cast<int>(rank) * BM;
+                    int b_row = tn * BN + static_cast<int>(rank) * Cfg::B_ROWS;
                     if (MODE == MODE_RESIDUE) {
                         const int l = pr / 3, x = pr - 3 * (pr / 3);
                         a_row += P.mod[l].a_plane[x] * P.rows_per_plane_a;
                         b_row += P.mod[l].b_plane[x] * P.rows_per_plane_b;
                     }
                     for (int kb = 0; kb < nkb; ++kb) {
+                        if (P.sync_lead > 0 && kb % kc == 0) {
+                            // progress throttle: a unit may not run more than sync_lead chunks
+                            // (sync_chunk k-blocks each) ahead of the chip-wide average, so
+                            // the operand panels streamed by all units stay L2-resident
+                            // until every unit sharing them has read them
+                            if (leader) atomicAdd(P.progress, 1ull);
+                            const long long need = nunits * (g + 1 - P.sync_lead);
+                            while (static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(P.progress)) < need)
+                                __nanosleep(128);
+                            ++g;
+                        }
                         mbar_wait(&empty[stage], phase ^ 1);
-                        mbar_arrive_expect_tx(&full[stage], SMEM_A_STAGE + SMEM_B_STAGE);
-                        tma_load_2d(&tmA, &full[stage], sA + stage * SMEM_A_STAGE, kb * BK, a_row, kEvictNormal);
-                        tma_load_2d(&tmB, &full[stage], sB + stage * SMEM_B_STAGE, kb * BK, b_row, kEvictNormal);
-                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                        if (CG == 1) {
+                            mbar_arrive_expect_tx(&full[stage], Cfg::A_STAGE + Cfg::B_STAGE);
+                            tma_load_2d(&tmA, &full[stage], sA + stage * Cfg::A_STAGE, kb * BK, a_row, kEvictNormal);
+                            tma_load_2d(&tmB, &full[stage], sB + stage * Cfg::B_STAGE, kb * BK, b_row, kEvictNormal);
+                        } else {
+                            const uint32_t lb = full0 + stage * 8u;
+                            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (Cfg::A_STAGE + Cfg::B_STAGE));
+                            else mbar_arrive_cluster(lb);
+                            tma_load_2d_cg2(&tmA, lb, sA + stage * Cfg::A_STAGE, kb * BK, a_row, kEvictNormal);
+                            tma_load_2d_cg2(&tmB, lb, sB + stage * Cfg::B_STAGE, kb * BK, b_row, kEvictNormal);
+                        }
+                        if (++stage == NS) { stage = 0; phase ^= 1; }
                     }
                 }
+            }
+            if (P.sync_lead > 0 && leader) {
+                // finished: count as having started every product so nobody waits on us
+                const long long gmax = static_cast<long long>((num_tiles + units - 1) / units) * prods * chunks_per_prod;
+                if (gmax > g) atomicAdd(P.progress, static_cast<unsigned long long>(gmax - g));
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        if (elect_one()) {
-            constexpr uint32_t idesc = make_idesc_e4m3_f32(BM, BN);
+        if (leader && elect_one()) {
+            constexpr uint32_t idesc = make_idesc_e4m3_f32(Cfg::TILE_M, BN);
             uint32_t stage = 0, phase = 0, g = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            for (int tile = unit; tile < num_tiles; tile += units) {
                 for (int pr = 0; pr < prods; ++pr, ++g) {
                     const uint32_t slot = g & 1u, use = g >> 1;
                     mbar_wait(&tempty[slot], (use & 1u) ^ 1u);
@@ -123,17 +237,20 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     for (int kb = 0; kb < nkb; ++kb) {
                         mbar_wait(&full[stage], phase);
                         tc_fence_after();
-                        const uint64_t a0 = make_desc_k128_sw128(smem_u32(sA + stage * SMEM_A_STAGE));
-                        const uint64_t b0 = make_desc_k128_sw128(smem_u32(sB + stage * SMEM_B_STAGE));
+                        const uint64_t a0 = make_desc_k128_sw128(smem_u32(sA + stage * Cfg::A_STAGE));
+                        const uint64_t b0 = make_desc_k128_sw128(smem_u32(sB + stage * Cfg::B_STAGE));
 #pragma unroll
                         for (int kk = 0; kk < BK / 32; ++kk) {
                             // advance 32 bytes of K inside the 128-byte swizzle atom
-                            mma_f8f6f4(d_tmem, a0 + 2 * kk, b0 + 2 * kk, idesc, (kb | kk) != 0);
+                            if (CG == 1) mma_f8f6f4(d_tmem, a0 + 2 * kk, b0 + 2 * kk, idesc, (kb | kk) != 0);
+                            else mma_f8f6f4_cg2(d_tmem, a0 + 2 * kk, b0 + 2 * kk, idesc, (kb | kk) != 0);
                         }
-                        mma_commit(&empty[stage]);
-                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                        if (CG == 1) mma_commit(&empty[stage]);
+                        else mma_commit_cg2(&empty[stage]);
+                        if (++stage == NS) { stage = 0; phase ^= 1; }
                     }
-                    mma_commit(&tfull[slot]);
+                    if (CG == 1) mma_commit(&tfull[slot]);
+                    else mma_commit_cg2(&tfull[slot]);
                 }
             }
         }
@@ -141,12 +258,22 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         // ------------------------------------------------------------ epilogue
         const uint32_t quad = warp & 3u;           // TMEM lane quadrant this warp may access
         const uint32_t half = (warp - 2u) >> 2;    // 128-column half of the 256-column tile
-        const uint32_t row_in_tile = quad * 32u + lane;
+        const uint32_t row_in_tile = rank * BM + quad * 32u + lane;
+        const uint32_t tempty0 = (CG == 2) ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
+        auto release_slot = [&](uint32_t slot) {
+            // accumulator slot drained: hand it back to the (leader's) MMA warp
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (CG == 1) mbar_arrive(&tempty[slot]);
+                else mbar_arrive_cluster(tempty0 + slot * 8u);
+            }
+        };
         uint32_t g = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        for (int tile = unit; tile < num_tiles; tile += units) {
             int tm, tn;
             tile_coords(tile, P.m_tiles, P.n_tiles, tm, tn);
-            const int64_t row = static_cast<int64_t>(tm) * BM + row_in_tile;
+            const int64_t row = static_cast<int64_t>(tm) * Cfg::TILE_M + row_in_tile;
             const int64_t col0 = static_cast<int64_t>(tn) * BN + half * 128u;
             if (MODE == MODE_RESIDUE) {
                 for (int l = 0; l < P.num_moduli; ++l) {
@@ -168,6 +295,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                             uint32_t v[32];
                             tmem_ld_32x32b_x32(taddr + c * 32, v);
                             tmem_ld_wait();
+                            if (c == 3) release_slot(slot);   // the whole slot is in registers
 #pragma unroll
                             for (int j = 0; j < 32; j += 2) {
                                 float acc[2];
@@ -198,16 +326,12 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                                         if (2.0f * r >= p) r -= p;
                                         else if (2.0f * r < -p) r += p;
                                         const int jj = c * 32 + j + u;
-                                        if (row_ok && col0 + jj < P.n)
-                                            out[static_cast<int64_t>(jj) * P.m] = static_cast<int16_t>(r);
+                                        if (row_ok && col0 + jj < P.n)       // streamed: read once by the CRT
+                                            __stcs(out + static_cast<int64_t>(jj) * P.m, static_cast<short>(r));
                                     }
                                 }
                             }
                         }
-                        // accumulator slot drained: hand it back to the MMA warp
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&tempty[slot]);
                     }
                 }
             } else {
@@ -239,9 +363,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         }
                     }
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[slot]);
+                release_slot(slot);
                 ++g;
                 if (MODE == MODE_BOUND && row < P.m && rowmax > 0.0f)
                     atomicMax(P.rmax + row, __float_as_uint(rowmax));
@@ -250,48 +372,61 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     }
 
     tc_fence_before();
-    __syncthreads();
+    if (CG == 2) cluster_sync_all();
+    else __syncthreads();
     if (warp == 1) {
         __syncwarp();
         tc_fence_after();
-        tmem_dealloc(tmem_base, 512);
+        tmem_dealloc_cg<CG>(tmem_base, 512);
     }
 }
 
-static bool g_attr_set[3] = {false, false, false};
-
-cudaError_t launch_gemm(int mode, const CUtensorMap& ta, const CUtensorMap& tb,
-                        const GemmParams& gp, int num_sms, cudaStream_t st) {
+template <int MODE, int CG>
+static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& gp,
+                              int num_sms, cudaStream_t st) {
+    static bool attr_set = false;
+    using Cfg = GemmCfg<CG>;
     const int num_tiles = gp.m_tiles * gp.n_tiles;
     if (num_tiles == 0) return cudaSuccess;
-    const int grid = num_tiles < num_sms ? num_tiles : num_sms;
-    cudaError_t err = cudaSuccess;
-    switch (mode) {
-        case MODE_RESIDUE:
-            if (!g_attr_set[0]) {
-                err = cudaFuncSetAttribute(gemm_kernel<MODE_RESIDUE>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
-                if (err != cudaSuccess) return err;
-                g_attr_set[0] = true;
-            }
-            gemm_kernel<MODE_RESIDUE><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(ta, tb, gp);
-            break;
-        case MODE_BOUND:
-            if (!g_attr_set[1]) {
-                err = cudaFuncSetAttribute(gemm_kernel<MODE_BOUND>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
-                if (err != cudaSuccess) return err;
-                g_attr_set[1] = true;
-            }
-            gemm_kernel<MODE_BOUND><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(ta, tb, gp);
-            break;
-        default:
-            if (!g_attr_set[2]) {
-                err = cudaFuncSetAttribute(gemm_kernel<MODE_RAW>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
-                if (err != cudaSuccess) return err;
-                g_attr_set[2] = true;
-            }
-            gemm_kernel<MODE_RAW><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(ta, tb, gp);
-            break;
+    const int max_units = num_sms / CG;
+    const int units = num_tiles < max_units ? num_tiles : max_units;
+    if (!attr_set) {
+        cudaError_t err = cudaFuncSetAttribute(gemm_kernel<MODE, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+        if (err != cudaSuccess) return err;
+        attr_set = true;
     }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(units * CG);
+    cfg.blockDim = dim3(GEMM_THREADS);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, CG>, ta, tb, gp);
+}
+
+cudaError_t launch_gemm(int mode, int cg, const CUtensorMap& ta, const CUtensorMap& tb,
+                        const GemmParams& gp, int num_sms, cudaStream_t st) {
+    cudaError_t err;
+    if (cg == 2) {
+        switch (mode) {
+            case MODE_RESIDUE: err = launch_one<MODE_RESIDUE, 2>(ta, tb, gp, num_sms, st); break;
+            case MODE_BOUND: err = launch_one<MODE_BOUND, 2>(ta, tb, gp, num_sms, st); break;
+            default: err = launch_one<MODE_RAW, 2>(ta, tb, gp, num_sms, st); break;
+        }
+    } else {
+        switch (mode) {
+            case MODE_RESIDUE: err = launch_one<MODE_RESIDUE, 1>(ta, tb, gp, num_sms, st); break;
+            case MODE_BOUND: err = launch_one<MODE_BOUND, 1>(ta, tb, gp, num_sms, st); break;
+            default: err = launch_one<MODE_RAW, 1>(ta, tb, gp, num_sms, st); break;
+        }
+    }
+    if (err != cudaSuccess) return err;
     return cudaGetLastError();
 }
 

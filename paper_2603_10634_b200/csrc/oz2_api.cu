@@ -3,6 +3,7 @@
 // launch sequence of the FP8 Ozaki-II pipeline.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -116,7 +117,10 @@ static Plan build_plan(int N) {
     for (int p : pl.p) big_mul_small(P, static_cast<uint32_t>(p));
     pl.P = P;
     const int nb = big_bitlen(P);
-    pl.L = (nb + 1 + 31) / 32;
+    // two's complement over L limbs must hold (-1.5 P, 1.5 P): 32 L >= nb + 2; at least
+    // 4 limbs (the CRT kernel is instantiated for L = 4..10)
+    pl.L = (nb + 2 + 31) / 32;
+    if (pl.L < 4) pl.L = 4;
     // P' = RD32((log2(P-1) - 1)/2)
     Big Pm1 = P;
     for (auto& x : Pm1) { if (x--) break; }    // P - 1 (P > 0)
@@ -144,7 +148,7 @@ static Plan build_plan(int N) {
         big_mul_small(w, static_cast<uint32_t>(q));
         pl.w.push_back(w);
         cp.p[l] = p;
-        cp.qp[l] = static_cast<double>(q) / static_cast<double>(p);
+        cp.qp32[l] = static_cast<uint32_t>((static_cast<uint64_t>(q) << 32) / static_cast<uint64_t>(p));
         for (int t = 0; t < pl.L && t < static_cast<int>(w.size()); ++t) cp.w[l][t] = w[t];
     }
     for (int t = 0; t < pl.L && t < static_cast<int>(P.size()); ++t) cp.P[t] = P[t];
@@ -342,6 +346,19 @@ static bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// tuning knobs (read per call; defaults are the measured best)
+static int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+static int sync_lead() {   // progress throttle of the residue GEMM (OZ2_SYNC_LEAD)
+    const int v = env_int("OZ2_SYNC_LEAD", 2);
+    return v < 0 ? 0 : v;
+}
+static int cta_group() {   // 1: 128x256 CTA tiles; 2: 256x256 CTA-pair tiles (OZ2_CG)
+    return env_int("OZ2_CG", 1) == 2 ? 2 : 1;
+}
+
 static void phase_mark(int i) {
     if (!g_ts.timing) return;
     if (!g_ts.ev[i]) cudaEventCreate(&g_ts.ev[i]);
@@ -409,17 +426,18 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
         // ---- step 2: bound GEMM C-bar' = A-bar B-bar, row/column maxima
         phase_mark(1);
         {
+            const int cg = cta_group();
             CUtensorMap ta, tb;
             if (!make_map(&ta, abar, L.k_pad, L.m_pad, L.k_pad, BK, BM)) return OZ2_ERR_CUDA;
-            if (!make_map(&tb, bbar, L.k_pad, L.n_pad, L.k_pad, BK, BN)) return OZ2_ERR_CUDA;
+            if (!make_map(&tb, bbar, L.k_pad, L.n_pad, L.k_pad, BK, BN / cg)) return OZ2_ERR_CUDA;
             GemmParams gp;
             std::memset(&gp, 0, sizeof(gp));
             gp.m = static_cast<int>(m); gp.n = static_cast<int>(n);
             gp.num_k_blocks = static_cast<int>(L.k_pad / BK);
-            gp.m_tiles = static_cast<int>(L.m_pad / BM); gp.n_tiles = static_cast<int>(L.n_pad / BN);
+            gp.m_tiles = static_cast<int>(L.m_pad / (BM * cg)); gp.n_tiles = static_cast<int>(L.n_pad / BN);
             gp.rows_per_plane_a = static_cast<int>(L.m_pad); gp.rows_per_plane_b = static_cast<int>(L.n_pad);
             gp.rmax = rsmax; gp.smax = rsmax + m;
-            OZ2_CK(launch_gemm(MODE_BOUND, ta, tb, gp, g_ts.num_sms, st));
+            OZ2_CK(launch_gemm(MODE_BOUND, cg, ta, tb, gp, g_ts.num_sms, st));
         }
         if (opt && opt->rmax) OZ2_CK(cudaMemcpyAsync(opt->rmax, rsmax, 4 * m, cudaMemcpyDeviceToDevice, st));
         if (opt && opt->smax) OZ2_CK(cudaMemcpyAsync(opt->smax, rsmax + m, 4 * n, cudaMemcpyDeviceToDevice, st));
@@ -453,17 +471,24 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
     // ---- step 5: 3N exact FP8 GEMMs with the modular epilogue
     phase_mark(4);
     {
+        const int cg = cta_group();
         CUtensorMap ta, tb;
         if (!make_map(&ta, digA, L.k_pad, static_cast<uint64_t>(pl->M) * L.m_pad, L.k_pad, BK, BM)) return OZ2_ERR_CUDA;
-        if (!make_map(&tb, digB, L.k_pad, static_cast<uint64_t>(pl->M) * L.n_pad, L.k_pad, BK, BN)) return OZ2_ERR_CUDA;
+        if (!make_map(&tb, digB, L.k_pad, static_cast<uint64_t>(pl->M) * L.n_pad, L.k_pad, BK, BN / cg)) return OZ2_ERR_CUDA;
         GemmParams gp = pl->gemm_mod;
         gp.m = static_cast<int>(m); gp.n = static_cast<int>(n);
         gp.num_k_blocks = static_cast<int>(L.k_pad / BK);
-        gp.m_tiles = static_cast<int>(L.m_pad / BM); gp.n_tiles = static_cast<int>(L.n_pad / BN);
+        gp.m_tiles = static_cast<int>(L.m_pad / (BM * cg)); gp.n_tiles = static_cast<int>(L.n_pad / BN);
         gp.rows_per_plane_a = static_cast<int>(L.m_pad); gp.rows_per_plane_b = static_cast<int>(L.n_pad);
         gp.num_moduli = N;
         gp.residues = res;
-        OZ2_CK(launch_gemm(MODE_RESIDUE, ta, tb, gp, g_ts.num_sms, st));
+        gp.sync_lead = sync_lead();
+        gp.sync_chunk = env_int("OZ2_SYNC_CHUNK", 16);
+        if (gp.sync_lead > 0) {
+            gp.progress = reinterpret_cast<unsigned long long*>(maxbits);   // dead after step 3
+            OZ2_CK(cudaMemsetAsync(gp.progress, 0, 8, st));
+        }
+        OZ2_CK(launch_gemm(MODE_RESIDUE, cg, ta, tb, gp, g_ts.num_sms, st));
     }
     if (opt && opt->residues)
         OZ2_CK(cudaMemcpyAsync(opt->residues, res, 2ull * N * m * n, cudaMemcpyDeviceToDevice, st));
@@ -664,16 +689,17 @@ int oz2_fp8_gemm_raw(const uint8_t* a, const uint8_t* b, float* C32, int64_t m, 
     if (e) return e;
     if (k == 0) { OZ2_CK(cudaMemsetAsync(C32, 0, 4ull * m * n, g_ts.stream)); return OZ2_SUCCESS; }
     if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15u) return OZ2_ERR_NOT_SUPPORTED;
+    const int cg = cta_group();
     CUtensorMap ta, tb;
     if (!make_map(&ta, a, k, m, k, BK, BM)) return OZ2_ERR_CUDA;
-    if (!make_map(&tb, b, k, n, k, BK, BN)) return OZ2_ERR_CUDA;
+    if (!make_map(&tb, b, k, n, k, BK, BN / cg)) return OZ2_ERR_CUDA;
     GemmParams gp;
     std::memset(&gp, 0, sizeof(gp));
     gp.m = static_cast<int>(m); gp.n = static_cast<int>(n);
     gp.num_k_blocks = static_cast<int>((k + BK - 1) / BK);
-    gp.m_tiles = static_cast<int>((m + BM - 1) / BM); gp.n_tiles = static_cast<int>((n + BN - 1) / BN);
+    gp.m_tiles = static_cast<int>((m + BM * cg - 1) / (BM * cg)); gp.n_tiles = static_cast<int>((n + BN - 1) / BN);
     gp.c32 = C32;
-    OZ2_CK(launch_gemm(MODE_RAW, ta, tb, gp, g_ts.num_sms, g_ts.stream));
+    OZ2_CK(launch_gemm(MODE_RAW, cg, ta, tb, gp, g_ts.num_sms, g_ts.stream));
     return OZ2_SUCCESS;
 }
 

@@ -16,11 +16,11 @@ constexpr int kPow2Tab = 1024;   // 2^E mod p for E in [0, 1024)
 constexpr int BM = 128;          // rows of A per CTA tile (TMEM lanes)
 constexpr int BN = 256;          // rows of B^T per CTA tile (TMEM columns per slot)
 constexpr int BK = 128;          // bytes (= E4M3 elements) of K per pipeline stage
-constexpr int STAGES = 4;
+constexpr int STAGES = 4;        // CG = 1: 48 KiB per stage
+constexpr int STAGES2 = 6;       // CG = 2: 32 KiB per stage per CTA
 constexpr int SMEM_A_STAGE = BM * BK;   // 16 KiB
 constexpr int SMEM_B_STAGE = BN * BK;   // 32 KiB
 constexpr int GEMM_THREADS = 320;       // warp0 TMA, warp1 MMA, warps 2..9 epilogue
-constexpr int GEMM_SMEM = STAGES * (SMEM_A_STAGE + SMEM_B_STAGE) + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int PAD_M = 256;       // row padding of operand planes (tile multiple)
 constexpr int PAD_N = 256;
 constexpr int PAD_K = 128;
@@ -45,6 +45,9 @@ struct GemmParams {
     uint32_t* rmax;              // [m] float bits (bound)
     uint32_t* smax;              // [n]
     float* c32;                  // raw: [m][n]
+    unsigned long long* progress;  // chip-wide product counter (progress throttle)
+    int sync_lead;               // 0 = off; else max chunks ahead of the chip-wide average
+    int sync_chunk;              // k-blocks per throttle chunk (0 = one chunk per product)
     ModEpi mod[kMaxModuli];
 };
 
@@ -67,7 +70,7 @@ struct DigitParams {
 struct CrtParams {
     int num_moduli;
     int p[kMaxModuli];
-    double qp[kMaxModuli];                       // q_l / p_l
+    uint32_t qp32[kMaxModuli];                   // round(2^32 q_l / p_l)
     uint32_t w[kMaxModuli][kMaxLimbs];           // w_l mod 2^(32L)
     uint32_t np[kMaxLimbs];                      // 2^(32L) - P
     uint32_t P[kMaxLimbs];
@@ -91,7 +94,7 @@ cudaError_t launch_exps(const unsigned long long* maxbits, const int32_t* eprime
 cudaError_t launch_digits(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
                           const int32_t* e, const DigitParams& dp, uint8_t* planes,
                           int64_t rows_pad, int64_t k_pad, cudaStream_t st);
-cudaError_t launch_gemm(int mode, const CUtensorMap& ta, const CUtensorMap& tb,
+cudaError_t launch_gemm(int mode, int cg, const CUtensorMap& ta, const CUtensorMap& tb,
                         const GemmParams& gp, int num_sms, cudaStream_t st);
 cudaError_t launch_crt(int limbs, const int16_t* res, int64_t m, int64_t n, const CrtParams& cp,
                        const int32_t* e_mu, const int32_t* e_nu, double alpha, double beta,

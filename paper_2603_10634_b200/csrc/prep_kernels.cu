@@ -186,8 +186,117 @@ __global__ void k_exps(const unsigned long long* __restrict__ maxbits,
 
 // ---------------------------------------------------------------------------------
 // k_digits: X' = trunc(2^e x) (exact), r_l = mod(X', p_l), FP8 digits
+//
+// Arithmetic is arranged to stay on the FP64/FP32/INT pipes (no conversion-pipe
+// instructions except the final E4M3 packing):
+//   * 2^e scaling by two exact power-of-two multiplies, truncation by an RZ add of 2^52;
+//   * q = round(M/p) by fma(M, 1/p, 1.5*2^52) - 1.5*2^52, r = fma(-q, p, M) exact,
+//     and r read as an int from the low word of r + 1.5*2^52;
+//   * int -> float by the 1.5*2^23 bit trick, round / ceil of r/s by magic adds.
 
-template <bool KMAJOR>
+__device__ __forceinline__ double pow2d(int e) {          // 2^e, |e| <= 1022
+    return __longlong_as_double(static_cast<long long>(e + 1023) << 52);
+}
+__device__ __forceinline__ float i2f_small(int v) {       // exact for |v| < 2^22
+    return __int_as_float(0x4B400000 + v) - 12582912.0f;
+}
+constexpr double kMagic52 = 6755399441055744.0;           // 1.5 * 2^52
+constexpr float kMagic23 = 12582912.0f;                   // 1.5 * 2^23
+
+__device__ __forceinline__ double dfma_rn(double a, double b, double c) {   // keeps b, c in registers
+    double d;
+    asm("fma.rn.f64 %0, %1, %2, %3;" : "=d"(d) : "d"(a), "d"(b), "d"(c));
+    return d;
+}
+
+// residue and digits of one modulus for the 4 elements of a lane; NSTEP = 1: |y| < 2^59,
+// NSTEP = 2: |y| < 2^96 (first reduced modulo Q = p 2^36, exactly), NSTEP = 0: the
+// general M 2^E form with (2^E mod p) from the table (any |y|).
+template <int NSTEP>
+__device__ __forceinline__ void digits_one_modulus(const ModDig& md, int l, const double (&y)[4],
+                                                   const double (&M)[4], const int (&E)[4],
+                                                   const uint16_t* __restrict__ pow2tab,
+                                                   uint8_t* out, int64_t plane_stride) {
+    const int p = static_cast<int>(md.p_f);
+    const double pinv = md.pinv_d, pd = md.p_d, magic = kMagic52;
+    float rf[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        int ri;
+        if (NSTEP == 0) {
+            const double qq = dfma_rn(M[q], pinv, magic) - magic;
+            const double rd = fma(-qq, pd, M[q]);
+            ri = __double2loint(rd + magic);
+            const int tw = __ldg(pow2tab + l * kPow2Tab + min(E[q], kPow2Tab - 1));
+            const float v = i2f_small(ri * tw);                           // |.| < 2^21
+            const float qv = fmaf(v, md.pinv_f, kMagic23) - kMagic23;
+            ri = __float_as_int(fmaf(-qv, md.p_f, v) + kMagic23) - 0x4B400000;
+            if (y[q] < 0.0) ri = -ri;
+        } else {
+            double yy = y[q];
+            if (NSTEP == 2) {
+                const double Q = pd * 68719476736.0, Qinv = pinv * (1.0 / 68719476736.0);  // p 2^36
+                const double q1 = dfma_rn(yy, Qinv, magic) - magic;
+                yy = fma(-q1, Q, yy);                                     // exact, |yy| < 1.5 Q
+            }
+            const double qq = dfma_rn(yy, pinv, magic) - magic;           // round(y/p) (+-1)
+            const double rd = fma(-qq, pd, yy);                           // exact, |rd| < 1.5 p
+            ri = __double2loint(rd + magic);
+        }
+        // symmetric range [-floor(p/2), ceil(p/2)-1] (R2)
+        if (2 * ri >= p) ri -= p;
+        else if (2 * ri < -p) ri += p;
+        rf[q] = i2f_small(ri);
+    }
+    uint8_t* o = out + static_cast<int64_t>(md.plane0) * plane_stride;
+    if (md.square) {
+        // D1 = round(r/s) ties-to-even, D2 = r - s D1 (R9)
+        uint32_t w1 = 0, w2 = 0;
+#pragma unroll
+        for (int q = 0; q < 4; q += 2) {
+            const float a1 = fmaf(rf[q], md.inv_s_f, kMagic23) - kMagic23;
+            const float b1 = fmaf(rf[q + 1], md.inv_s_f, kMagic23) - kMagic23;
+            const float a2 = fmaf(-a1, md.s_f, rf[q]), b2 = fmaf(-b1, md.s_f, rf[q + 1]);
+            w1 |= static_cast<uint32_t>(cvt_e4m3x2(a1, b1)) << (8 * q);
+            w2 |= static_cast<uint32_t>(cvt_e4m3x2(a2, b2)) << (8 * q);
+        }
+        *reinterpret_cast<uint32_t*>(o) = w1;
+        *reinterpret_cast<uint32_t*>(o + plane_stride) = w2;
+    } else {
+        // D1 = sign(r) ceil(|r|/16), D2 = r - 16 D1, D3 = D1 + D2
+        uint32_t w1 = 0, w2 = 0, w3 = 0;
+#pragma unroll
+        for (int q = 0; q < 4; q += 2) {
+            const float a1 = copysignf(__fadd_ru(fabsf(rf[q]) * 0.0625f, kMagic23) - kMagic23, rf[q]);
+            const float b1 = copysignf(__fadd_ru(fabsf(rf[q + 1]) * 0.0625f, kMagic23) - kMagic23, rf[q + 1]);
+            const float a2 = fmaf(-16.0f, a1, rf[q]), b2 = fmaf(-16.0f, b1, rf[q + 1]);
+            const float a3 = a1 + a2, b3 = b1 + b2;
+            w1 |= static_cast<uint32_t>(cvt_e4m3x2(a1, b1)) << (8 * q);
+            w2 |= static_cast<uint32_t>(cvt_e4m3x2(a2, b2)) << (8 * q);
+            w3 |= static_cast<uint32_t>(cvt_e4m3x2(a3, b3)) << (8 * q);
+        }
+        *reinterpret_cast<uint32_t*>(o) = w1;
+        *reinterpret_cast<uint32_t*>(o + plane_stride) = w2;
+        *reinterpret_cast<uint32_t*>(o + 2 * plane_stride) = w3;
+    }
+}
+
+template <int NSTEP, int NMOD>
+__device__ __forceinline__ void digits_all_moduli(const DigitParams& dp, const double (&y)[4],
+                                                  const double (&M)[4], const int (&E)[4],
+                                                  uint8_t* out, int64_t plane_stride) {
+    if (NMOD > 0) {
+#pragma unroll
+        for (int l = 0; l < NMOD; ++l)
+            digits_one_modulus<NSTEP>(dp.mod[l], l, y, M, E, dp.pow2tab, out, plane_stride);
+    } else {
+#pragma unroll 1
+        for (int l = 0; l < dp.num_moduli; ++l)
+            digits_one_modulus<NSTEP>(dp.mod[l], l, y, M, E, dp.pow2tab, out, plane_stride);
+    }
+}
+
+template <bool KMAJOR, int NMOD>
 __global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, int64_t rows,
                                                 int64_t k, int64_t ld,
                                                 const int32_t* __restrict__ e_scale,
@@ -206,75 +315,40 @@ __global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, in
         const int rr = w + 8 * j;
         const int64_t r = r0 + rr;
         const int e = (r < rows) ? e_scale[r] : 0;
-        // |X'| = M 2^E with M < 2^53 an integer (E = 0 below 2^53), sign separately
-        double M[4];
+        const double s1 = pow2d(e >> 1), s2 = pow2d(e - (e >> 1));
+        double y[4], M[4];
         int E[4];
-        bool neg[4];
-        bool anyE = false;
+        double amax = 0.0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const double y = trunc(ldexp(tile[rr * TP + lane * 4 + q], e));   // eq. def:A'
-            neg[q] = y < 0.0;
-            double ay = fabs(y);
-            int ee = 0;
-            if (ay >= 9007199254740992.0) {            // 2^53
-                ee = ilogb(ay) - 52;
-                ay = ldexp(ay, -ee);
-                anyE = true;
-            }
-            M[q] = ay;
-            E[q] = ee;
+            const double v = (tile[rr * TP + lane * 4 + q] * s1) * s2;     // exact (eq. def:A')
+            double a = fabs(v);
+            if (a < 4503599627370496.0) a = __dadd_rz(a, 4503599627370496.0) - 4503599627370496.0;  // trunc
+            y[q] = copysign(a, v);
+            amax = fmax(amax, a);
         }
-        const bool warpE = __any_sync(0xffffffffu, anyE);
         uint8_t* out = planes + r * k_pad + h0 + lane * 4;
-#pragma unroll 1
-        for (int l = 0; l < dp.num_moduli; ++l) {
-            const ModDig md = dp.mod[l];
-            float res[4];
+        // warp-uniform choice of the reduction depth
+        const bool need2 = __any_sync(0xffffffffu, amax >= 576460752303423488.0);   // 2^59
+        const bool need0 = __any_sync(0xffffffffu, amax >= 7.922816251426434e28);    // 2^96
+        if (need0) {
+            // |X'| = M 2^E with M < 2^53 an integer (E = 0 below 2^53)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const double qq = rint(M[q] * md.pinv_d);
-                float rf = static_cast<float>(fma(-qq, md.p_d, M[q]));   // exact, |rf| <= p/2+1
-                if (warpE) {
-                    const float tw = static_cast<float>(__ldg(dp.pow2tab + l * kPow2Tab + min(E[q], kPow2Tab - 1)));
-                    rf *= tw;                                        // exact (< 2^20)
-                    rf = fmaf(-rintf(rf * md.pinv_f), md.p_f, rf);
+                double a = fabs(y[q]);
+                int ee = 0;
+                if (a >= 9007199254740992.0) {
+                    ee = static_cast<int>((__double_as_longlong(a) >> 52) & 0x7FF) - 1023 - 52;
+                    a = a * pow2d(-ee);
                 }
-                if (neg[q]) rf = -rf;
-                // symmetric range [-floor(p/2), ceil(p/2)-1] (R2)
-                if (2.0f * rf >= md.p_f) rf -= md.p_f;
-                else if (2.0f * rf < -md.p_f) rf += md.p_f;
-                res[q] = rf;
+                M[q] = a;
+                E[q] = ee;
             }
-            if (md.square) {
-                // D1 = round(r/s) ties-to-even, D2 = r - s D1 (R9)
-                uint32_t w1 = 0, w2 = 0;
-#pragma unroll
-                for (int q = 0; q < 4; q += 2) {
-                    const float a1 = rintf(res[q] * md.inv_s_f), b1 = rintf(res[q + 1] * md.inv_s_f);
-                    const float a2 = fmaf(-a1, md.s_f, res[q]), b2 = fmaf(-b1, md.s_f, res[q + 1]);
-                    w1 |= static_cast<uint32_t>(cvt_e4m3x2(a1 + 0.0f, b1 + 0.0f)) << (8 * q);
-                    w2 |= static_cast<uint32_t>(cvt_e4m3x2(a2 + 0.0f, b2 + 0.0f)) << (8 * q);
-                }
-                *reinterpret_cast<uint32_t*>(out + (md.plane0 + 0) * plane_stride) = w1;
-                *reinterpret_cast<uint32_t*>(out + (md.plane0 + 1) * plane_stride) = w2;
-            } else {
-                // D1 = sign(r) ceil(|r|/16), D2 = r - 16 D1, D3 = D1 + D2
-                uint32_t w1 = 0, w2 = 0, w3 = 0;
-#pragma unroll
-                for (int q = 0; q < 4; q += 2) {
-                    const float a1 = copysignf(ceilf(fabsf(res[q]) * 0.0625f), res[q]);
-                    const float b1 = copysignf(ceilf(fabsf(res[q + 1]) * 0.0625f), res[q + 1]);
-                    const float a2 = fmaf(-16.0f, a1, res[q]), b2 = fmaf(-16.0f, b1, res[q + 1]);
-                    const float a3 = a1 + a2, b3 = b1 + b2;
-                    w1 |= static_cast<uint32_t>(cvt_e4m3x2(a1 + 0.0f, b1 + 0.0f)) << (8 * q);
-                    w2 |= static_cast<uint32_t>(cvt_e4m3x2(a2 + 0.0f, b2 + 0.0f)) << (8 * q);
-                    w3 |= static_cast<uint32_t>(cvt_e4m3x2(a3 + 0.0f, b3 + 0.0f)) << (8 * q);
-                }
-                *reinterpret_cast<uint32_t*>(out + (md.plane0 + 0) * plane_stride) = w1;
-                *reinterpret_cast<uint32_t*>(out + (md.plane0 + 1) * plane_stride) = w2;
-                *reinterpret_cast<uint32_t*>(out + (md.plane0 + 2) * plane_stride) = w3;
-            }
+            digits_all_moduli<0, NMOD>(dp, y, M, E, out, plane_stride);
+        } else if (need2) {
+            digits_all_moduli<2, NMOD>(dp, y, M, E, out, plane_stride);
+        } else {
+            digits_all_moduli<1, NMOD>(dp, y, M, E, out, plane_stride);
         }
     }
 }
@@ -323,8 +397,17 @@ cudaError_t launch_digits(const double* X, int64_t rows, int64_t k, int64_t ld, 
                           const int32_t* e, const DigitParams& dp, uint8_t* planes,
                           int64_t rows_pad, int64_t k_pad, cudaStream_t st) {
     dim3 grid(static_cast<unsigned>(k_pad / TH), static_cast<unsigned>(rows_pad / TR));
-    if (kmajor) k_digits<true><<<grid, 256, 0, st>>>(X, rows, k, ld, e, dp, planes, rows_pad, k_pad);
-    else k_digits<false><<<grid, 256, 0, st>>>(X, rows, k, ld, e, dp, planes, rows_pad, k_pad);
+#define OZ2_DIG(NM)                                                                                  \
+    if (kmajor) k_digits<true, NM><<<grid, 256, 0, st>>>(X, rows, k, ld, e, dp, planes, rows_pad, k_pad); \
+    else k_digits<false, NM><<<grid, 256, 0, st>>>(X, rows, k, ld, e, dp, planes, rows_pad, k_pad);
+    switch (dp.num_moduli) {   // fully unrolled for the common moduli counts
+        case 12: OZ2_DIG(12) break;
+        case 13: OZ2_DIG(13) break;
+        case 14: OZ2_DIG(14) break;
+        case 16: OZ2_DIG(16) break;
+        default: OZ2_DIG(0) break;
+    }
+#undef OZ2_DIG
     return cudaGetLastError();
 }
 

@@ -21,14 +21,23 @@ from oracle import exact, fp8, fp32, moduli as mod, scheme
 from synth import gen_host
 
 
-@pytest.fixture(scope="module")
-def dev():
+@pytest.fixture(scope="module", params=["cg1", "cg2"])
+def dev(request):
+    """The library, once with 128x256 single-CTA GEMM tiles and once with 256x256
+    CTA-pair (tcgen05 cta_group::2) tiles (OZ2_CG selects the kernel per call)."""
+    import os
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import paper_2603_10634_b200 as P
     P.lib()
-    return P
+    old = os.environ.get("OZ2_CG")
+    os.environ["OZ2_CG"] = "2" if request.param == "cg2" else "1"
+    yield P
+    if old is None:
+        os.environ.pop("OZ2_CG", None)
+    else:
+        os.environ["OZ2_CG"] = old
 
 
 _LUT = np.array([fp8.encode_int(v) for v in range(-16, 17)], dtype=np.uint8)
