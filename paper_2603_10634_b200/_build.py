@@ -12,7 +12,7 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "liboz2.so")
 SOURCES = ["oz2_api.cu", "prep_kernels.cu", "gemm_kernel.cu", "crt_kernel.cu"]
-HEADERS = ["oz2_internal.h", "oz2_ptx.cuh"]
+HEADERS = ["oz2_internal.h", "oz2_ptx.cuh", "crt_common.cuh"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

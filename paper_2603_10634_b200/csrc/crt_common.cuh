@@ -1,0 +1,155 @@
+// crt_common.cuh -- exact per-element Chinese-remainder reconstruction and inverse
+// scaling (eq. CRT_finalreduction, eq. inversescaling), shared by
+// the standalone k_crt and the fused epilogue of the residue GEMM.
+//
+// With u_l = C'_l mod p_l in [0, p_l) and w_l = q_l P/p_l:
+//   S = sum_l u_l w_l                     (exact, L 32-bit limbs, wrap-around mod 2^(32L))
+//   t = round(sum_l u_l q_l/p_l)          (fixed point, 2^-32 units: S/P to within 2^-19)
+//   C' = S - t P  (mod 2^(32L)), then one correction into [-P/2, P/2)   (symmetric, R2)
+// 2^(32L-1) > 1.5 P, so the two's-complement value of the L-limb result is exact even
+// when t is off by one (|frac(S/P) - 1/2| < 2^-19), and one correction fixes that case.
+// RN64(|C'|) from the top 64 significant bits with a sticky bit (exact RNE), then an
+// exact power-of-two scaling by 2^-(e_mu_i + e_nu_j) (exact unless subnormal, R10).
+#pragma once
+#include <cstdint>
+#include "oz2_internal.h"
+
+namespace oz2 {
+
+template <int L>
+__device__ __forceinline__ int cmp_limbs(const uint32_t (&a)[L], const uint32_t* b) {
+#pragma unroll
+    for (int t = L - 1; t >= 0; --t) {
+        if (a[t] != b[t]) return a[t] > b[t] ? 1 : -1;
+    }
+    return 0;
+}
+
+template <int L>
+__device__ __forceinline__ void add_limbs(uint32_t (&a)[L], const uint32_t* b) {
+    uint64_t c = 0;
+#pragma unroll
+    for (int t = 0; t < L; ++t) {
+        const uint64_t s = static_cast<uint64_t>(a[t]) + b[t] + c;
+        a[t] = static_cast<uint32_t>(s);
+        c = s >> 32;
+    }
+}
+
+template <int L>
+__device__ __forceinline__ void negate_limbs(uint32_t (&a)[L]) {
+    uint64_t c = 1;
+#pragma unroll
+    for (int t = 0; t < L; ++t) {
+        const uint64_t s = static_cast<uint64_t>(~a[t]) + c;
+        a[t] = static_cast<uint32_t>(s);
+        c = s >> 32;
+    }
+}
+
+// constants of one plan staged in shared memory (broadcast reads)
+struct CrtShared {
+    uint32_t w[kMaxModuli][kMaxLimbs];
+    uint32_t qp[kMaxModuli];
+    uint32_t p[kMaxModuli];
+};
+
+__device__ __forceinline__ void crt_stage_constants(CrtShared* s, const CrtParams& cp, int tid, int nthreads) {
+    for (int t = tid; t < cp.num_moduli * kMaxLimbs; t += nthreads) s->w[t / kMaxLimbs][t % kMaxLimbs] = cp.w[t / kMaxLimbs][t % kMaxLimbs];
+    for (int t = tid; t < cp.num_moduli; t += nthreads) {
+        s->qp[t] = cp.qp32[t];
+        s->p[t] = static_cast<uint32_t>(cp.p[t]);
+    }
+}
+
+// value of C'(i,j) * 2^-escale, rounded once to nearest binary64; rp points at the
+// residue of modulus 0 of the element, residues of modulus l at rp + l * lstride
+template <int L>
+__device__ __forceinline__ double crt_element(const int16_t* rp, int64_t lstride, const CrtShared* s,
+                                              const CrtParams& cp, int escale, bool streaming) {
+    const int nm = cp.num_moduli;
+    uint64_t acc[L];
+#pragma unroll
+    for (int t = 0; t < L; ++t) acc[t] = 0;
+    uint64_t tacc = 0x80000000ull;                       // + 1/2: round-to-nearest of S/P
+#pragma unroll 4
+    for (int l = 0; l < nm; ++l) {
+        const int c = streaming ? static_cast<int>(__ldcs(rp + l * lstride)) : static_cast<int>(__ldg(rp + l * lstride));
+        const uint32_t u = static_cast<uint32_t>(c) + (c < 0 ? s->p[l] : 0u);
+        tacc += static_cast<uint64_t>(u) * s->qp[l];    // sum u_l q_l/p_l in 2^-32 units
+#pragma unroll
+        for (int t = 0; t < L; ++t) acc[t] += static_cast<uint64_t>(u) * s->w[l][t];
+    }
+    const uint32_t tq = static_cast<uint32_t>(tacc >> 32);   // t = round(S / P) (+-1)
+    uint32_t r[L];
+    uint64_t carry = 0;
+#pragma unroll
+    for (int t = 0; t < L; ++t) {
+        const uint64_t v = acc[t] + static_cast<uint64_t>(tq) * cp.np[t] + carry;
+        r[t] = static_cast<uint32_t>(v);
+        carry = v >> 32;
+    }
+    bool negv = (r[L - 1] >> 31) != 0;
+    if (!negv) {
+        if (cmp_limbs<L>(r, cp.halfP) >= 0) {             // C' >= P/2: subtract P
+            add_limbs<L>(r, cp.np);
+            negv = (r[L - 1] >> 31) != 0;
+        }
+    } else {
+        uint32_t a[L];
+#pragma unroll
+        for (int t = 0; t < L; ++t) a[t] = r[t];
+        negate_limbs<L>(a);
+        if (cmp_limbs<L>(a, cp.halfP) > 0) {              // C' < -P/2: add P
+            add_limbs<L>(r, cp.P);
+            negv = (r[L - 1] >> 31) != 0;
+        }
+    }
+    if (negv) negate_limbs<L>(r);
+    uint32_t w2 = 0, w1 = r[1], w0 = r[0];
+    int top = 1;
+    bool found = false;
+    uint32_t below = 0;                                  // OR of limbs under the window
+#pragma unroll
+    for (int t = L - 1; t >= 2; --t) {
+        if (!found && r[t] != 0u) {
+            found = true;
+            top = t;
+            w2 = r[t];
+            w1 = r[t - 1];
+            w0 = r[t - 2];
+            uint32_t o = 0;
+#pragma unroll
+            for (int u = 0; u < t - 2; ++u) o |= r[u];
+            below = o;
+        }
+    }
+    double v;
+    int ex;
+    if (!found) {
+        v = __ull2double_rn((static_cast<uint64_t>(w1) << 32) | w0);
+        ex = 0;
+    } else {
+        const int lz = __clz(w2);
+        const uint64_t hi = (static_cast<uint64_t>(w2) << 32) | w1;
+        uint64_t top64 = lz ? (hi << lz) | (static_cast<uint64_t>(w0) >> (32 - lz)) : hi;
+        const bool sticky = (lz ? ((w0 << lz) != 0u) : (w0 != 0u)) || below != 0u;
+        top64 |= sticky ? 1ull : 0ull;
+        v = __ull2double_rn(top64);
+        ex = 32 * (top - 1) - lz;                        // |C'| ~ top64 * 2^ex
+    }
+    const int E = ex - escale;
+    if (v != 0.0 && E >= -1022 && E <= 1023 - 64)
+        v *= __longlong_as_double(static_cast<long long>(E + 1023) << 52);
+    else if (v != 0.0)
+        v = ldexp(v, E);
+    return negv ? -v : v;
+}
+
+// C <- alpha v + beta C (R11; beta == 0 never reads C)
+__device__ __forceinline__ void store_alpha_beta(double* cptr, double v, double alpha, double beta) {
+    if (beta == 0.0) *cptr = alpha * v;
+    else *cptr = fma(alpha, v, beta * *cptr);
+}
+
+}  // namespace oz2

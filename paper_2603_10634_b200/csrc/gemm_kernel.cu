@@ -35,6 +35,7 @@
 #include <cuda_fp16.h>
 #include "oz2_internal.h"
 #include "oz2_ptx.cuh"
+#include "crt_common.cuh"
 
 namespace oz2 {
 
@@ -45,7 +46,7 @@ struct GemmCfg {
     static constexpr int A_STAGE = BM * BK;
     static constexpr int B_STAGE = B_ROWS * BK;
     static constexpr int NSTAGE = CG == 1 ? STAGES : STAGES2;
-    static constexpr int SMEM = NSTAGE * (A_STAGE + B_STAGE) + 1024 + 256;
+    static constexpr int SMEM = NSTAGE * (A_STAGE + B_STAGE) + 1024 + 256 + static_cast<int>(sizeof(CrtShared));
 };
 
 __device__ __forceinline__ void tile_coords(int t, int m_tiles, int n_tiles, int& tm, int& tn) {
@@ -74,8 +75,11 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
     return r;
 }
+// Relaxed remote arrive: it only contributes an arrival count (the TMA bytes carry their
+// own complete_tx, and the TMEM reads it publishes have completed at tcgen05.wait::ld), so
+// no release fence is needed -- a .release.cluster arrive costs a MEMBAR per k-stage.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // 2-SM TMA: bytes land in this CTA's smem, completion is counted on the leader's barrier
 __device__ __forceinline__ void tma_load_2d_cg2(const CUtensorMap* m, uint32_t leader_bar, void* smem,
@@ -118,7 +122,7 @@ __device__ __forceinline__ void tmem_dealloc_cg(uint32_t taddr, uint32_t ncols) 
     else asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
 
-template <int MODE, int CG>
+template <int MODE, int CG, int FL>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
             const __grid_constant__ GemmParams P) {
@@ -133,6 +137,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     uint64_t* tfull = empty + NS;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    CrtShared* crt_s = reinterpret_cast<CrtShared*>(smem + NS * (Cfg::A_STAGE + Cfg::B_STAGE) + 256);
+    if (FL > 0) crt_stage_constants(crt_s, P.crt, threadIdx.x, blockDim.x);
 
     const uint32_t warp = warp_id_uniform();
     const uint32_t lane = lane_id();
@@ -275,6 +281,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             tile_coords(tile, P.m_tiles, P.n_tiles, tm, tn);
             const int64_t row = static_cast<int64_t>(tm) * Cfg::TILE_M + row_in_tile;
             const int64_t col0 = static_cast<int64_t>(tn) * BN + half * 128u;
+            const bool row_ok = row < P.m;
             if (MODE == MODE_RESIDUE) {
                 for (int l = 0; l < P.num_moduli; ++l) {
                     const float p = P.mod[l].p, pinv = P.mod[l].pinv;
@@ -282,7 +289,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     // (|.| <= p/2 + 1 <= 546), held exactly in binary16 pairs
                     __half2 part[64];
                     int16_t* out = P.residues + (static_cast<int64_t>(l) * P.n + col0) * P.m + row;
-                    const bool row_ok = row < P.m;
 #pragma unroll
                     for (int x = 0; x < 3; ++x, ++g) {
                         const float coef = P.mod[l].coef[x];
@@ -334,6 +340,22 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         }
                     }
                 }
+                if (FL > 0 && row_ok) {
+                    // fused CRT + inverse scaling of this thread's row x 128 columns: the N
+                    // residues were written by this same thread (program order), most still
+                    // in L2; the slots are already released, so this overlaps the MMAs of
+                    // the next tile (eqs. CRT_finalreduction, inversescaling)
+                    const int emu = P.e_mu[row];
+                    const int64_t lstride = static_cast<int64_t>(P.n) * P.m;
+#pragma unroll 1
+                    for (int jj = 0; jj < 128; ++jj) {
+                        const int64_t col = col0 + jj;
+                        if (col >= P.n) break;
+                        const double v = crt_element<(FL > 0 ? FL : 4)>(P.residues + col * P.m + row, lstride, crt_s,
+                                                                         P.crt, emu + P.e_nu[col], true);
+                        store_alpha_beta(P.C + row + col * P.ldc, v, P.alpha, P.beta);
+                    }
+                }
             } else {
                 const uint32_t slot = g & 1u, use = g >> 1;
                 mbar_wait(&tfull[slot], use & 1u);
@@ -381,7 +403,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     }
 }
 
-template <int MODE, int CG>
+template <int MODE, int CG, int FL>
 static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& gp,
                               int num_sms, cudaStream_t st) {
     static bool attr_set = false;
@@ -391,7 +413,7 @@ static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, cons
     const int max_units = num_sms / CG;
     const int units = num_tiles < max_units ? num_tiles : max_units;
     if (!attr_set) {
-        cudaError_t err = cudaFuncSetAttribute(gemm_kernel<MODE, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+        cudaError_t err = cudaFuncSetAttribute(gemm_kernel<MODE, CG, FL>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
         if (err != cudaSuccess) return err;
         attr_set = true;
     }
@@ -407,25 +429,26 @@ static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, cons
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, CG>, ta, tb, gp);
+    return cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, CG, FL>, ta, tb, gp);
 }
 
-cudaError_t launch_gemm(int mode, int cg, const CUtensorMap& ta, const CUtensorMap& tb,
-                        const GemmParams& gp, int num_sms, cudaStream_t st) {
-    cudaError_t err;
-    if (cg == 2) {
-        switch (mode) {
-            case MODE_RESIDUE: err = launch_one<MODE_RESIDUE, 2>(ta, tb, gp, num_sms, st); break;
-            case MODE_BOUND: err = launch_one<MODE_BOUND, 2>(ta, tb, gp, num_sms, st); break;
-            default: err = launch_one<MODE_RAW, 2>(ta, tb, gp, num_sms, st); break;
-        }
-    } else {
-        switch (mode) {
-            case MODE_RESIDUE: err = launch_one<MODE_RESIDUE, 1>(ta, tb, gp, num_sms, st); break;
-            case MODE_BOUND: err = launch_one<MODE_BOUND, 1>(ta, tb, gp, num_sms, st); break;
-            default: err = launch_one<MODE_RAW, 1>(ta, tb, gp, num_sms, st); break;
-        }
+template <int CG>
+static cudaError_t launch_cg(int mode, int fl, const CUtensorMap& ta, const CUtensorMap& tb,
+                            const GemmParams& gp, int num_sms, cudaStream_t st) {
+    if (mode == MODE_BOUND) return launch_one<MODE_BOUND, CG, 0>(ta, tb, gp, num_sms, st);
+    if (mode == MODE_RAW) return launch_one<MODE_RAW, CG, 0>(ta, tb, gp, num_sms, st);
+    switch (fl) {
+        case 4: return launch_one<MODE_RESIDUE, CG, 4>(ta, tb, gp, num_sms, st);
+        case 5: return launch_one<MODE_RESIDUE, CG, 5>(ta, tb, gp, num_sms, st);
+        case 6: return launch_one<MODE_RESIDUE, CG, 6>(ta, tb, gp, num_sms, st);
+        default: return launch_one<MODE_RESIDUE, CG, 0>(ta, tb, gp, num_sms, st);
     }
+}
+
+cudaError_t launch_gemm(int mode, int cg, int fused_limbs, const CUtensorMap& ta, const CUtensorMap& tb,
+                        const GemmParams& gp, int num_sms, cudaStream_t st) {
+    const cudaError_t err = (cg == 2) ? launch_cg<2>(mode, fused_limbs, ta, tb, gp, num_sms, st)
+                                      : launch_cg<1>(mode, fused_limbs, ta, tb, gp, num_sms, st);
     if (err != cudaSuccess) return err;
     return cudaGetLastError();
 }

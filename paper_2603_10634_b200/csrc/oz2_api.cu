@@ -356,7 +356,7 @@ static int sync_lead() {   // progress throttle of the residue GEMM (OZ2_SYNC_LE
     return v < 0 ? 0 : v;
 }
 static int cta_group() {   // 1: 128x256 CTA tiles; 2: 256x256 CTA-pair tiles (OZ2_CG)
-    return env_int("OZ2_CG", 1) == 2 ? 2 : 1;
+    return env_int("OZ2_CG", 2) == 1 ? 1 : 2;
 }
 
 static void phase_mark(int i) {
@@ -437,7 +437,7 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             gp.m_tiles = static_cast<int>(L.m_pad / (BM * cg)); gp.n_tiles = static_cast<int>(L.n_pad / BN);
             gp.rows_per_plane_a = static_cast<int>(L.m_pad); gp.rows_per_plane_b = static_cast<int>(L.n_pad);
             gp.rmax = rsmax; gp.smax = rsmax + m;
-            OZ2_CK(launch_gemm(MODE_BOUND, cg, ta, tb, gp, g_ts.num_sms, st));
+            OZ2_CK(launch_gemm(MODE_BOUND, cg, 0, ta, tb, gp, g_ts.num_sms, st));
         }
         if (opt && opt->rmax) OZ2_CK(cudaMemcpyAsync(opt->rmax, rsmax, 4 * m, cudaMemcpyDeviceToDevice, st));
         if (opt && opt->smax) OZ2_CK(cudaMemcpyAsync(opt->smax, rsmax + m, 4 * n, cudaMemcpyDeviceToDevice, st));
@@ -470,6 +470,7 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
                                      cudaMemcpyDeviceToDevice, st));
     // ---- step 5: 3N exact FP8 GEMMs with the modular epilogue
     phase_mark(4);
+    int fused = 0;
     {
         const int cg = cta_group();
         CUtensorMap ta, tb;
@@ -488,13 +489,21 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             gp.progress = reinterpret_cast<unsigned long long*>(maxbits);   // dead after step 3
             OZ2_CK(cudaMemsetAsync(gp.progress, 0, 8, st));
         }
-        OZ2_CK(launch_gemm(MODE_RESIDUE, cg, ta, tb, gp, g_ts.num_sms, st));
+        // fuse the CRT into the epilogue for up to 6 limbs (N <= 20) unless OZ2_FUSED_CRT=0
+        fused = (pl->L <= 6 && env_int("OZ2_FUSED_CRT", 1) != 0) ? pl->L : 0;
+        if (fused) {
+            gp.crt = pl->crt;
+            gp.e_mu = e_mu; gp.e_nu = e_nu;
+            gp.alpha = alpha; gp.beta = beta;
+            gp.C = C; gp.ldc = ldc;
+        }
+        OZ2_CK(launch_gemm(MODE_RESIDUE, cg, fused, ta, tb, gp, g_ts.num_sms, st));
     }
     if (opt && opt->residues)
         OZ2_CK(cudaMemcpyAsync(opt->residues, res, 2ull * N * m * n, cudaMemcpyDeviceToDevice, st));
     // ---- step 6: CRT + inverse scaling (eqs. CRT_finalreduction, inversescaling)
     phase_mark(5);
-    OZ2_CK(launch_crt(pl->L, res, m, n, pl->crt, e_mu, e_nu, alpha, beta, C, ldc, st));
+    if (!fused) OZ2_CK(launch_crt(pl->L, res, m, n, pl->crt, e_mu, e_nu, alpha, beta, C, ldc, st));
     phase_mark(6);
     g_ts.timed_last = g_ts.timing;
     return OZ2_SUCCESS;
@@ -699,7 +708,7 @@ int oz2_fp8_gemm_raw(const uint8_t* a, const uint8_t* b, float* C32, int64_t m, 
     gp.num_k_blocks = static_cast<int>((k + BK - 1) / BK);
     gp.m_tiles = static_cast<int>((m + BM * cg - 1) / (BM * cg)); gp.n_tiles = static_cast<int>((n + BN - 1) / BN);
     gp.c32 = C32;
-    OZ2_CK(launch_gemm(MODE_RAW, cg, ta, tb, gp, g_ts.num_sms, g_ts.stream));
+    OZ2_CK(launch_gemm(MODE_RAW, cg, 0, ta, tb, gp, g_ts.num_sms, g_ts.stream));
     return OZ2_SUCCESS;
 }
 

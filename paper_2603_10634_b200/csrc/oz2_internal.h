@@ -27,6 +27,17 @@ constexpr int PAD_K = 128;
 
 enum GemmMode : int { MODE_RESIDUE = 0, MODE_BOUND = 1, MODE_RAW = 2 };
 
+// ---- CRT ------------------------------------------------------------------------
+struct CrtParams {
+    int num_moduli;
+    int p[kMaxModuli];
+    uint32_t qp32[kMaxModuli];                   // round(2^32 q_l / p_l)
+    uint32_t w[kMaxModuli][kMaxLimbs];           // w_l mod 2^(32L)
+    uint32_t np[kMaxLimbs];                      // 2^(32L) - P
+    uint32_t P[kMaxLimbs];
+    uint32_t halfP[kMaxLimbs];                   // P / 2 (P is even: 1024 | P)
+};
+
 struct ModEpi {          // per modulus, residue-GEMM epilogue
     float p, pinv;
     float coef[3];       // square: (s, s, 1); non-square: (240, -15, 16)
@@ -46,6 +57,13 @@ struct GemmParams {
     uint32_t* smax;              // [n]
     float* c32;                  // raw: [m][n]
     unsigned long long* progress;  // chip-wide product counter (progress throttle)
+    // fused CRT + inverse scaling epilogue (MODE_RESIDUE, FL > 0)
+    const int32_t* e_mu;
+    const int32_t* e_nu;
+    double alpha, beta;
+    double* C;
+    int64_t ldc;
+    CrtParams crt;
     int sync_lead;               // 0 = off; else max chunks ahead of the chip-wide average
     int sync_chunk;              // k-blocks per throttle chunk (0 = one chunk per product)
     ModEpi mod[kMaxModuli];
@@ -66,17 +84,6 @@ struct DigitParams {
     ModDig mod[kMaxModuli];
 };
 
-// ---- CRT ------------------------------------------------------------------------
-struct CrtParams {
-    int num_moduli;
-    int p[kMaxModuli];
-    uint32_t qp32[kMaxModuli];                   // round(2^32 q_l / p_l)
-    uint32_t w[kMaxModuli][kMaxLimbs];           // w_l mod 2^(32L)
-    uint32_t np[kMaxLimbs];                      // 2^(32L) - P
-    uint32_t P[kMaxLimbs];
-    uint32_t halfP[kMaxLimbs];                   // P / 2 (P is even: 1024 | P)
-};
-
 // ---- exponents ------------------------------------------------------------------
 struct ExpParams {
     float p_prime, delta, f_k;
@@ -94,7 +101,7 @@ cudaError_t launch_exps(const unsigned long long* maxbits, const int32_t* eprime
 cudaError_t launch_digits(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
                           const int32_t* e, const DigitParams& dp, uint8_t* planes,
                           int64_t rows_pad, int64_t k_pad, cudaStream_t st);
-cudaError_t launch_gemm(int mode, int cg, const CUtensorMap& ta, const CUtensorMap& tb,
+cudaError_t launch_gemm(int mode, int cg, int fused_limbs, const CUtensorMap& ta, const CUtensorMap& tb,
                         const GemmParams& gp, int num_sms, cudaStream_t st);
 cudaError_t launch_crt(int limbs, const int16_t* res, int64_t m, int64_t n, const CrtParams& cp,
                        const int32_t* e_mu, const int32_t* e_nu, double alpha, double beta,

@@ -1,0 +1,107 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times
+(oz2_dgemm on device buffers, default kernels), on sampled outputs the oracle computes
+one by one: the exponents of the sampled rows/columns (each needs a full row of
+A-bar B-bar), the residues C'_l and the final C of the sampled entries.  Residues and C
+must be bit-exact wherever the exponents agree (reading R13); exponents must agree on
+all but a vanishing fraction (the R6 rounding window).  Accuracy against the exact
+product is checked against the closed-form a-priori bound."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from oracle import exact, scheme
+from synth import gen_device
+
+
+@pytest.fixture(scope="module")
+def dev():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2603_10634_b200 as P
+    P.lib()
+    return P
+
+
+def _run_sampled(P, m, k, n, N, phi, seed, I, J):
+    import torch
+    A = gen_device(m, k, "phi", phi=phi, seed=seed)
+    B = gen_device(k, n, "phi", phi=phi, seed=seed + 1)
+    C = torch.empty((n, m), dtype=torch.float64, device="cuda").t()
+    e_mu = torch.zeros(m, dtype=torch.int32, device="cuda")
+    e_nu = torch.zeros(n, dtype=torch.int32, device="cuda")
+    res = torch.zeros(N * n * m, dtype=torch.int16, device="cuda")
+    opt = P.oz2_options()
+    opt.e_mu = e_mu.data_ptr()
+    opt.e_nu = e_nu.data_ptr()
+    opt.residues = res.data_ptr()
+    P.oz2_set_stream(torch.cuda.current_stream().cuda_stream)
+    P.oz2_set_workspace(None, 0)
+    rc = P.oz2_dgemm_ex("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0,
+                        C.data_ptr(), m, N, opt)
+    assert rc == 0
+    torch.cuda.synchronize()
+    It = torch.tensor(I, device="cuda")
+    Jt = torch.tensor(J, device="cuda")
+    res3 = res.view(N, n, m)
+    out = {
+        "C": C[It][:, Jt].cpu().numpy(),
+        "e_mu": e_mu[It].cpu().numpy(),
+        "e_nu": e_nu[Jt].cpu().numpy(),
+        "res": res3[:, Jt][:, :, It].permute(0, 2, 1).cpu().numpy(),     # [l][a][b]
+        "A_rows": A[It].cpu().numpy(),
+        "B_cols": B[:, Jt].cpu().numpy(),
+        "A": A.cpu().numpy(),
+        "B": B.cpu().numpy(),
+    }
+    del A, B, C, res, res3
+    torch.cuda.empty_cache()
+    P.oz2_finalize()
+    return out
+
+
+def _check(out, N, I, J, ref_exps=None):
+    A, B = out["A"], out["B"]
+    k = A.shape[1]
+    if ref_exps is None:
+        _, emu, _ = scheme.row_exponents(A, I, B.T, N)
+        _, enu, _ = scheme.row_exponents(B.T, J, A, N)
+    else:
+        emu, enu = ref_exps
+    assert np.array_equal(out["e_mu"], emu) and np.array_equal(out["e_nu"], enu)
+    res, Cref = scheme.entries(A, B, N, I, J, list(emu), list(enu))
+    assert np.array_equal(out["res"], res)
+    assert np.array_equal(out["C"], Cref)
+    ex = exact.exact_entries(A, B, I, J)
+    bound = exact.apriori_bound(A[I], B[:, J], list(emu), list(enu))
+    assert np.all(np.abs(out["C"] - ex) <= 2 * bound + np.abs(ex) * 2.0 ** -52)
+    return float(np.linalg.norm(out["C"] - ex) / np.linalg.norm(ex))
+
+
+@pytest.mark.parametrize("phi", [0.0, 4.0])
+def test_config2_8192_moduli_sweep(dev, phi):
+    """BASELINE config 2: m=n=k=8192, N in 12..20, accuracy vs exact falls with N."""
+    m = n = k = 8192
+    I, J = [0, 4097, 8191], [1, 5000, 8190]
+    errs = []
+    for N in [12, 16, 20]:
+        out = _run_sampled(dev, m, k, n, N, phi, 11, I, J)
+        errs.append(_check(out, N, I, J))
+    assert errs[1] <= errs[0] and errs[2] <= max(errs[1], 2e-17)
+
+
+def test_config3_16384_bench_workload(dev):
+    """BASELINE config 3 as bench.py runs it: m=n=k=16384, phi=1, N=13."""
+    I, J = [3, 9000, 16383], [0, 12345]
+    out = _run_sampled(dev, 16384, 16384, 16384, 13, 1.0, 21, I, J)
+    err = _check(out, 13, I, J)
+    assert err < 1e-15
+
+
+@pytest.mark.parametrize("N,phi", [(12, 0.0), (13, 1.0)])
+def test_config4_large_k_65536(dev, N, phi):
+    """BASELINE config 4: m=n=4096, k=65536 -- the FP32 exactness limit k = 2^16."""
+    I, J = [0, 2048, 4095], [7, 4000]
+    out = _run_sampled(dev, 4096, 65536, 4096, N, phi, 31, I, J)
+    _check(out, N, I, J)
