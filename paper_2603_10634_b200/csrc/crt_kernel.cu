@@ -31,7 +31,12 @@ cudaError_t launch_crt(int limbs, const int16_t* res, int64_t m, int64_t n, cons
                        const int32_t* e_mu, const int32_t* e_nu, double alpha, double beta,
                        double* C, int64_t ldc, cudaStream_t st) {
     if (m == 0 || n == 0) return cudaSuccess;
-    dim3 grid(static_cast<unsigned>((m + 255) / 256), static_cast<unsigned>(n < 65535 ? n : 65535));
+    // ~2048 blocks in total, each looping over many columns (amortises the staging of
+    // the CRT constants in shared memory)
+    const int64_t gx = (m + 255) / 256;
+    int64_t gy = 2048 / gx;
+    gy = gy < 1 ? 1 : (gy > n ? n : gy);
+    dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy < 65535 ? gy : 65535));
 #define OZ2_CRT_CASE(LL) \
     case LL: k_crt<LL><<<grid, 256, 0, st>>>(res, m, n, cp, e_mu, e_nu, alpha, beta, C, ldc); break;
     switch (limbs) {

@@ -49,10 +49,11 @@ struct GemmCfg {
     static constexpr int SMEM = NSTAGE * (A_STAGE + B_STAGE) + 1024 + 256 + static_cast<int>(sizeof(CrtShared));
 };
 
+template <int G>
 __device__ __forceinline__ void tile_coords(int t, int m_tiles, int n_tiles, int& tm, int& tn) {
-    // groups of 16 tile-rows swept column by column: concurrently running CTAs share
-    // A and B panels in L2
-    constexpr int G = 16;
+    // groups of G tile-rows swept column by column: the ~148 concurrently running tiles
+    // cover a near-square 2048 x ~2300 block of C, so the A and B panels they stream are
+    // shared in L2 (G x TILE_M = 2048 rows for both CTA-group sizes)
     const int group = t / (G * n_tiles);
     const int first_m = group * G;
     const int gm = min(G, m_tiles - first_m);
@@ -186,7 +187,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             const uint32_t full0 = smem_u32(&full[0]) & 0xFEFFFFFFu;   // leader's barrier (CG=2)
             for (int tile = unit; tile < num_tiles; tile += units) {
                 int tm, tn;
-                tile_coords(tile, P.m_tiles, P.n_tiles, tm, tn);
+                tile_coords<16 / CG>(tile, P.m_tiles, P.n_tiles, tm, tn);
                 for (int pr = 0; pr < prods; ++pr) {
                     int a_row = tm * Cfg::TILE_M + static_cast<int>(rank) * BM;
                     int b_row = tn * BN + static_cast<int>(rank) * Cfg::B_ROWS;
@@ -275,10 +276,31 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 else mbar_arrive_cluster(tempty0 + slot * 8u);
             }
         };
+        // Fused CRT + inverse scaling (FL > 0): a finished tile's CRT is spread over the
+        // products of the next tile, crt_per_prod columns after each product, so its
+        // residue loads never delay the release of an accumulator slot.  The N residues
+        // of an element were written by this same thread (program order).
+        int64_t crt_row = -1, crt_col0 = 0;
+        int crt_j = 128;
+        const int crt_per_prod = (MODE == MODE_RESIDUE) ? (128 + 3 * P.num_moduli - 1) / (3 * P.num_moduli) + 1 : 0;
+        auto crt_steps = [&](int ncols) {
+            if (FL == 0 || crt_j >= 128) return;
+            if (crt_row >= P.m) { crt_j = 128; return; }
+            const int emu = P.e_mu[crt_row];
+            const int64_t lstride = static_cast<int64_t>(P.n) * P.m;
+#pragma unroll 1
+            for (int s2 = 0; s2 < ncols && crt_j < 128; ++s2, ++crt_j) {
+                const int64_t col = crt_col0 + crt_j;
+                if (col >= P.n) { crt_j = 128; break; }
+                const double v = crt_element<(FL > 0 ? FL : 4)>(P.residues + col * P.m + crt_row, lstride, crt_s,
+                                                                 P.crt, emu + P.e_nu[col], true);
+                store_alpha_beta(P.C + crt_row + col * P.ldc, v, P.alpha, P.beta);
+            }
+        };
         uint32_t g = 0;
         for (int tile = unit; tile < num_tiles; tile += units) {
             int tm, tn;
-            tile_coords(tile, P.m_tiles, P.n_tiles, tm, tn);
+            tile_coords<16 / CG>(tile, P.m_tiles, P.n_tiles, tm, tn);
             const int64_t row = static_cast<int64_t>(tm) * Cfg::TILE_M + row_in_tile;
             const int64_t col0 = static_cast<int64_t>(tn) * BN + half * 128u;
             const bool row_ok = row < P.m;
@@ -338,23 +360,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                                 }
                             }
                         }
+                        crt_steps(crt_per_prod);
                     }
                 }
-                if (FL > 0 && row_ok) {
-                    // fused CRT + inverse scaling of this thread's row x 128 columns: the N
-                    // residues were written by this same thread (program order), most still
-                    // in L2; the slots are already released, so this overlaps the MMAs of
-                    // the next tile (eqs. CRT_finalreduction, inversescaling)
-                    const int emu = P.e_mu[row];
-                    const int64_t lstride = static_cast<int64_t>(P.n) * P.m;
-#pragma unroll 1
-                    for (int jj = 0; jj < 128; ++jj) {
-                        const int64_t col = col0 + jj;
-                        if (col >= P.n) break;
-                        const double v = crt_element<(FL > 0 ? FL : 4)>(P.residues + col * P.m + row, lstride, crt_s,
-                                                                         P.crt, emu + P.e_nu[col], true);
-                        store_alpha_beta(P.C + row + col * P.ldc, v, P.alpha, P.beta);
-                    }
+                if (FL > 0) {
+                    crt_steps(128);               // finish the previous tile if still pending
+                    crt_row = row;                // this tile's CRT is spread over the next tile
+                    crt_col0 = col0;
+                    crt_j = 0;
                 }
             } else {
                 const uint32_t slot = g & 1u, use = g >> 1;
@@ -391,6 +404,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     atomicMax(P.rmax + row, __float_as_uint(rowmax));
             }
         }
+        crt_steps(128);                           // the last tile's CRT
     }
 
     tc_fence_before();

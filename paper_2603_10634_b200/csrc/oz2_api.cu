@@ -490,7 +490,8 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             OZ2_CK(cudaMemsetAsync(gp.progress, 0, 8, st));
         }
         // fuse the CRT into the epilogue for up to 6 limbs (N <= 20) unless OZ2_FUSED_CRT=0
-        fused = (pl->L <= 6 && env_int("OZ2_FUSED_CRT", 1) != 0) ? pl->L : 0;
+        // (k >= 8192: a product then lasts long enough to hide one CRT step per product)
+        fused = (pl->L <= 6 && k >= 8192 && env_int("OZ2_FUSED_CRT", 1) != 0) ? pl->L : 0;
         if (fused) {
             gp.crt = pl->crt;
             gp.e_mu = e_mu; gp.e_nu = e_nu;

@@ -122,6 +122,10 @@ __device__ __forceinline__ void load_tile(const double* __restrict__ X, int64_t 
     }
 }
 
+__device__ __forceinline__ double pow2d(int e) {          // 2^e, |e| <= 1022
+    return __longlong_as_double(static_cast<long long>(e + 1023) << 52);
+}
+
 // ---------------------------------------------------------------------------------
 // k_cast: e' and X-bar = RU_fp8(|x| 2^e')
 
@@ -150,13 +154,14 @@ __global__ void __launch_bounds__(256) k_cast(const double* __restrict__ X, int6
         const int rr = w + 8 * j;
         const int64_t r = r0 + rr;
         const int e = (r < rows) ? eprime_of(maxbits[r]) : 0;
+        const double s1 = pow2d(e >> 1), s2 = pow2d(e - (e >> 1));   // 2^e in two exact steps
         uint32_t word = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const double x = tile[rr * TP + lane * 4 + q];
             uint32_t c = 0;
             if (x != 0.0) {
-                c = fp8_ru_code(ldexp(fabs(x), e));
+                c = fp8_ru_code((fabs(x) * s1) * s2);
                 c = c ? c : 1u;               // an underflowed nonzero still rounds up to 2^-9
             }
             word |= c << (8 * q);
@@ -194,9 +199,6 @@ __global__ void k_exps(const unsigned long long* __restrict__ maxbits,
 //     and r read as an int from the low word of r + 1.5*2^52;
 //   * int -> float by the 1.5*2^23 bit trick, round / ceil of r/s by magic adds.
 
-__device__ __forceinline__ double pow2d(int e) {          // 2^e, |e| <= 1022
-    return __longlong_as_double(static_cast<long long>(e + 1023) << 52);
-}
 __device__ __forceinline__ float i2f_small(int v) {       // exact for |v| < 2^22
     return __int_as_float(0x4B400000 + v) - 12582912.0f;
 }
