@@ -166,9 +166,11 @@ def run_oz2(args, rank, world, local_rank):
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
     P.oz2_set_workspace(ws.data_ptr(), ws.numel())
 
+    Bt = B.t()                                   # contiguous (n x k) storage of column-major B
+
     def step():
         if world > 1:
-            dist.broadcast(B, src=0)
+            dist.broadcast(Bt, src=0)
         rc = P.oz2_dgemm("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0, C.data_ptr(), m, N)
         if rc != 0:
             raise RuntimeError(f"oz2_dgemm rc={rc}")
@@ -272,7 +274,7 @@ def run_oz2(args, rank, world, local_rank):
         return {"normwise": float(np.linalg.norm(d) / np.linalg.norm(exact)),
                 "max_rel": float(np.max(np.abs(d) / np.abs(exact)))}
 
-    step()
+    P.oz2_dgemm("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0, C.data_ptr(), m, N)
     torch.cuda.synchronize()
     acc = {"sample": "8 x 8 entries, exact dot products (TwoProduct + fsum)",
            f"oz2_N{N}": errs(C[I][:, J].cpu().numpy()),

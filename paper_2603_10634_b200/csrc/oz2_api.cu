@@ -332,6 +332,11 @@ static PFN_encodeTiled_t encode_fn() {
     return fn;
 }
 
+// tuning knobs (read per call; defaults are the measured best)
+static int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
 // 2D byte tensor [outer][inner] with row pitch `pitch` bytes, box inner x outer, 128B swizzle
 static bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                      uint64_t pitch, uint32_t box_inner, uint32_t box_outer) {
@@ -341,16 +346,17 @@ static bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_
     cuuint64_t strides[1] = {pitch};
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t es[2] = {1, 1};
+    // L2 promotion of TMA misses (OZ2_L2PROMO: 0 none, 1 64B, 2 128B, 3 256B)
+    const int promo = env_int("OZ2_L2PROMO", 3);
+    const CUtensorMapL2promotion pr = promo == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                    : promo == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                    : promo == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                 : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, pr,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// tuning knobs (read per call; defaults are the measured best)
-static int env_int(const char* name, int dflt) {
-    const char* e = std::getenv(name);
-    return e ? std::atoi(e) : dflt;
-}
 static int sync_lead() {   // progress throttle of the residue GEMM (OZ2_SYNC_LEAD)
     const int v = env_int("OZ2_SYNC_LEAD", 2);
     return v < 0 ? 0 : v;

@@ -251,31 +251,38 @@ __device__ __forceinline__ void digits_one_modulus(const ModDig& md, int l, cons
         rf[q] = i2f_small(ri);
     }
     uint8_t* o = out + static_cast<int64_t>(md.plane0) * plane_stride;
+    // digit arithmetic on packed FP32 pairs (sm_100 FFMA2/FADD2); every value is an exact
+    // small integer, the magic-number adds implement round / ceil
+    const float2 M2 = make_float2(kMagic23, kMagic23), nM2 = make_float2(-kMagic23, -kMagic23);
     if (md.square) {
         // D1 = round(r/s) ties-to-even, D2 = r - s D1 (R9)
+        const float2 is2 = make_float2(md.inv_s_f, md.inv_s_f), ns2 = make_float2(-md.s_f, -md.s_f);
         uint32_t w1 = 0, w2 = 0;
 #pragma unroll
         for (int q = 0; q < 4; q += 2) {
-            const float a1 = fmaf(rf[q], md.inv_s_f, kMagic23) - kMagic23;
-            const float b1 = fmaf(rf[q + 1], md.inv_s_f, kMagic23) - kMagic23;
-            const float a2 = fmaf(-a1, md.s_f, rf[q]), b2 = fmaf(-b1, md.s_f, rf[q + 1]);
-            w1 |= static_cast<uint32_t>(cvt_e4m3x2(a1, b1)) << (8 * q);
-            w2 |= static_cast<uint32_t>(cvt_e4m3x2(a2, b2)) << (8 * q);
+            const float2 r = make_float2(rf[q], rf[q + 1]);
+            const float2 d1 = __fadd2_rn(__ffma2_rn(r, is2, M2), nM2);
+            const float2 d2 = __ffma2_rn(d1, ns2, r);
+            w1 |= static_cast<uint32_t>(cvt_e4m3x2(d1.x, d1.y)) << (8 * q);
+            w2 |= static_cast<uint32_t>(cvt_e4m3x2(d2.x, d2.y)) << (8 * q);
         }
         *reinterpret_cast<uint32_t*>(o) = w1;
         *reinterpret_cast<uint32_t*>(o + plane_stride) = w2;
     } else {
         // D1 = sign(r) ceil(|r|/16), D2 = r - 16 D1, D3 = D1 + D2
+        const float2 s16 = make_float2(0.0625f, 0.0625f), n16 = make_float2(-16.0f, -16.0f);
         uint32_t w1 = 0, w2 = 0, w3 = 0;
 #pragma unroll
         for (int q = 0; q < 4; q += 2) {
-            const float a1 = copysignf(__fadd_ru(fabsf(rf[q]) * 0.0625f, kMagic23) - kMagic23, rf[q]);
-            const float b1 = copysignf(__fadd_ru(fabsf(rf[q + 1]) * 0.0625f, kMagic23) - kMagic23, rf[q + 1]);
-            const float a2 = fmaf(-16.0f, a1, rf[q]), b2 = fmaf(-16.0f, b1, rf[q + 1]);
-            const float a3 = a1 + a2, b3 = b1 + b2;
-            w1 |= static_cast<uint32_t>(cvt_e4m3x2(a1, b1)) << (8 * q);
-            w2 |= static_cast<uint32_t>(cvt_e4m3x2(a2, b2)) << (8 * q);
-            w3 |= static_cast<uint32_t>(cvt_e4m3x2(a3, b3)) << (8 * q);
+            const float2 r = make_float2(rf[q], rf[q + 1]);
+            const float2 a = make_float2(fabsf(rf[q]), fabsf(rf[q + 1]));
+            const float2 c = __fadd2_rn(__ffma2_ru(a, s16, M2), nM2);          // ceil(|r|/16)
+            const float2 d1 = make_float2(copysignf(c.x, r.x), copysignf(c.y, r.y));
+            const float2 d2 = __ffma2_rn(d1, n16, r);
+            const float2 d3 = __fadd2_rn(d1, d2);
+            w1 |= static_cast<uint32_t>(cvt_e4m3x2(d1.x, d1.y)) << (8 * q);
+            w2 |= static_cast<uint32_t>(cvt_e4m3x2(d2.x, d2.y)) << (8 * q);
+            w3 |= static_cast<uint32_t>(cvt_e4m3x2(d3.x, d3.y)) << (8 * q);
         }
         *reinterpret_cast<uint32_t*>(o) = w1;
         *reinterpret_cast<uint32_t*>(o + plane_stride) = w2;

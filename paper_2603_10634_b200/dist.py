@@ -29,7 +29,11 @@ def dgemm_rowsharded(A_local, B, alpha=1.0, beta=0.0, C_local=None, num_moduli=1
     CUDA path (``paper_2603_10634_b200.dgemm``)."""
     import torch.distributed as dist
     if dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.broadcast(B, src=src, group=group)
+        # collectives need contiguous storage: broadcast whichever of B / B^T is contiguous
+        buf = B if B.is_contiguous() else B.t()
+        if not buf.is_contiguous():
+            raise ValueError("B must be row- or column-major contiguous")
+        dist.broadcast(buf, src=src, group=group)
     if gemm_fn is None:
         from .oz2 import dgemm
         gemm_fn = dgemm

@@ -190,7 +190,7 @@ def test_ragged_layouts(dev, transa, transb, N, phi):
     assert rel <= 1e-15
 
 
-@pytest.mark.parametrize("N", [2, 6, 12, 16, 20])
+@pytest.mark.parametrize("N", [2, 6, 12, 16, 20, 27, 33])
 def test_imported_exponents_bit_exact(dev, N):
     """Oracle exponents fed to the GPU (oracle -> GPU only): every residue and every
     output element bit-exact, including huge |A'| (>= 2^63 for N >= 14)."""
