@@ -92,6 +92,17 @@ __device__ __forceinline__ void tma_load_2d_cg2(const CUtensorMap* m, uint32_t l
           "r"(c0), "r"(c1), "l"(cache_hint)
         : "memory");
 }
+// 2-SM TMA multicast: the box lands at the same smem offset in every CTA of `mask`, and
+// each destination pair's leader barrier (same offset) counts the bytes
+__device__ __forceinline__ void tma_load_2d_cg2_mc(const CUtensorMap* m, uint32_t leader_bar, void* smem,
+                                                   int32_t c0, int32_t c1, uint16_t mask, uint64_t cache_hint) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+        " [%0], [%1, {%4, %5}], [%2], %3, %6;"
+        ::"r"(smem_u32(smem)), "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar), "h"(mask),
+          "r"(c0), "r"(c1), "l"(cache_hint)
+        : "memory");
+}
 __device__ __forceinline__ void mma_f8f6f4_cg2(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
                                                uint32_t idesc, uint32_t accumulate) {
     asm volatile(
@@ -100,12 +111,11 @@ __device__ __forceinline__ void mma_f8f6f4_cg2(uint32_t d_tmem, uint64_t a_desc,
         "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}"
         ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
 }
-// arrive on the barrier at the same smem offset in both CTAs of the pair
-__device__ __forceinline__ void mma_commit_cg2(uint64_t* bar) {
+// arrive on the barrier at the same smem offset in every CTA of `mask`
+__device__ __forceinline__ void mma_commit_cg2(uint64_t* bar, uint16_t mask) {
     asm volatile(
-        "{\n\t.reg .b16 msk;\n\tmov.b16 msk, 3;\n\t"
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], msk;\n\t}"
-        ::"r"(smem_u32(bar)) : "memory");
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+        ::"r"(smem_u32(bar)), "h"(mask) : "memory");
 }
 template <int CG>
 __device__ __forceinline__ void tmem_alloc_cg(uint32_t* dst_smem, uint32_t ncols) {
@@ -123,7 +133,7 @@ __device__ __forceinline__ void tmem_dealloc_cg(uint32_t taddr, uint32_t ncols) 
     else asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
 
-template <int MODE, int CG, int FL>
+template <int MODE, int CG, int FL, int MC>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
             const __grid_constant__ GemmParams P) {
@@ -143,8 +153,15 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 
     const uint32_t warp = warp_id_uniform();
     const uint32_t lane = lane_id();
-    const uint32_t rank = (CG == 2) ? cluster_rank() : 0u;
+    // cluster = MC pairs (CG = 2) of CTAs; pairs of one cluster work on horizontally
+    // adjacent tiles and share (multicast) the A operand
+    constexpr int CS = CG * MC;                                       // cluster size
+    const uint32_t crank = (CS > 1) ? cluster_rank() : 0u;
+    const uint32_t rank = crank & (CG - 1);                           // rank in the pair
+    const uint32_t pairi = crank / CG;                                // pair in the cluster
     const bool leader = rank == 0;
+    const uint16_t pair_mask = static_cast<uint16_t>(((1u << CG) - 1u) << (pairi * CG));
+    const uint16_t all_mask = static_cast<uint16_t>((1u << CS) - 1u);
 
     if (warp == 0) {
         if (elect_one()) {
@@ -152,7 +169,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             tma_prefetch_desc(&tmB);
             for (int s = 0; s < NS; ++s) {
                 mbar_init(&full[s], CG);          // CG = 2: leader expect_tx + peer arrive
-                mbar_init(&empty[s], 1);
+                mbar_init(&empty[s], MC);         // one MMA commit per pair reading the stage
             }
             for (int s = 0; s < 2; ++s) {
                 mbar_init(&tfull[s], 1);
@@ -165,16 +182,17 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         tmem_alloc_cg<CG>(tmem_slot, 512);
     }
     tc_fence_before();
-    if (CG == 2) cluster_sync_all();
+    if (CS > 1) cluster_sync_all();
     else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const int num_tiles = P.m_tiles * P.n_tiles;
+    const int n_super = P.n_tiles / MC;                  // MC tiles along n per cluster tile
+    const int num_tiles = P.m_tiles * n_super;
     const int prods = (MODE == MODE_RESIDUE) ? 3 * P.num_moduli : 1;
     const int nkb = P.num_k_blocks;
-    const int unit = blockIdx.x / CG;            // tile-processing unit (CTA or CTA pair)
-    const int units = gridDim.x / CG;
+    const int unit = blockIdx.x / CS;            // tile-processing unit (cluster)
+    const int units = gridDim.x / CS;
 
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
@@ -184,12 +202,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             const long long nunits = units;
             const int kc = P.sync_chunk > 0 ? P.sync_chunk : nkb;   // k-blocks per chunk
             const long long chunks_per_prod = (nkb + kc - 1) / kc;
-            const uint32_t full0 = smem_u32(&full[0]) & 0xFEFFFFFFu;   // leader's barrier (CG=2)
+            const uint32_t full0 = smem_u32(&full[0]) & 0xFEFFFFFFu;   // pair leader's barrier (TMA operand)
+            const uint32_t full_leader = (CS > 1) ? mapa_shared(smem_u32(&full[0]), crank & ~(CG - 1u)) : 0u;
             for (int tile = unit; tile < num_tiles; tile += units) {
                 int tm, tn;
-                tile_coords<16 / CG>(tile, P.m_tiles, P.n_tiles, tm, tn);
+                tile_coords<16 / CG>(tile, P.m_tiles, n_super, tm, tn);
+                tn = tn * MC + static_cast<int>(pairi);
                 for (int pr = 0; pr < prods; ++pr) {
-                    int a_row = tm * Cfg::TILE_M + static_cast<int>(rank) * BM;
+                    int a_row = tm * Cfg::TILE_M + static_cast<int>(rank) * BM + (MC == 2 ? static_cast<int>(pairi) * (BM / 2) : 0);
                     int b_row = tn * BN + static_cast<int>(rank) * Cfg::B_ROWS;
                     if (MODE == MODE_RESIDUE) {
                         const int l = pr / 3, x = pr - 3 * (pr / 3);
@@ -202,7 +222,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                             // (sync_chunk k-blocks each) ahead of the chip-wide average, so
                             // the operand panels streamed by all units stay L2-resident
                             // until every unit sharing them has read them
-                            if (leader) atomicAdd(P.progress, 1ull);
+                            if (crank == 0) atomicAdd(P.progress, 1ull);
                             const long long need = nunits * (g + 1 - P.sync_lead);
                             while (static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(P.progress)) < need)
                                 __nanosleep(128);
@@ -216,15 +236,23 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         } else {
                             const uint32_t lb = full0 + stage * 8u;
                             if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (Cfg::A_STAGE + Cfg::B_STAGE));
-                            else mbar_arrive_cluster(lb);
-                            tma_load_2d_cg2(&tmA, lb, sA + stage * Cfg::A_STAGE, kb * BK, a_row, kEvictNormal);
+                            else mbar_arrive_cluster(full_leader + stage * 8u);
+                            if (MC == 1) {
+                                tma_load_2d_cg2(&tmA, lb, sA + stage * Cfg::A_STAGE, kb * BK, a_row, kEvictNormal);
+                            } else {
+                                // this CTA's half of the A tile, multicast to the CTA with the same
+                                // rank in the other pair (which loads the other half for both)
+                                const uint16_t amask = static_cast<uint16_t>((1u << rank) | (1u << (rank + CG)));
+                                tma_load_2d_cg2_mc(&tmA, lb, sA + stage * Cfg::A_STAGE + pairi * (Cfg::A_STAGE / 2),
+                                                   kb * BK, a_row, amask, kEvictNormal);
+                            }
                             tma_load_2d_cg2(&tmB, lb, sB + stage * Cfg::B_STAGE, kb * BK, b_row, kEvictNormal);
                         }
                         if (++stage == NS) { stage = 0; phase ^= 1; }
                     }
                 }
             }
-            if (P.sync_lead > 0 && leader) {
+            if (P.sync_lead > 0 && crank == 0) {
                 // finished: count as having started every product so nobody waits on us
                 const long long gmax = static_cast<long long>((num_tiles + units - 1) / units) * prods * chunks_per_prod;
                 if (gmax > g) atomicAdd(P.progress, static_cast<unsigned long long>(gmax - g));
@@ -253,11 +281,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                             else mma_f8f6f4_cg2(d_tmem, a0 + 2 * kk, b0 + 2 * kk, idesc, (kb | kk) != 0);
                         }
                         if (CG == 1) mma_commit(&empty[stage]);
-                        else mma_commit_cg2(&empty[stage]);
+                        else mma_commit_cg2(&empty[stage], MC == 2 ? all_mask : pair_mask);
                         if (++stage == NS) { stage = 0; phase ^= 1; }
                     }
                     if (CG == 1) mma_commit(&tfull[slot]);
-                    else mma_commit_cg2(&tfull[slot]);
+                    else mma_commit_cg2(&tfull[slot], pair_mask);
                 }
             }
         }
@@ -266,7 +294,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         const uint32_t quad = warp & 3u;           // TMEM lane quadrant this warp may access
         const uint32_t half = (warp - 2u) >> 2;    // 128-column half of the 256-column tile
         const uint32_t row_in_tile = rank * BM + quad * 32u + lane;
-        const uint32_t tempty0 = (CG == 2) ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
+        const uint32_t tempty0 = (CG == 2) ? mapa_shared(smem_u32(&tempty[0]), crank & ~(CG - 1u)) : 0u;
         auto release_slot = [&](uint32_t slot) {
             // accumulator slot drained: hand it back to the (leader's) MMA warp
             tc_fence_before();
@@ -300,7 +328,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         uint32_t g = 0;
         for (int tile = unit; tile < num_tiles; tile += units) {
             int tm, tn;
-            tile_coords<16 / CG>(tile, P.m_tiles, P.n_tiles, tm, tn);
+            tile_coords<16 / CG>(tile, P.m_tiles, n_super, tm, tn);
+            tn = tn * MC + static_cast<int>(pairi);
             const int64_t row = static_cast<int64_t>(tm) * Cfg::TILE_M + row_in_tile;
             const int64_t col0 = static_cast<int64_t>(tn) * BN + half * 128u;
             const bool row_ok = row < P.m;
@@ -408,7 +437,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     }
 
     tc_fence_before();
-    if (CG == 2) cluster_sync_all();
+    if (CS > 1) cluster_sync_all();
     else __syncthreads();
     if (warp == 1) {
         __syncwarp();
@@ -417,52 +446,57 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     }
 }
 
-template <int MODE, int CG, int FL>
+template <int MODE, int CG, int FL, int MC>
 static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& gp,
                               int num_sms, cudaStream_t st) {
     static bool attr_set = false;
     using Cfg = GemmCfg<CG>;
-    const int num_tiles = gp.m_tiles * gp.n_tiles;
+    constexpr int CS = CG * MC;
+    const int num_tiles = gp.m_tiles * (gp.n_tiles / MC);
     if (num_tiles == 0) return cudaSuccess;
-    const int max_units = num_sms / CG;
+    const int max_units = num_sms / CS;
     const int units = num_tiles < max_units ? num_tiles : max_units;
     if (!attr_set) {
-        cudaError_t err = cudaFuncSetAttribute(gemm_kernel<MODE, CG, FL>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+        cudaError_t err = cudaFuncSetAttribute(gemm_kernel<MODE, CG, FL, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
         if (err != cudaSuccess) return err;
         attr_set = true;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(units * CG);
+    cfg.gridDim = dim3(units * CS);
     cfg.blockDim = dim3(GEMM_THREADS);
     cfg.dynamicSmemBytes = Cfg::SMEM;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.x = CS;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, CG, FL>, ta, tb, gp);
+    return cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, CG, FL, MC>, ta, tb, gp);
 }
 
-template <int CG>
+template <int CG, int MC>
 static cudaError_t launch_cg(int mode, int fl, const CUtensorMap& ta, const CUtensorMap& tb,
                             const GemmParams& gp, int num_sms, cudaStream_t st) {
-    if (mode == MODE_BOUND) return launch_one<MODE_BOUND, CG, 0>(ta, tb, gp, num_sms, st);
-    if (mode == MODE_RAW) return launch_one<MODE_RAW, CG, 0>(ta, tb, gp, num_sms, st);
+    if (mode == MODE_BOUND) return launch_one<MODE_BOUND, CG, 0, MC>(ta, tb, gp, num_sms, st);
+    if (mode == MODE_RAW) return launch_one<MODE_RAW, CG, 0, MC>(ta, tb, gp, num_sms, st);
     switch (fl) {
-        case 4: return launch_one<MODE_RESIDUE, CG, 4>(ta, tb, gp, num_sms, st);
-        case 5: return launch_one<MODE_RESIDUE, CG, 5>(ta, tb, gp, num_sms, st);
-        case 6: return launch_one<MODE_RESIDUE, CG, 6>(ta, tb, gp, num_sms, st);
-        default: return launch_one<MODE_RESIDUE, CG, 0>(ta, tb, gp, num_sms, st);
+        case 4: return launch_one<MODE_RESIDUE, CG, 4, MC>(ta, tb, gp, num_sms, st);
+        case 5: return launch_one<MODE_RESIDUE, CG, 5, MC>(ta, tb, gp, num_sms, st);
+        case 6: return launch_one<MODE_RESIDUE, CG, 6, MC>(ta, tb, gp, num_sms, st);
+        default: return launch_one<MODE_RESIDUE, CG, 0, MC>(ta, tb, gp, num_sms, st);
     }
 }
 
+// cg = 1: 128x256 single-CTA tiles; cg = 2: 256x256 CTA pairs; cg = 4: clusters of two
+// pairs on horizontally adjacent tiles sharing A by TMA multicast (needs even n_tiles)
 cudaError_t launch_gemm(int mode, int cg, int fused_limbs, const CUtensorMap& ta, const CUtensorMap& tb,
                         const GemmParams& gp, int num_sms, cudaStream_t st) {
-    const cudaError_t err = (cg == 2) ? launch_cg<2>(mode, fused_limbs, ta, tb, gp, num_sms, st)
-                                      : launch_cg<1>(mode, fused_limbs, ta, tb, gp, num_sms, st);
+    cudaError_t err;
+    if (cg == 4) err = launch_cg<2, 2>(mode, fused_limbs, ta, tb, gp, num_sms, st);
+    else if (cg == 2) err = launch_cg<2, 1>(mode, fused_limbs, ta, tb, gp, num_sms, st);
+    else err = launch_cg<1, 1>(mode, fused_limbs, ta, tb, gp, num_sms, st);
     if (err != cudaSuccess) return err;
     return cudaGetLastError();
 }

@@ -358,12 +358,20 @@ static bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_
 }
 
 static int sync_lead() {   // progress throttle of the residue GEMM (OZ2_SYNC_LEAD)
-    const int v = env_int("OZ2_SYNC_LEAD", 2);
+    const int v = env_int("OZ2_SYNC_LEAD", 1);
     return v < 0 ? 0 : v;
 }
-static int cta_group() {   // 1: 128x256 CTA tiles; 2: 256x256 CTA-pair tiles (OZ2_CG)
-    return env_int("OZ2_CG", 2) == 1 ? 1 : 2;
+// 1: 128x256 CTA tiles; 2: 256x256 CTA-pair tiles; 4: two pairs per cluster sharing A by
+// TMA multicast (needs an even number of 256-column tiles, else 2)   (OZ2_CG)
+static int cta_group(int64_t n_pad) {
+    const int v = env_int("OZ2_CG", 2);
+    if (v == 1) return 1;
+    if (v == 4 && (n_pad / BN) % 2 == 0) return 4;
+    return 2;
 }
+static int a_box_rows(int cg) { return cg == 4 ? BM / 2 : BM; }
+static int b_box_rows(int cg) { return cg == 1 ? BN : BN / 2; }
+static int tile_m(int cg) { return cg == 1 ? BM : 2 * BM; }
 
 static void phase_mark(int i) {
     if (!g_ts.timing) return;
@@ -432,15 +440,15 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
         // ---- step 2: bound GEMM C-bar' = A-bar B-bar, row/column maxima
         phase_mark(1);
         {
-            const int cg = cta_group();
+            const int cg = cta_group(L.n_pad);
             CUtensorMap ta, tb;
-            if (!make_map(&ta, abar, L.k_pad, L.m_pad, L.k_pad, BK, BM)) return OZ2_ERR_CUDA;
-            if (!make_map(&tb, bbar, L.k_pad, L.n_pad, L.k_pad, BK, BN / cg)) return OZ2_ERR_CUDA;
+            if (!make_map(&ta, abar, L.k_pad, L.m_pad, L.k_pad, BK, a_box_rows(cg))) return OZ2_ERR_CUDA;
+            if (!make_map(&tb, bbar, L.k_pad, L.n_pad, L.k_pad, BK, b_box_rows(cg))) return OZ2_ERR_CUDA;
             GemmParams gp;
             std::memset(&gp, 0, sizeof(gp));
             gp.m = static_cast<int>(m); gp.n = static_cast<int>(n);
             gp.num_k_blocks = static_cast<int>(L.k_pad / BK);
-            gp.m_tiles = static_cast<int>(L.m_pad / (BM * cg)); gp.n_tiles = static_cast<int>(L.n_pad / BN);
+            gp.m_tiles = static_cast<int>(L.m_pad / tile_m(cg)); gp.n_tiles = static_cast<int>(L.n_pad / BN);
             gp.rows_per_plane_a = static_cast<int>(L.m_pad); gp.rows_per_plane_b = static_cast<int>(L.n_pad);
             gp.rmax = rsmax; gp.smax = rsmax + m;
             OZ2_CK(launch_gemm(MODE_BOUND, cg, 0, ta, tb, gp, g_ts.num_sms, st));
@@ -478,19 +486,19 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
     phase_mark(4);
     int fused = 0;
     {
-        const int cg = cta_group();
+        const int cg = cta_group(L.n_pad);
         CUtensorMap ta, tb;
-        if (!make_map(&ta, digA, L.k_pad, static_cast<uint64_t>(pl->M) * L.m_pad, L.k_pad, BK, BM)) return OZ2_ERR_CUDA;
-        if (!make_map(&tb, digB, L.k_pad, static_cast<uint64_t>(pl->M) * L.n_pad, L.k_pad, BK, BN / cg)) return OZ2_ERR_CUDA;
+        if (!make_map(&ta, digA, L.k_pad, static_cast<uint64_t>(pl->M) * L.m_pad, L.k_pad, BK, a_box_rows(cg))) return OZ2_ERR_CUDA;
+        if (!make_map(&tb, digB, L.k_pad, static_cast<uint64_t>(pl->M) * L.n_pad, L.k_pad, BK, b_box_rows(cg))) return OZ2_ERR_CUDA;
         GemmParams gp = pl->gemm_mod;
         gp.m = static_cast<int>(m); gp.n = static_cast<int>(n);
         gp.num_k_blocks = static_cast<int>(L.k_pad / BK);
-        gp.m_tiles = static_cast<int>(L.m_pad / (BM * cg)); gp.n_tiles = static_cast<int>(L.n_pad / BN);
+        gp.m_tiles = static_cast<int>(L.m_pad / tile_m(cg)); gp.n_tiles = static_cast<int>(L.n_pad / BN);
         gp.rows_per_plane_a = static_cast<int>(L.m_pad); gp.rows_per_plane_b = static_cast<int>(L.n_pad);
         gp.num_moduli = N;
         gp.residues = res;
         gp.sync_lead = sync_lead();
-        gp.sync_chunk = env_int("OZ2_SYNC_CHUNK", 16);
+        gp.sync_chunk = env_int("OZ2_SYNC_CHUNK", 8);
         if (gp.sync_lead > 0) {
             gp.progress = reinterpret_cast<unsigned long long*>(maxbits);   // dead after step 3
             OZ2_CK(cudaMemsetAsync(gp.progress, 0, 8, st));
@@ -705,15 +713,15 @@ int oz2_fp8_gemm_raw(const uint8_t* a, const uint8_t* b, float* C32, int64_t m, 
     if (e) return e;
     if (k == 0) { OZ2_CK(cudaMemsetAsync(C32, 0, 4ull * m * n, g_ts.stream)); return OZ2_SUCCESS; }
     if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15u) return OZ2_ERR_NOT_SUPPORTED;
-    const int cg = cta_group();
+    const int cg = cta_group(((n + BN - 1) / BN) * BN);
     CUtensorMap ta, tb;
-    if (!make_map(&ta, a, k, m, k, BK, BM)) return OZ2_ERR_CUDA;
-    if (!make_map(&tb, b, k, n, k, BK, BN / cg)) return OZ2_ERR_CUDA;
+    if (!make_map(&ta, a, k, m, k, BK, a_box_rows(cg))) return OZ2_ERR_CUDA;
+    if (!make_map(&tb, b, k, n, k, BK, b_box_rows(cg))) return OZ2_ERR_CUDA;
     GemmParams gp;
     std::memset(&gp, 0, sizeof(gp));
     gp.m = static_cast<int>(m); gp.n = static_cast<int>(n);
     gp.num_k_blocks = static_cast<int>((k + BK - 1) / BK);
-    gp.m_tiles = static_cast<int>((m + BM * cg - 1) / (BM * cg)); gp.n_tiles = static_cast<int>((n + BN - 1) / BN);
+    gp.m_tiles = static_cast<int>((m + tile_m(cg) - 1) / tile_m(cg)); gp.n_tiles = static_cast<int>((n + BN - 1) / BN);
     gp.c32 = C32;
     OZ2_CK(launch_gemm(MODE_RAW, cg, 0, ta, tb, gp, g_ts.num_sms, g_ts.stream));
     return OZ2_SUCCESS;

@@ -21,10 +21,11 @@ from oracle import exact, fp8, fp32, moduli as mod, scheme
 from synth import gen_host
 
 
-@pytest.fixture(scope="module", params=["cg1", "cg2"])
+@pytest.fixture(scope="module", params=["cg1", "cg2", "cg4"])
 def dev(request):
-    """The library, once with 128x256 single-CTA GEMM tiles and once with 256x256
-    CTA-pair (tcgen05 cta_group::2) tiles (OZ2_CG selects the kernel per call)."""
+    """The library with each GEMM variant (OZ2_CG selects it per call): 128x256
+    single-CTA tiles, 256x256 CTA-pair (tcgen05 cta_group::2) tiles, and clusters of two
+    pairs sharing A by TMA multicast."""
     import os
     import torch
     if not torch.cuda.is_available():
@@ -32,7 +33,7 @@ def dev(request):
     import paper_2603_10634_b200 as P
     P.lib()
     old = os.environ.get("OZ2_CG")
-    os.environ["OZ2_CG"] = "2" if request.param == "cg2" else "1"
+    os.environ["OZ2_CG"] = request.param[2:]
     yield P
     if old is None:
         os.environ.pop("OZ2_CG", None)
