@@ -199,6 +199,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         if (elect_one()) {
             uint32_t stage = 0, phase = 0;
             long long g = 0;                         // throttle chunks started by this unit
+            bool throttle_on = true;
             const long long nunits = units;
             const int kc = P.sync_chunk > 0 ? P.sync_chunk : nkb;   // k-blocks per chunk
             const long long chunks_per_prod = (nkb + kc - 1) / kc;
@@ -221,11 +222,19 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                             // progress throttle: a unit may not run more than sync_lead chunks
                             // (sync_chunk k-blocks each) ahead of the chip-wide average, so
                             // the operand panels streamed by all units stay L2-resident
-                            // until every unit sharing them has read them
+                            // until every unit sharing them has read them.  It is only a
+                            // performance heuristic: a bounded wait (~1 ms) turns it off for
+                            // this CTA if other units cannot make progress (e.g. not all
+                            // resident), so it can never deadlock.
                             if (crank == 0) atomicAdd(P.progress, 1ull);
-                            const long long need = nunits * (g + 1 - P.sync_lead);
-                            while (static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(P.progress)) < need)
-                                __nanosleep(128);
+                            if (throttle_on) {
+                                const long long need = nunits * (g + 1 - P.sync_lead);
+                                int spins = 0;
+                                while (static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(P.progress)) < need) {
+                                    __nanosleep(128);
+                                    if (++spins > 8000) { throttle_on = false; break; }
+                                }
+                            }
                             ++g;
                         }
                         mbar_wait(&empty[stage], phase ^ 1);
@@ -454,13 +463,39 @@ static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, cons
     constexpr int CS = CG * MC;
     const int num_tiles = gp.m_tiles * (gp.n_tiles / MC);
     if (num_tiles == 0) return cudaSuccess;
-    const int max_units = num_sms / CS;
-    const int units = num_tiles < max_units ? num_tiles : max_units;
+    static int max_clusters = 0;               // co-resident clusters of this configuration
     if (!attr_set) {
         cudaError_t err = cudaFuncSetAttribute(gemm_kernel<MODE, CG, FL, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
         if (err != cudaSuccess) return err;
+        if (CS > 1) {
+            err = cudaFuncSetAttribute(gemm_kernel<MODE, CG, FL, MC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+            cudaLaunchConfig_t q = {};
+            q.gridDim = dim3((num_sms / CS) * CS);
+            q.blockDim = dim3(GEMM_THREADS);
+            q.dynamicSmemBytes = Cfg::SMEM;
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = CS;
+            qa[0].val.clusterDim.y = 1;
+            qa[0].val.clusterDim.z = 1;
+            q.attrs = qa;
+            q.numAttrs = 1;
+            int nc = 0;
+            if (cudaOccupancyMaxActiveClusters(&nc, gemm_kernel<MODE, CG, FL, MC>, &q) != cudaSuccess || nc <= 0) {
+                cudaGetLastError();
+                nc = num_sms / CS;
+            }
+            max_clusters = nc;
+        } else {
+            max_clusters = num_sms;
+        }
         attr_set = true;
     }
+    // persistent grid: never more units than can be resident at once (the progress
+    // throttle assumes every unit runs concurrently)
+    int max_units = num_sms / CS;
+    if (max_clusters < max_units) max_units = max_clusters;
+    const int units = num_tiles < max_units ? num_tiles : max_units;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(units * CS);
     cfg.blockDim = dim3(GEMM_THREADS);

@@ -266,3 +266,34 @@ def test_torch_wrapper_layouts(dev):
     C3 = torch.zeros(100, 90, dtype=torch.float64, device="cuda")     # row-major C
     dev.dgemm(A, B, C=C3, num_moduli=13)
     assert (torch.linalg.norm(C3 - ref) / torch.linalg.norm(ref)).item() < 1e-14
+
+
+def test_workspace_and_timing_api(dev):
+    """Caller-owned workspace (too small -> OZ2_ERR_WORKSPACE, exact size works), the
+    per-phase timers, and the single-process path of the row-sharded driver."""
+    import torch
+    from paper_2603_10634_b200.dist import dgemm_rowsharded
+    m, k, n, N = 300, 520, 270, 13
+    A = torch.from_numpy(gen_host(m, k, "phi", phi=1.0, seed=51)).cuda()
+    B = torch.from_numpy(gen_host(k, n, "phi", phi=1.0, seed=52)).cuda()
+    C = torch.zeros((n, m), dtype=torch.float64, device="cuda").t()
+    need = dev.oz2_workspace_size("N", "N", m, n, k, N)
+    small = torch.empty(need - 1024, dtype=torch.uint8, device="cuda")
+    dev.oz2_set_stream(torch.cuda.current_stream().cuda_stream)
+    dev.oz2_set_workspace(small.data_ptr(), small.numel())
+    args = ("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0, C.data_ptr(), m, N)
+    assert dev.oz2_dgemm(*args) == dev.OZ2_ERR_WORKSPACE
+    ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    dev.oz2_set_workspace(ws.data_ptr(), ws.numel())
+    dev.oz2_set_timing(True)
+    assert dev.oz2_dgemm(*args) == 0
+    ph = dev.oz2_get_timing()
+    dev.oz2_set_timing(False)
+    assert set(ph) == set(dev.PHASES)
+    parts = sum(v for key, v in ph.items() if key != "total")
+    assert ph["total"] > 0 and abs(parts - ph["total"]) <= 0.05 * ph["total"] + 0.05
+    dev.oz2_set_workspace(None, 0)
+    ref = scheme.dgemm(A.cpu().numpy(), B.cpu().numpy(), N).C
+    assert np.array_equal(C.cpu().numpy(), ref)
+    C2 = dgemm_rowsharded(A, B, num_moduli=N)          # no process group: plain call
+    assert np.array_equal(C2.cpu().numpy(), ref)
