@@ -372,10 +372,18 @@ def main():
         return
     import torch
     import torch.distributed as dist
+    # one process per GPU; OZ2_DIST_BACKEND=gloo (with ranks sharing a device when there
+    # are fewer GPUs than ranks) exists only to exercise the multi-rank control flow on a
+    # single-GPU box -- NCCL is the real path
+    dev_index = local_rank % max(1, torch.cuda.device_count())
     if world > 1:
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    out, extras = run_oz2(args, rank, world, local_rank)
+        torch.cuda.set_device(dev_index)
+        backend = os.environ.get("OZ2_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
+    out, extras = run_oz2(args, rank, world, dev_index)
     if rank == 0:
         if extras:
             out["e2e"] = extras.pop("e2e")

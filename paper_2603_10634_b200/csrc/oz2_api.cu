@@ -177,6 +177,7 @@ static Plan build_plan(int N) {
         md.pinv_d = 1.0 / p;
         md.p_f = static_cast<float>(p);
         md.pinv_f = 1.0f / static_cast<float>(p);
+        md.hp_f = (p % 2 == 0) ? 0.5f / static_cast<float>(p) : 0.0f;
         md.square = is_square_i(p) ? 1 : 0;
         const int s = md.square ? static_cast<int>(std::lround(std::sqrt(static_cast<double>(p)))) : 16;
         md.s_f = static_cast<float>(s);

@@ -73,6 +73,7 @@ struct GemmParams {
 struct ModDig {
     double p_d, pinv_d;
     float p_f, pinv_f, s_f, inv_s_f;
+    float hp_f;                  // (p even ? 1/2 : 0) / p: offset of the symmetric rounding
     int square;
     int plane0;                  // first digit plane of this modulus
 };

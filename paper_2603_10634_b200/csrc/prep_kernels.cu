@@ -219,7 +219,6 @@ __device__ __forceinline__ void digits_one_modulus(const ModDig& md, int l, cons
                                                    const double (&M)[4], const int (&E)[4],
                                                    const uint16_t* __restrict__ pow2tab,
                                                    uint8_t* out, int64_t plane_stride) {
-    const int p = static_cast<int>(md.p_f);
     const double pinv = md.pinv_d, pd = md.p_d, magic = kMagic52;
     float rf[4];
 #pragma unroll
@@ -245,10 +244,22 @@ __device__ __forceinline__ void digits_one_modulus(const ModDig& md, int l, cons
             const double rd = fma(-qq, pd, yy);                           // exact, |rd| < 1.5 p
             ri = __double2loint(rd + magic);
         }
-        // symmetric range [-floor(p/2), ceil(p/2)-1] (R2)
-        if (2 * ri >= p) ri -= p;
-        else if (2 * ri < -p) ri += p;
-        rf[q] = i2f_small(ri);
+        rf[q] = __int_as_float(0x4B400000 + ri);                          // r + 1.5 2^23
+    }
+    // exact symmetric range [-floor(p/2), ceil(p/2)-1] (R2) in packed FP32:
+    // r <- r - p round((r + h)/p), h = 0 (odd p) or 1/2 (even p): no ties can occur
+    {
+        const float2 M2 = make_float2(kMagic23, kMagic23), nM2 = make_float2(-kMagic23, -kMagic23);
+        const float2 pi2 = make_float2(md.pinv_f, md.pinv_f), hp2 = make_float2(md.hp_f, md.hp_f);
+        const float2 np2 = make_float2(-md.p_f, -md.p_f);
+#pragma unroll
+        for (int q = 0; q < 4; q += 2) {
+            const float2 r = __fadd2_rn(make_float2(rf[q], rf[q + 1]), nM2);
+            const float2 qv = __fadd2_rn(__fadd2_rn(__ffma2_rn(r, pi2, hp2), M2), nM2);
+            const float2 rs = __ffma2_rn(qv, np2, r);
+            rf[q] = rs.x;
+            rf[q + 1] = rs.y;
+        }
     }
     uint8_t* o = out + static_cast<int64_t>(md.plane0) * plane_stride;
     // digit arithmetic on packed FP32 pairs (sm_100 FFMA2/FADD2); every value is an exact
