@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="oz2", choices=["oz2", "reference"])
-    ap.add_argument("--n", type=int, default=16384)
+    ap.add_argument("--size", type=int, default=16384, help="m = n = k per GPU")
     ap.add_argument("--moduli", type=int, default=13)
     ap.add_argument("--phi", type=float, default=1.0)
     ap.add_argument("--no-extras", action="store_true", help="skip e2e/cuBLAS/accuracy/sweep/cpu legs")
@@ -153,8 +153,8 @@ def run_oz2(args, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    n = k = args.n
-    m = args.n                                   # rows per rank (weak scaling)
+    n = k = args.size
+    m = args.size                                   # rows per rank (weak scaling)
     N = args.moduli
     A = gen_device(m, k, "phi", phi=args.phi, seed=1000 + rank, device="cuda")
     B = gen_device(k, n, "phi", phi=args.phi, seed=7, device="cuda") if rank == 0 else \
@@ -232,7 +232,7 @@ def run_oz2(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (paper generator (rand-0.5)*exp(randn*phi), seeded, on device)",
-        "config": {"workload": f"config3: m=n=k={args.n} per GPU, phi={args.phi}, N={N} hybrid moduli, accurate mode",
+        "config": {"workload": f"config3: m=n=k={args.size} per GPU, phi={args.phi}, N={N} hybrid moduli, accurate mode",
                    "m_per_gpu": m, "n": n, "k": k, "num_moduli": N, "phi": args.phi,
                    "l2": "no flush: A, B, C are 2 GiB each (>> 126 MB L2)",
                    "parallelism": f"row-sharded A/C over {world} GPU(s), B broadcast (NCCL)" if world > 1 else "single GPU"},
@@ -327,7 +327,7 @@ def cpu_baseline(args, sample_rows=16, seed_off=0):
     from oracle import scheme
     from synth import gen_host
     s = sample_rows
-    k = args.n
+    k = args.size
     A = gen_host(s, k, "phi", phi=args.phi, seed=50 + seed_off)
     B = gen_host(k, s, "phi", phi=args.phi, seed=60 + seed_off)
     with threadpool_limits(limits=1):
@@ -349,15 +349,15 @@ def run_reference(args, rank, world):
     for s_ in range(args.steps):
         vals.append(cpu_baseline(args, sample_rows=2, seed_off=100 + s_))
     total = time.perf_counter() - t0
-    flops = sum(2.0 * 2 * 2 * args.n for _ in vals)
+    flops = sum(2.0 * 2 * 2 * args.size for _ in vals)
     value = flops / total / 1e12
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": f"config3 sub-blocks: 2 x {args.n} x 2 per step, N={args.moduli}, phi={args.phi}"},
+            "config": {"workload": f"config3 sub-blocks: 2 x {args.size} x 2 per step, N={args.moduli}, phi={args.phi}"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"2 x {args.n} x 2 sub-block per step (full oracle pipeline)"},
+                             "sample": f"2 x {args.size} x 2 sub-block per step (full oracle pipeline)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

@@ -27,7 +27,7 @@ extern "C" {
 #define OZ2_ERR_CUDA           1   /* a CUDA runtime call or kernel launch failed     */
 #define OZ2_ERR_ALLOC          2   /* device or pinned host allocation failed         */
 #define OZ2_ERR_WORKSPACE      3   /* caller-provided workspace smaller than needed   */
-#define OZ2_ERR_NOT_SUPPORTED  4   /* k > 65536, or no sm_100 device          */
+#define OZ2_ERR_NOT_SUPPORTED  4   /* k > 2^22, mixed host/device pointers, no sm_100 */
 #define OZ2_ERR_NONFINITE      5   /* oz2_get_status(): A or B held NaN/Inf           */
 
 /* ---- the primary call -------------------------------------------------------- */
@@ -38,9 +38,12 @@ extern "C" {
  * as C ~ AB; alpha, beta, trans and ld follow DGEMM).
  *
  *   transa, transb  'N'/'n' (op(X) = X), 'T'/'t'/'C'/'c' (op(X) = X^T).
- *   m, n, k         >= 0.  k <= 65536 (the paper's exactness assumption k <= 2^16,
- *                   P:208 and eq. error-free-FP8-matmult); larger k
- *                   returns OZ2_ERR_NOT_SUPPORTED.
+ *   m, n, k         >= 0.  The paper assumes k <= 2^16 so that one FP32 accumulation
+ *                   of digit products is exact (eq. error-free-FP8-matmult
+ *                   P:258-261); longer k (up to 2^22) runs every product in 2^16-long
+ *                   K segments whose results are reduced mod p and summed (exact
+ *                   modular arithmetic, DESIGN.md NEXT-2); k > 2^22 returns
+ *                   OZ2_ERR_NOT_SUPPORTED.
  *   A, lda          A is m x k (transa 'N', lda >= max(1,m)) or k x m (lda >= max(1,k)).
  *   B, ldb          B is k x n (transb 'N', ldb >= max(1,k)) or n x k (ldb >= max(1,n)).
  *   C, ldc          m x n, ldc >= max(1,m).  Read only when beta != 0.

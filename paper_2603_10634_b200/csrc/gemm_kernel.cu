@@ -189,8 +189,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 
     const int n_super = P.n_tiles / MC;                  // MC tiles along n per cluster tile
     const int num_tiles = P.m_tiles * n_super;
-    const int prods = (MODE == MODE_RESIDUE) ? 3 * P.num_moduli : 1;
     const int nkb = P.num_k_blocks;
+    // k > 2^16: each product runs as nseg segments of <= 512 k-blocks (2^16 elements), so
+    // every FP32 accumulation stays within the exactness window (eq. error-free-FP8-matmult);
+    // the epilogue reduces each segment mod p and accumulates the residue (NEXT-2)
+    const int nseg = (MODE == MODE_RESIDUE) ? P.num_kseg : 1;
+    const int kseg = (MODE == MODE_RESIDUE) ? P.kseg_blocks : nkb;
+    const int prods = (MODE == MODE_RESIDUE) ? 3 * P.num_moduli * nseg : 1;
     const int unit = blockIdx.x / CS;            // tile-processing unit (cluster)
     const int units = gridDim.x / CS;
 
@@ -212,12 +217,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 for (int pr = 0; pr < prods; ++pr) {
                     int a_row = tm * Cfg::TILE_M + static_cast<int>(rank) * BM + (MC == 2 ? static_cast<int>(pairi) * (BM / 2) : 0);
                     int b_row = tn * BN + static_cast<int>(rank) * Cfg::B_ROWS;
+                    int kb0 = 0, kb1 = nkb;
                     if (MODE == MODE_RESIDUE) {
-                        const int l = pr / 3, x = pr - 3 * (pr / 3);
+                        const int l = pr / (3 * nseg), rem = pr - l * 3 * nseg;
+                        const int x = rem / nseg, seg = rem - x * nseg;
                         a_row += P.mod[l].a_plane[x] * P.rows_per_plane_a;
                         b_row += P.mod[l].b_plane[x] * P.rows_per_plane_b;
+                        kb0 = seg * kseg;
+                        kb1 = min(nkb, kb0 + kseg);
                     }
-                    for (int kb = 0; kb < nkb; ++kb) {
+                    for (int kb = kb0; kb < kb1; ++kb) {
                         if (P.sync_lead > 0 && kb % kc == 0) {
                             // progress throttle: a unit may not run more than sync_lead chunks
                             // (sync_chunk k-blocks each) ahead of the chip-wide average, so
@@ -278,7 +287,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     mbar_wait(&tempty[slot], (use & 1u) ^ 1u);
                     tc_fence_after();
                     const uint32_t d_tmem = tmem_base + slot * BN;
-                    for (int kb = 0; kb < nkb; ++kb) {
+                    const int seg = (MODE == MODE_RESIDUE) ? pr % nseg : 0;
+                    const int kb0 = seg * kseg, kb1 = min(nkb, kb0 + kseg);
+                    for (int kb = kb0; kb < kb1; ++kb) {
                         mbar_wait(&full[stage], phase);
                         tc_fence_after();
                         const uint64_t a0 = make_desc_k128_sw128(smem_u32(sA + stage * Cfg::A_STAGE));
@@ -286,8 +297,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 #pragma unroll
                         for (int kk = 0; kk < BK / 32; ++kk) {
                             // advance 32 bytes of K inside the 128-byte swizzle atom
-                            if (CG == 1) mma_f8f6f4(d_tmem, a0 + 2 * kk, b0 + 2 * kk, idesc, (kb | kk) != 0);
-                            else mma_f8f6f4_cg2(d_tmem, a0 + 2 * kk, b0 + 2 * kk, idesc, (kb | kk) != 0);
+                            const uint32_t acc = (kb > kb0 || kk > 0) ? 1u : 0u;
+                            if (CG == 1) mma_f8f6f4(d_tmem, a0 + 2 * kk, b0 + 2 * kk, idesc, acc);
+                            else mma_f8f6f4_cg2(d_tmem, a0 + 2 * kk, b0 + 2 * kk, idesc, acc);
                         }
                         if (CG == 1) mma_commit(&empty[stage]);
                         else mma_commit_cg2(&empty[stage], MC == 2 ? all_mask : pair_mask);
@@ -350,8 +362,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     __half2 part[64];
                     int16_t* out = P.residues + (static_cast<int64_t>(l) * P.n + col0) * P.m + row;
 #pragma unroll
-                    for (int x = 0; x < 3; ++x, ++g) {
-                        const float coef = P.mod[l].coef[x];
+                    for (int x = 0; x < 3; ++x) {
+                      const float coef = P.mod[l].coef[x];
+                      for (int seg = 0; seg < nseg; ++seg, ++g) {
+                        const bool first = (x == 0) && (seg == 0);
+                        const bool last = (x == 2) && (seg == nseg - 1);
                         const uint32_t slot = g & 1u, use = g >> 1;
                         mbar_wait(&tfull[slot], use & 1u);
                         tc_fence_after();
@@ -372,7 +387,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                                     acc[u] = r;
                                 }
                                 const int idx = (c * 32 + j) >> 1;
-                                if (x == 0) {
+                                if (first) {
                                     acc[0] *= coef;
                                     acc[1] *= coef;
                                 } else {
@@ -382,7 +397,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                                 }
 #pragma unroll
                                 for (int u = 0; u < 2; ++u) acc[u] = fmaf(-rintf(acc[u] * pinv), p, acc[u]);
-                                if (x < 2) {
+                                if (!last) {
                                     part[idx] = __floats2half2_rn(acc[0], acc[1]);  // exact (|acc| <= 546)
                                 } else {
                                     // C'_l = mod(sum_x coef_x r_x, p), symmetric range (R2)
@@ -399,6 +414,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                             }
                         }
                         crt_steps(crt_per_prod);
+                      }
                     }
                 }
                 if (FL > 0) {

@@ -494,12 +494,19 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
         GemmParams gp = pl->gemm_mod;
         gp.m = static_cast<int>(m); gp.n = static_cast<int>(n);
         gp.num_k_blocks = static_cast<int>(L.k_pad / BK);
+        gp.kseg_blocks = kMaxK / BK;                                  // 2^16 per segment
+        gp.num_kseg = (gp.num_k_blocks + gp.kseg_blocks - 1) / gp.kseg_blocks;
         gp.m_tiles = static_cast<int>(L.m_pad / tile_m(cg)); gp.n_tiles = static_cast<int>(L.n_pad / BN);
         gp.rows_per_plane_a = static_cast<int>(L.m_pad); gp.rows_per_plane_b = static_cast<int>(L.n_pad);
         gp.num_moduli = N;
         gp.residues = res;
         gp.sync_lead = sync_lead();
-        gp.sync_chunk = env_int("OZ2_SYNC_CHUNK", 8);
+        {   // chunks must tile the 512-block K segments: a power of two in [1, 512]
+            int kc = env_int("OZ2_SYNC_CHUNK", 8);
+            int pw = 1;
+            while (pw * 2 <= kc && pw * 2 <= 512) pw *= 2;
+            gp.sync_chunk = pw;
+        }
         if (gp.sync_lead > 0) {
             gp.progress = reinterpret_cast<unsigned long long*>(maxbits);   // dead after step 3
             OZ2_CK(cudaMemsetAsync(gp.progress, 0, 8, st));
@@ -555,7 +562,7 @@ int dgemm_impl(char transa, char transb, int64_t m, int64_t n, int64_t k, double
     if (m == 0 || n == 0) return OZ2_SUCCESS;
     int e = ensure_device();
     if (e) return e;
-    if (k > 65536) return OZ2_ERR_NOT_SUPPORTED;
+    if (k > kMaxKTotal) return OZ2_ERR_NOT_SUPPORTED;      // f_k = 1/(1 - k 2^-23) needs k << 2^23
     if (m > (1ll << 30) || n > (1ll << 30)) return OZ2_ERR_NOT_SUPPORTED;
     cudaStream_t st = g_ts.stream;
     const bool quick = (alpha == 0.0 || k == 0);

@@ -11,6 +11,8 @@ namespace oz2 {
 constexpr int kMaxModuli = 33;   // N < 34
 constexpr int kMaxLimbs = 12;
 constexpr int kPow2Tab = 1024;   // 2^E mod p for E in [0, 1024)
+constexpr int kMaxK = 65536;     // exactness window of one FP32 accumulation
+constexpr int64_t kMaxKTotal = int64_t(1) << 22;   // longer k runs in 2^16 segments (NEXT-2)
 
 // ---- GEMM (tcgen05) ------------------------------------------------------------
 constexpr int BM = 128;          // rows of A per CTA tile (TMEM lanes)
@@ -48,6 +50,8 @@ struct ModEpi {          // per modulus, residue-GEMM epilogue (P:292-299, P:241
 struct GemmParams {
     int m, n;                    // true sizes (store masks)
     int num_k_blocks;
+    int num_kseg;                // residue mode: K segments of <= kseg_blocks k-blocks
+    int kseg_blocks;             // 512 (= 2^16 / BK): FP32 exactness window per segment
     int m_tiles, n_tiles;
     int rows_per_plane_a;        // m_pad
     int rows_per_plane_b;        // n_pad

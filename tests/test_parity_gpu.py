@@ -297,3 +297,17 @@ def test_workspace_and_timing_api(dev):
     assert np.array_equal(C.cpu().numpy(), ref)
     C2 = dgemm_rowsharded(A, B, num_moduli=N)          # no process group: plain call
     assert np.array_equal(C2.cpu().numpy(), ref)
+
+
+def test_k_beyond_exactness_window(dev):
+    """k > 2^16 (NEXT-2): products run in 2^16-long K segments reduced mod p; residues and C
+    stay bit-exact against the oracle, which needs no segmentation (exact integers)."""
+    from gpu_helpers import run
+    m, k, n, N = 16, 65536 + 300, 24, 12
+    A = gen_host(m, k, "phi", phi=1.0, seed=61)
+    B = gen_host(k, n, "phi", phi=1.0, seed=62)
+    ref = scheme.dgemm(A, B, N)
+    res = run(A, B, N, e_mu_in=ref.e_mu, e_nu_in=ref.e_nu)
+    for l in range(N):
+        assert np.array_equal(res["residues"][l], ref.residues[l]), l
+    assert np.array_equal(res["C"], ref.C)
