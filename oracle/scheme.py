@@ -172,6 +172,57 @@ def scaling_exponents(e_prime, Rmax, k: int, Pp: Fraction, dlt: Fraction, row_ze
 
 
 # ---------------------------------------------------------------------------------
+# fast mode (NEXT-1): Cauchy-Schwarz scaling
+
+
+FAST_INFLATE = Fraction(1) + Fraction(1, 2 ** 26)
+
+
+def round_up64(q: Fraction) -> Fraction:
+    """Smallest binary64 value >= q (q > 0, normal range)."""
+    f = float(q)                       # correctly rounded (nearest)
+    if Fraction(f) < q:
+        f = np.nextafter(f, np.inf)
+    return Fraction(float(f))
+
+
+def round_down64(q: Fraction) -> Fraction:
+    f = float(q)
+    if Fraction(f) > q:
+        f = np.nextafter(f, -np.inf)
+    return Fraction(float(f))
+
+
+def fast_exponent(sumsq: Fraction, H: Fraction):
+    """Reading R15.  Fast mode bounds 2 sum_h |a'_ih||b'_hj| by 2 mu_i nu_j ||a_i|| ||b_j||
+    (Cauchy-Schwarz) and needs mu_i ||a_i|| <= sqrt((P-1)/2) per side (the paper
+    prints no formula; SPEC S:218-226 gives e_i = floor(log2(sqrt((P-1)/2) / n_i))).
+    We take n2_i = RU64(sum_h a_ih^2 * (1 + 2^-26)), a certified upper bound of the squared
+    norm for any binary64 summation order (k <= 2^22), H = RD64((P-1)/2), and
+    e_i = max{e : 2^(2e) n2_i <= H}.  Zero rows get 0."""
+    if sumsq == 0:
+        return 0
+    n2 = round_up64(sumsq * FAST_INFLATE)
+    # largest e with 2^(2e) n2 <= H
+    e = math.floor(math.log2(float(H / n2)) / 2) + 1
+    while Fraction(2) ** (2 * e) * n2 > H:
+        e -= 1
+    while Fraction(2) ** (2 * (e + 1)) * n2 <= H:
+        e += 1
+    return e
+
+
+def fast_exponents(X: np.ndarray, plan) -> list:
+    """Fast-mode scaling exponents of the rows of X (A, or B^T for nu)."""
+    H = round_down64(Fraction(plan.P - 1, 2))
+    out = []
+    for row in X:
+        ss = sum((Fraction(float(v)) ** 2 for v in row), Fraction(0))
+        out.append(fast_exponent(ss, H))
+    return out
+
+
+# ---------------------------------------------------------------------------------
 # step 4-5: integers and residues (P:157-161, P:177)
 
 
@@ -335,7 +386,7 @@ def plan_constants(N: int):
 
 
 def dgemm(A: np.ndarray, B: np.ndarray, N: int, alpha: float = 1.0, beta: float = 0.0,
-          C=None, e_mu=None, e_nu=None, want_digits: bool = False) -> Result:
+          C=None, e_mu=None, e_nu=None, want_digits: bool = False, mode: str = "accurate") -> Result:
     """C <- alpha * emul(A B) + beta * C, accurate mode, hybrid moduli.
 
     ``e_mu`` / ``e_nu`` optionally fix the scaling exponents (used by tests that feed
@@ -354,6 +405,12 @@ def dgemm(A: np.ndarray, B: np.ndarray, N: int, alpha: float = 1.0, beta: float 
     R, S, _ = bound_row_col_max(Abar, BbarT)
     zA = [not np.any(A[i]) for i in range(m)]
     zB = [not np.any(BT[j]) for j in range(n)]
+    if mode == "fast":
+        # fast mode skips the bound GEMM (3N instead of 3N+1 GEMMs, Table 2)
+        if e_mu is None:
+            e_mu = fast_exponents(A, plan)
+        if e_nu is None:
+            e_nu = fast_exponents(BT, plan)
     if e_mu is None:
         e_mu = scaling_exponents(eA, R, k, Pp, dlt, zA)
     if e_nu is None:

@@ -281,3 +281,36 @@ def test_entries_match_full_oracle():
             assert C[a, b] == r.C[i, j]
             for l in range(13):
                 assert res[l, a, b] == r.residues[l][i, j]
+
+
+# ------------------------------------------------------------------ fast mode (NEXT-1)
+
+def test_fast_exponent_definition():
+    """e = max{e : 2^(2e) n2 <= H}: brute-force over a window, powers of two, zero row."""
+    from fractions import Fraction as F
+    H = scheme.round_down64(F(2 ** 111 - 1, 2))
+    for ss in [F(1), F(3, 7), F(2) ** -40, F(123456789), F(2) ** 60 + 1]:
+        e = scheme.fast_exponent(ss, H)
+        n2 = scheme.round_up64(ss * scheme.FAST_INFLATE)
+        assert F(2) ** (2 * e) * n2 <= H < F(2) ** (2 * (e + 1)) * n2
+    assert scheme.fast_exponent(F(0), H) == 0
+
+
+@pytest.mark.parametrize("phi", [0.0, 2.0])
+def test_fast_mode_certified_and_less_accurate(phi):
+    """Fast mode satisfies the condition 2 sum|a'||b'| < P exactly (Cauchy-Schwarz),
+    and its error is >= accurate mode's at equal N."""
+    m, k, n = 10, 60, 9
+    A = gen_host(m, k, "phi", phi=phi, seed=71, order="C")
+    B = gen_host(k, n, "phi", phi=phi, seed=72, order="C")
+    rf = scheme.dgemm(A, B, 12, mode="fast")
+    ra = scheme.dgemm(A, B, 12)
+    assert _certified(rf, A, B)
+    exactP = rf.extra["Aint"].dot(rf.extra["BintT"].T)
+    assert all(int(rf.extra["Cprime"][i, j]) == int(exactP[i, j]) for i in range(m) for j in range(n))
+    assert all(ef <= ea for ef, ea in zip(rf.e_mu, ra.e_mu))
+    F = exact.exact_gemm_fraction(A, B)
+    ex = np.array([[float(F[i, j]) for j in range(n)] for i in range(m)])
+    ef = np.linalg.norm(rf.C - ex) / np.linalg.norm(ex)
+    ea = np.linalg.norm(ra.C - ex) / np.linalg.norm(ex)
+    assert ea <= ef * 1.0000001 or ef < 1e-17
