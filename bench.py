@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--size", type=int, default=16384, help="m = n = k per GPU")
     ap.add_argument("--moduli", type=int, default=13)
     ap.add_argument("--phi", type=float, default=1.0)
+    ap.add_argument("--mode", default="accurate", choices=["accurate", "fast"],
+                    help="scaling mode (fast: Cauchy-Schwarz bound, no bound GEMM; DESIGN.md R15)")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e/cuBLAS/accuracy/sweep/cpu legs")
     return ap.parse_args()
 
@@ -165,6 +167,8 @@ def run_oz2(args, rank, world, local_rank):
     ws_bytes = P.oz2_workspace_size("N", "N", m, n, k, N)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
     P.oz2_set_workspace(ws.data_ptr(), ws.numel())
+    if P.oz2_set_mode(args.mode) != 0:
+        raise RuntimeError("oz2_set_mode failed")
 
     Bt = B.t()                                   # contiguous (n x k) storage of column-major B
 
@@ -225,17 +229,24 @@ def run_oz2(args, rank, world, local_rank):
                 "peak_source": f"{peak_kind}: 2 x bf16_tflops_sustained (nominal fp8/bf16 = 4.5/2.25)",
                 "algorithmic_flops_per_launch": gemm_flops,
                 "share_of_step": round(gemm_ms / phases["total"], 4)}
-    launches_per_step = 10
+    # rowmax x2, cast x2, [bound GEMM], exps, digits x2, residue GEMM, [k_crt unless fused]
+    fused = (P.oz2_plan_query(N, k).num_limbs <= 6 and k >= 8192
+             and os.environ.get("OZ2_FUSED_CRT", "1") != "0")
+    launches_per_step = 8 + (args.mode == "accurate") + (not fused)
 
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (paper generator (rand-0.5)*exp(randn*phi), seeded, on device)",
-        "config": {"workload": f"config3: m=n=k={args.size} per GPU, phi={args.phi}, N={N} hybrid moduli, accurate mode",
+        "config": {"workload": (f"{'config3' if args.size == 16384 else 'custom'}: m=n=k={args.size} per GPU, "
+                               f"phi={args.phi}, N={N} hybrid moduli, {args.mode} mode"),
+                   "mode": args.mode,
                    "m_per_gpu": m, "n": n, "k": k, "num_moduli": N, "phi": args.phi,
-                   "l2": "no flush: A, B, C are 2 GiB each (>> 126 MB L2)",
-                   "parallelism": f"row-sharded A/C over {world} GPU(s), B broadcast (NCCL)" if world > 1 else "single GPU"},
+                   "l2": (f"no flush: A, B, C are {8 * m * k / 2**30:.2f}, {8 * k * n / 2**30:.2f}, "
+                          f"{8 * m * n / 2**30:.2f} GiB (L2 is 126 MB)"),
+                   "parallelism": (f"row-sharded A/C over {world} GPU(s), B broadcast ({dist.get_backend()})"
+                                   if world > 1 else "single GPU")},
         "gpu_launches": launches_per_step * args.steps,
         "phases_ms": {k_: round(v, 3) for k_, v in phases.items()},
         "roofline": roofline,
@@ -295,6 +306,25 @@ def run_oz2(args, rank, world, local_rank):
         msN = e0.elapsed_time(e1) / 3
         sweep[str(NN)] = {"tflops": round(flops_rank / (msN * 1e-3) / 1e12, 3), **errs(C[I][:, J].cpu().numpy())}
     acc["moduli_sweep"] = sweep
+    # the other scaling mode on the same inputs (fast N=13 ~ accurate N=12)
+    other = "fast" if args.mode == "accurate" else "accurate"
+    P.oz2_set_mode(other)
+    osweep = {}
+    for NN in [12, 13, 14]:
+        if P.oz2_workspace_size("N", "N", m, n, k, NN) > ws.numel():
+            continue
+        f = lambda: P.oz2_dgemm("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0, C.data_ptr(), m, NN)
+        f()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(3):
+            f()
+        e1.record()
+        torch.cuda.synchronize()
+        msN = e0.elapsed_time(e1) / 3
+        osweep[str(NN)] = {"tflops": round(flops_rank / (msN * 1e-3) / 1e12, 3), **errs(C[I][:, J].cpu().numpy())}
+    P.oz2_set_mode(args.mode)
+    acc[f"{other}_mode_sweep"] = osweep
     extras["accuracy"] = acc
 
     # ---- e2e: host (pinned) buffers through the same C ABI

@@ -30,6 +30,10 @@ extern "C" {
 #define OZ2_ERR_NOT_SUPPORTED  4   /* k > 2^22, mixed host/device pointers, no sm_100 */
 #define OZ2_ERR_NONFINITE      5   /* oz2_get_status(): A or B held NaN/Inf           */
 
+/* ---- scaling modes (see oz2_set_mode) ------------------------------- */
+#define OZ2_MODE_ACCURATE      0   /* bound GEMM on FP8 tensor cores       */
+#define OZ2_MODE_FAST          1   /* Cauchy-Schwarz bound, no bound GEMM (R15)       */
+
 /* ---- the primary call -------------------------------------------------------- */
 
 /*
@@ -68,6 +72,11 @@ extern "C" {
  *   4. A' = trunc(diag(mu) A), residues mod p_l, FP8 digit split
  *   5. 3 exact FP8 GEMMs per modulus, reduced mod p_l in the epilogue             (eqs. 3matmult-notKaratsuba, C'-Karatsuba)
  *   6. C' = mod(sum_l q_l P/p_l C'_l, P) and C = diag(mu)^-1 C' diag(nu)^-1        (eqs. CRT_finalreduction, inversescaling)
+ *
+ * Fast mode (oz2_set_mode(OZ2_MODE_FAST), Table 2's 3N-GEMM variant) replaces
+ * steps 2-3 by the Cauchy-Schwarz bound (reading R15): S_i = sum_h A-bar_ih^2 (exact, from
+ * the step-1 FP8 upper bounds, accumulated in integers), log2 mu_i = e'_i + t_i with
+ * t_i = max{t : 2^(2t) S_i <= RD64((P-1)/2)}; same for nu.  Steps 4-6 are unchanged.
  *
  * Quick returns (BLAS): m == 0 or n == 0: nothing.  alpha == 0 or k == 0:
  * C <- beta C (C not read when beta == 0).
@@ -120,6 +129,12 @@ int oz2_dgemm_ex(char transa, char transb, int64_t m, int64_t n, int64_t k,
  * NULL = legacy default stream). */
 int oz2_set_stream(void* stream);
 
+/* Scaling mode for subsequent oz2_dgemm / oz2_dgemm_ex calls of this host thread:
+ * OZ2_MODE_ACCURATE (default) or OZ2_MODE_FAST; -1 for any other value.  In fast mode
+ * the abar/bbar/rmax/smax outputs of oz2_options are not written. */
+int oz2_set_mode(int mode);
+int oz2_get_mode(void);
+
 /* Bytes of device workspace a call with these arguments needs (0 on invalid args). */
 size_t oz2_workspace_size(char transa, char transb, int64_t m, int64_t n, int64_t k,
                           int num_moduli);
@@ -165,6 +180,7 @@ typedef struct oz2_plan_info {
     double  log2_P;            /* log2 P                                                   */
     uint32_t P_limbs[12];      /* P, little-endian 32-bit limbs (num_limbs used)           */
     uint32_t w_limbs[33][12];  /* w_l = q_l P/p_l (eq. CRT_finalreduction)                 */
+    double  fast_H;            /* RD64((P-1)/2), fast mode's per-side budget (R15)         */
 } oz2_plan_info;
 
 int oz2_plan_query(int num_moduli, int64_t k, oz2_plan_info* out);

@@ -193,33 +193,42 @@ def round_down64(q: Fraction) -> Fraction:
     return Fraction(float(f))
 
 
-def fast_exponent(sumsq: Fraction, H: Fraction):
-    """Reading R15.  Fast mode bounds 2 sum_h |a'_ih||b'_hj| by 2 mu_i nu_j ||a_i|| ||b_j||
-    (Cauchy-Schwarz) and needs mu_i ||a_i|| <= sqrt((P-1)/2) per side (the paper
-    prints no formula; SPEC S:218-226 gives e_i = floor(log2(sqrt((P-1)/2) / n_i))).
-    We take n2_i = RU64(sum_h a_ih^2 * (1 + 2^-26)), a certified upper bound of the squared
-    norm for any binary64 summation order (k <= 2^22), H = RD64((P-1)/2), and
-    e_i = max{e : 2^(2e) n2_i <= H}.  Zero rows get 0."""
-    if sumsq == 0:
-        return 0
-    n2 = round_up64(sumsq * FAST_INFLATE)
-    # largest e with 2^(2e) n2 <= H
-    e = math.floor(math.log2(float(H / n2)) / 2) + 1
-    while Fraction(2) ** (2 * e) * n2 > H:
-        e -= 1
-    while Fraction(2) ** (2 * (e + 1)) * n2 <= H:
-        e += 1
-    return e
+def fast_H(plan) -> Fraction:
+    """H = RD64((P-1)/2), the per-side budget of fast mode (reading R15)."""
+    return round_down64(Fraction(plan.P - 1, 2))
 
 
-def fast_exponents(X: np.ndarray, plan) -> list:
-    """Fast-mode scaling exponents of the rows of X (A, or B^T for nu)."""
-    H = round_down64(Fraction(plan.P - 1, 2))
+def fast_offset(S: Fraction, H: Fraction) -> int:
+    """t = max{t : 2^(2t) S <= H} for S > 0 (reading R15)."""
+    t = math.floor((math.log2(H) - math.log2(S)) / 2) + 1
+    while Fraction(2) ** (2 * t) * S > H:
+        t -= 1
+    while Fraction(2) ** (2 * (t + 1)) * S <= H:
+        t += 1
+    return t
+
+
+def fast_sumsq(codes: np.ndarray) -> list:
+    """S_i = sum_h abar_ih^2 over the FP8 upper bounds abar = RU_fp8(mu'|a|) (exact)."""
     out = []
-    for row in X:
-        ss = sum((Fraction(float(v)) ** 2 for v in row), Fraction(0))
-        out.append(fast_exponent(ss, H))
+    for row in codes:
+        out.append(sum((Fraction(fp8.decode(int(c))) ** 2 for c in row), Fraction(0)))
     return out
+
+
+def fast_exponents(e_prime, codes: np.ndarray, plan, row_zero) -> list:
+    """Fast-mode scaling exponents (Cauchy-Schwarz instead of the bound GEMM).
+
+    Reading R15.  With abar_ih = RU_fp8(2^e'_i |a_ih|) >= 2^e'_i |a_ih| and
+    a'_ih = trunc(2^(e'_i + t_i) a_ih):
+        2 sum_h |a'_ih||b'_hj| <= 2 2^(t_i + t_j) sum_h abar_ih bbar_hj
+                               <= 2 sqrt(2^(2 t_i) S_i) sqrt(2^(2 t_j) S_j) <= 2 H < P
+    when 2^(2 t) S <= H = RD64((P-1)/2) on both sides, so log2 mu_i = e'_i + t_i with the
+    largest such t_i certifies condition.  S_i is a sum of squares of E4M3
+    values (multiples of 2^-18), so it is exact in any order.  Zero rows get 0 (R3)."""
+    H = fast_H(plan)
+    S = fast_sumsq(codes)
+    return [0 if z else int(e) + fast_offset(s, H) for e, s, z in zip(e_prime, S, row_zero)]
 
 
 # ---------------------------------------------------------------------------------
@@ -408,9 +417,9 @@ def dgemm(A: np.ndarray, B: np.ndarray, N: int, alpha: float = 1.0, beta: float 
     if mode == "fast":
         # fast mode skips the bound GEMM (3N instead of 3N+1 GEMMs, Table 2)
         if e_mu is None:
-            e_mu = fast_exponents(A, plan)
+            e_mu = fast_exponents(eA, Abar, plan, zA)
         if e_nu is None:
-            e_nu = fast_exponents(BT, plan)
+            e_nu = fast_exponents(eB, BbarT, plan, zB)
     if e_mu is None:
         e_mu = scaling_exponents(eA, R, k, Pp, dlt, zA)
     if e_nu is None:

@@ -98,6 +98,7 @@ struct Plan {
     std::vector<int> p;
     float p_prime = 0, delta = 0;
     double log2P = 0;
+    FastExpParams fast{};             // H = RD64((P-1)/2) for fast mode (R15)
     CrtParams crt{};
     DigitParams dig{};
     GemmParams gemm_mod{};            // only .mod[] filled
@@ -133,6 +134,23 @@ static Plan build_plan(int N) {
     int shP = 0;
     const uint64_t topP = big_top64(P, shP);
     pl.log2P = static_cast<double>(static_cast<long double>(shP) + log2l(static_cast<long double>(topP)));
+    {   // H = RD64((P-1)/2).  P is even (1024 | P), so (P-1)/2 = F + 1/2 with F = P/2 - 1:
+        // exact as (2F+1) 2^-1 while F < 2^52, else RD64(F) = F truncated to 53 bits.
+        Big F = P;
+        big_divmod_small(F, 2);
+        for (auto& x : F) { if (x--) break; }
+        big_trim(F);
+        const int fb = big_bitlen(F);
+        int sh = 0;
+        const uint64_t top = big_top64(F, sh);           // F = top 2^sh (+ lower bits if sh > 0)
+        if (fb <= 52) {
+            pl.fast.h = 2 * top + 1;
+            pl.fast.th = -1;
+        } else {
+            pl.fast.h = top >> (fb - sh - 53);           // top has fb - sh significant bits
+            pl.fast.th = fb - 53;
+        }
+    }
     // CRT constants
     CrtParams& cp = pl.crt;
     std::memset(&cp, 0, sizeof(cp));
@@ -229,6 +247,7 @@ struct ThreadState {
     int32_t* d_status = nullptr;
     int device = -1;
     int num_sms = 0;
+    int mode = OZ2_MODE_ACCURATE;
     std::map<int, std::unique_ptr<Plan>> plans;
     bool timing = false;
     bool timed_last = false;
@@ -291,7 +310,7 @@ static inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * 
 struct Layout {
     int64_t m_pad, n_pad, k_pad;
     int M;
-    size_t maxbits, eprime, rsmax, eexp, digA, digB, res, total;
+    size_t maxbits, eprime, rsmax, sumsq, eexp, digA, digB, res, total;
 };
 
 static Layout make_layout(int64_t m, int64_t n, int64_t k, int N, int M) {
@@ -305,6 +324,7 @@ static Layout make_layout(int64_t m, int64_t n, int64_t k, int N, int M) {
     L.maxbits = off; off = align_up(off + 8 * mn, 256);
     L.eprime = off;  off = align_up(off + 4 * mn, 256);
     L.rsmax = off;   off = align_up(off + 4 * mn, 256);
+    L.sumsq = off;   off = align_up(off + 8 * mn, 256);
     L.eexp = off;    off = align_up(off + 4 * mn, 256);
     L.digA = off;    off = align_up(off + static_cast<size_t>(M) * L.m_pad * L.k_pad, 1024);
     L.digB = off;    off = align_up(off + static_cast<size_t>(M) * L.n_pad * L.k_pad, 1024);
@@ -411,6 +431,8 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
     auto* maxbits = reinterpret_cast<unsigned long long*>(ws + L.maxbits);
     auto* eprime = reinterpret_cast<int32_t*>(ws + L.eprime);
     auto* rsmax = reinterpret_cast<uint32_t*>(ws + L.rsmax);
+    auto* sumsq = reinterpret_cast<unsigned long long*>(ws + L.sumsq);
+    const bool fast = g_ts.mode == OZ2_MODE_FAST;
     auto* eexp = reinterpret_cast<int32_t*>(ws + L.eexp);
     uint8_t* digA = ws + L.digA;
     uint8_t* digB = ws + L.digB;
@@ -430,17 +452,20 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
         OZ2_CK(cudaMemsetAsync(rsmax, 0, 4 * static_cast<size_t>(m + n), st));
         OZ2_CK(launch_rowmax(A, m, k, lda, a_kmajor, maxbits, st));
         OZ2_CK(launch_rowmax(B, n, k, ldb, b_kmajor, maxbits + m, st));
-        OZ2_CK(launch_cast(A, m, k, lda, a_kmajor, maxbits, eprime, abar, L.m_pad, L.k_pad, g_ts.d_status, st));
-        OZ2_CK(launch_cast(B, n, k, ldb, b_kmajor, maxbits + m, eprime + m, bbar, L.n_pad, L.k_pad, g_ts.d_status, st));
+        if (fast) OZ2_CK(cudaMemsetAsync(sumsq, 0, 8 * static_cast<size_t>(m + n), st));
+        OZ2_CK(launch_cast(A, m, k, lda, a_kmajor, maxbits, eprime, abar, L.m_pad, L.k_pad, g_ts.d_status,
+                           fast ? sumsq : nullptr, st));
+        OZ2_CK(launch_cast(B, n, k, ldb, b_kmajor, maxbits + m, eprime + m, bbar, L.n_pad, L.k_pad, g_ts.d_status,
+                           fast ? sumsq + m : nullptr, st));
         if (opt && opt->e_prime_a) OZ2_CK(cudaMemcpyAsync(opt->e_prime_a, eprime, 4 * m, cudaMemcpyDeviceToDevice, st));
         if (opt && opt->e_prime_b) OZ2_CK(cudaMemcpyAsync(opt->e_prime_b, eprime + m, 4 * n, cudaMemcpyDeviceToDevice, st));
-        if (opt && opt->abar && k)
+        if (opt && opt->abar && k && !fast)
             OZ2_CK(cudaMemcpy2DAsync(opt->abar, k, abar, L.k_pad, k, m, cudaMemcpyDeviceToDevice, st));
-        if (opt && opt->bbar && k)
+        if (opt && opt->bbar && k && !fast)
             OZ2_CK(cudaMemcpy2DAsync(opt->bbar, k, bbar, L.k_pad, k, n, cudaMemcpyDeviceToDevice, st));
         // ---- step 2: bound GEMM C-bar' = A-bar B-bar, row/column maxima
         phase_mark(1);
-        {
+        if (!fast) {
             const int cg = cta_group(L.n_pad);
             CUtensorMap ta, tb;
             if (!make_map(&ta, abar, L.k_pad, L.m_pad, L.k_pad, BK, a_box_rows(cg))) return OZ2_ERR_CUDA;
@@ -454,12 +479,17 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             gp.rmax = rsmax; gp.smax = rsmax + m;
             OZ2_CK(launch_gemm(MODE_BOUND, cg, 0, ta, tb, gp, g_ts.num_sms, st));
         }
-        if (opt && opt->rmax) OZ2_CK(cudaMemcpyAsync(opt->rmax, rsmax, 4 * m, cudaMemcpyDeviceToDevice, st));
-        if (opt && opt->smax) OZ2_CK(cudaMemcpyAsync(opt->smax, rsmax + m, 4 * n, cudaMemcpyDeviceToDevice, st));
+        if (opt && opt->rmax && !fast) OZ2_CK(cudaMemcpyAsync(opt->rmax, rsmax, 4 * m, cudaMemcpyDeviceToDevice, st));
+        if (opt && opt->smax && !fast) OZ2_CK(cudaMemcpyAsync(opt->smax, rsmax + m, 4 * n, cudaMemcpyDeviceToDevice, st));
         // ---- step 3: scaling exponents (eq. mu-computation / nu-computation)
         phase_mark(2);
-        ExpParams ep{pl->p_prime, pl->delta, f_k_of(k)};
-        OZ2_CK(launch_exps(maxbits, eprime, rsmax, m + n, ep, eexp, st));
+        if (fast) {
+            // fast mode: Cauchy-Schwarz over the FP8 upper bounds, no bound GEMM (R15)
+            OZ2_CK(launch_exps_fast(maxbits, eprime, sumsq, m + n, pl->fast, eexp, st));
+        } else {
+            ExpParams ep{pl->p_prime, pl->delta, f_k_of(k)};
+            OZ2_CK(launch_exps(maxbits, eprime, rsmax, m + n, ep, eexp, st));
+        }
     } else {
         phase_mark(1);
         phase_mark(2);
@@ -633,6 +663,14 @@ size_t oz2_workspace_size(char transa, char transb, int64_t m, int64_t n, int64_
     return make_layout(m, n, k, num_moduli, pl.M).total;
 }
 
+int oz2_set_mode(int mode) {
+    if (mode != OZ2_MODE_ACCURATE && mode != OZ2_MODE_FAST) return -1;
+    g_ts.mode = mode;
+    return OZ2_SUCCESS;
+}
+
+int oz2_get_mode(void) { return g_ts.mode; }
+
 int oz2_set_workspace(void* ptr, size_t bytes) {
     g_ts.user_ws = ptr;
     g_ts.user_ws_bytes = ptr ? bytes : 0;
@@ -704,6 +742,7 @@ int oz2_plan_query(int num_moduli, int64_t k, oz2_plan_info* out) {
     out->delta = pl.delta;
     out->f_k = f_k_of(k);
     out->log2_P = pl.log2P;
+    out->fast_H = std::ldexp(static_cast<double>(pl.fast.h), pl.fast.th);
     for (int t = 0; t < pl.L && t < 12; ++t) out->P_limbs[t] = pl.crt.P[t];
     for (int l = 0; l < num_moduli; ++l)
         for (int t = 0; t < pl.L && t < 12; ++t) out->w_limbs[l][t] = pl.crt.w[l][t];

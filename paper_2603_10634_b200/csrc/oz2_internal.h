@@ -94,12 +94,22 @@ struct ExpParams {
     float p_prime, delta, f_k;
 };
 
+// fast mode: H = RD64((P-1)/2) = h 2^th, h < 2^53 (reading R15)
+struct FastExpParams {
+    unsigned long long h;
+    int th;
+};
+
 // launchers (defined in the .cu files)
 cudaError_t launch_rowmax(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
                           unsigned long long* maxbits, cudaStream_t st);
 cudaError_t launch_cast(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
                         const unsigned long long* maxbits, int32_t* eprime, uint8_t* xbar,
-                        int64_t rows_pad, int64_t k_pad, int32_t* status, cudaStream_t st);
+                        int64_t rows_pad, int64_t k_pad, int32_t* status,
+                        unsigned long long* sumsq, cudaStream_t st);
+cudaError_t launch_exps_fast(const unsigned long long* maxbits, const int32_t* eprime,
+                             const unsigned long long* sumsq, int64_t count, FastExpParams fp,
+                             int32_t* e_out, cudaStream_t st);
 cudaError_t launch_exps(const unsigned long long* maxbits, const int32_t* eprime,
                         const uint32_t* rsmax, int64_t count, ExpParams ep, int32_t* e_out,
                         cudaStream_t st);

@@ -128,12 +128,22 @@ __device__ __forceinline__ double pow2d(int e) {          // 2^e, |e| <= 1022
 
 // ---------------------------------------------------------------------------------
 // k_cast: e' and X-bar = RU_fp8(|x| 2^e')
+// FAST (fast mode, reading R15): X-bar is not stored; instead S_r = sum_h xbar_rh^2 is
+// accumulated exactly as an integer in units of 2^-18 (E4M3 squares are multiples of
+// 2^-18 and <= 2^16, so S_r < 2^56 for k <= 2^22 and the sum is order-independent).
 
-template <bool KMAJOR>
+__device__ __forceinline__ unsigned long long fp8_sq_units(uint32_t c) {   // code^2 / 2^-18
+    const uint32_t E = (c >> 3) & 15u, mt = c & 7u;
+    return E ? static_cast<unsigned long long>((8u + mt) * (8u + mt)) << (2 * E - 2)
+             : static_cast<unsigned long long>(mt * mt);
+}
+
+template <bool KMAJOR, bool FAST>
 __global__ void __launch_bounds__(256) k_cast(const double* __restrict__ X, int64_t rows, int64_t k,
                                               int64_t ld, const unsigned long long* __restrict__ maxbits,
                                               int32_t* __restrict__ eprime, uint8_t* __restrict__ xbar,
-                                              int64_t k_pad, int32_t* __restrict__ status) {
+                                              int64_t k_pad, int32_t* __restrict__ status,
+                                              unsigned long long* __restrict__ sumsq) {
     __shared__ double tile[TR * TP];
     const int64_t h0 = static_cast<int64_t>(blockIdx.x) * TH;
     const int64_t r0 = static_cast<int64_t>(blockIdx.y) * TR;
@@ -156,6 +166,7 @@ __global__ void __launch_bounds__(256) k_cast(const double* __restrict__ X, int6
         const int e = (r < rows) ? eprime_of(maxbits[r]) : 0;
         const double s1 = pow2d(e >> 1), s2 = pow2d(e - (e >> 1));   // 2^e in two exact steps
         uint32_t word = 0;
+        unsigned long long sq = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const double x = tile[rr * TP + lane * 4 + q];
@@ -164,9 +175,16 @@ __global__ void __launch_bounds__(256) k_cast(const double* __restrict__ X, int6
                 c = fp8_ru_code((fabs(x) * s1) * s2);
                 c = c ? c : 1u;               // an underflowed nonzero still rounds up to 2^-9
             }
-            word |= c << (8 * q);
+            if (FAST) sq += fp8_sq_units(c);
+            else word |= c << (8 * q);
         }
-        *reinterpret_cast<uint32_t*>(xbar + r * k_pad + h0 + lane * 4) = word;
+        if (FAST) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+            if (lane == 0 && sq && r < rows) atomicAdd(sumsq + r, sq);
+        } else {
+            *reinterpret_cast<uint32_t*>(xbar + r * k_pad + h0 + lane * 4) = word;
+        }
     }
 }
 
@@ -187,6 +205,32 @@ __global__ void k_exps(const unsigned long long* __restrict__ maxbits,
     const float x2 = __fmul_rd(ep.delta, x1);
     const float x3 = __fadd_rd(ep.p_prime, x2);
     e_out[r] = eprime[r] + static_cast<int>(floorf(x3));   // int() = floor (R8)
+}
+
+// ---------------------------------------------------------------------------------
+// k_exps_fast: fast-mode exponents (reading R15)
+//   log2 mu_r = e'_r + t_r,  t_r = max{t : 2^(2t) S_r <= H},  H = h 2^th = RD64((P-1)/2)
+// decided exactly in integers: with S_r = U 2^-18 the test is U <= h 2^d, d = th + 18 - 2t.
+
+__device__ __forceinline__ bool fast_fits(unsigned long long U, unsigned long long h, int hbits, int d) {
+    if (d >= 0) return hbits + d > 63 || U <= (h << d);
+    return -d < 64 && U <= (h >> -d);
+}
+
+__global__ void k_exps_fast(const unsigned long long* __restrict__ maxbits,
+                            const int32_t* __restrict__ eprime,
+                            const unsigned long long* __restrict__ sumsq, int64_t count,
+                            FastExpParams fp, int32_t* __restrict__ e_out) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= count) return;
+    const unsigned long long U = sumsq[r];
+    if (maxbits[r] == 0ull || U == 0ull) { e_out[r] = 0; return; }       // zero row (R3)
+    const int hbits = 64 - __clzll(static_cast<long long>(fp.h));
+    const int ubits = 64 - __clzll(static_cast<long long>(U));
+    // U < 2^ubits <= h 2^(ubits - hbits + 1): start one step above the answer
+    int t = (fp.th + 18 - (ubits - hbits + 1)) / 2 + 2;
+    while (!fast_fits(U, fp.h, hbits, fp.th + 18 - 2 * t)) --t;
+    e_out[r] = eprime[r] + t;
 }
 
 // ---------------------------------------------------------------------------------
@@ -398,10 +442,24 @@ cudaError_t launch_rowmax(const double* X, int64_t rows, int64_t k, int64_t ld, 
 
 cudaError_t launch_cast(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
                         const unsigned long long* maxbits, int32_t* eprime, uint8_t* xbar,
-                        int64_t rows_pad, int64_t k_pad, int32_t* status, cudaStream_t st) {
+                        int64_t rows_pad, int64_t k_pad, int32_t* status,
+                        unsigned long long* sumsq, cudaStream_t st) {
     dim3 grid(static_cast<unsigned>(k_pad / TH), static_cast<unsigned>(rows_pad / TR));
-    if (kmajor) k_cast<true><<<grid, 256, 0, st>>>(X, rows, k, ld, maxbits, eprime, xbar, k_pad, status);
-    else k_cast<false><<<grid, 256, 0, st>>>(X, rows, k, ld, maxbits, eprime, xbar, k_pad, status);
+    if (sumsq) {
+        if (kmajor) k_cast<true, true><<<grid, 256, 0, st>>>(X, rows, k, ld, maxbits, eprime, xbar, k_pad, status, sumsq);
+        else k_cast<false, true><<<grid, 256, 0, st>>>(X, rows, k, ld, maxbits, eprime, xbar, k_pad, status, sumsq);
+    } else {
+        if (kmajor) k_cast<true, false><<<grid, 256, 0, st>>>(X, rows, k, ld, maxbits, eprime, xbar, k_pad, status, sumsq);
+        else k_cast<false, false><<<grid, 256, 0, st>>>(X, rows, k, ld, maxbits, eprime, xbar, k_pad, status, sumsq);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_exps_fast(const unsigned long long* maxbits, const int32_t* eprime,
+                             const unsigned long long* sumsq, int64_t count, FastExpParams fp,
+                             int32_t* e_out, cudaStream_t st) {
+    if (count == 0) return cudaSuccess;
+    k_exps_fast<<<static_cast<unsigned>((count + 255) / 256), 256, 0, st>>>(maxbits, eprime, sumsq, count, fp, e_out);
     return cudaGetLastError();
 }
 

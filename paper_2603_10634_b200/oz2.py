@@ -17,6 +17,9 @@ OZ2_ERR_ALLOC = 2
 OZ2_ERR_WORKSPACE = 3
 OZ2_ERR_NOT_SUPPORTED = 4
 OZ2_ERR_NONFINITE = 5
+OZ2_MODE_ACCURATE = 0
+OZ2_MODE_FAST = 1
+_MODES = {"accurate": OZ2_MODE_ACCURATE, "fast": OZ2_MODE_FAST}
 
 _c_int64 = ctypes.c_int64
 _vp = ctypes.c_void_p
@@ -40,6 +43,7 @@ class oz2_plan_info(ctypes.Structure):
         ("log2_P", ctypes.c_double),
         ("P_limbs", ctypes.c_uint32 * 12),
         ("w_limbs", (ctypes.c_uint32 * 12) * 33),
+        ("fast_H", ctypes.c_double),
     ]
 
 
@@ -52,6 +56,8 @@ SIGNATURES = [
      [ctypes.c_char, ctypes.c_char, _c_int64, _c_int64, _c_int64, ctypes.c_double, _vp, _c_int64,
       _vp, _c_int64, ctypes.c_double, _vp, _c_int64, ctypes.c_int, ctypes.POINTER(oz2_options)]),
     ("oz2_set_stream", ctypes.c_int, [_vp]),
+    ("oz2_set_mode", ctypes.c_int, [ctypes.c_int]),
+    ("oz2_get_mode", ctypes.c_int, []),
     ("oz2_workspace_size", ctypes.c_size_t,
      [ctypes.c_char, ctypes.c_char, _c_int64, _c_int64, _c_int64, ctypes.c_int]),
     ("oz2_set_workspace", ctypes.c_int, [_vp, ctypes.c_size_t]),
@@ -109,6 +115,15 @@ def oz2_dgemm_ex(transa, transb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, n
 
 def oz2_set_stream(stream):
     return lib().oz2_set_stream(stream)
+
+
+def oz2_set_mode(mode):
+    """mode: OZ2_MODE_ACCURATE / OZ2_MODE_FAST or "accurate" / "fast"."""
+    return lib().oz2_set_mode(_MODES.get(mode, mode))
+
+
+def oz2_get_mode():
+    return lib().oz2_get_mode()
 
 
 def oz2_workspace_size(transa, transb, m, n, k, num_moduli):
@@ -193,10 +208,22 @@ def _colmajor(X):
     return X, "N", X.stride(1)
 
 
-def dgemm(A, B, alpha=1.0, beta=0.0, C=None, num_moduli=13):
+def dgemm(A, B, alpha=1.0, beta=0.0, C=None, num_moduli=13, mode=None):
     """C <- alpha A @ B + beta C on torch float64 CUDA tensors via oz2_dgemm.
 
-    Any 2-D strided layout is accepted; the result is column-major (Fortran order)."""
+    Any 2-D strided layout is accepted; the result is column-major (Fortran order).
+    ``mode`` ("accurate" / "fast") applies to this call only; None keeps the thread's."""
+    if mode is None:
+        return _dgemm(A, B, alpha, beta, C, num_moduli)
+    prev = oz2_get_mode()
+    _check(oz2_set_mode(mode), "oz2_set_mode")
+    try:
+        return _dgemm(A, B, alpha, beta, C, num_moduli)
+    finally:
+        oz2_set_mode(prev)
+
+
+def _dgemm(A, B, alpha, beta, C, num_moduli):
     import torch
     assert A.dtype == torch.float64 and B.dtype == torch.float64
     m, k = A.shape

@@ -24,7 +24,7 @@ def store(X: np.ndarray, trans: str):
 
 
 def run(A, B, N, transa="N", transb="N", alpha=1.0, beta=0.0, C0=None, e_mu_in=None,
-        e_nu_in=None, want_digits=False, ldc_pad=0):
+        e_nu_in=None, want_digits=False, ldc_pad=0, mode="accurate"):
     """Full pipeline through oz2_dgemm_ex; returns dict of host numpy outputs."""
     t = torch()
     m, k = A.shape
@@ -64,8 +64,12 @@ def run(A, B, N, transa="N", transb="N", alpha=1.0, beta=0.0, C0=None, e_mu_in=N
         opt.e_nu_in = b.data_ptr()
     oz2.oz2_set_stream(t.cuda.current_stream().cuda_stream)
     oz2.oz2_set_workspace(None, 0)
-    rc = oz2.oz2_dgemm_ex(transa, transb, m, n, k, alpha, dA.data_ptr(), lda, dB.data_ptr(), ldb,
-                          beta, dC.data_ptr(), ldc, N, opt)
+    assert oz2.oz2_set_mode(mode) == 0
+    try:
+        rc = oz2.oz2_dgemm_ex(transa, transb, m, n, k, alpha, dA.data_ptr(), lda, dB.data_ptr(),
+                              ldb, beta, dC.data_ptr(), ldc, N, opt)
+    finally:
+        oz2.oz2_set_mode("accurate")
     assert rc == 0, rc
     t.cuda.synchronize()
     res = {key: v.cpu().numpy() for key, v in out.items()}

@@ -73,6 +73,15 @@ def test_plan_constants_match_oracle(oz2mod):
             assert sum(info.P_limbs[t] << (32 * t) for t in range(L)) == plan.P
             for l, w in enumerate(plan.w):
                 assert sum(info.w_limbs[l][t] << (32 * t) for t in range(L)) == w
+        # fast mode's per-side budget H = RD64((P-1)/2) (R15)
+        assert Fraction(info.fast_H) == scheme.fast_H(plan)
+
+
+def test_mode_switch(oz2mod):
+    assert oz2mod.oz2_get_mode() == oz2mod.OZ2_MODE_ACCURATE
+    assert oz2mod.oz2_set_mode("fast") == 0 and oz2mod.oz2_get_mode() == oz2mod.OZ2_MODE_FAST
+    assert oz2mod.oz2_set_mode(7) == -1 and oz2mod.oz2_get_mode() == oz2mod.OZ2_MODE_FAST
+    assert oz2mod.oz2_set_mode("accurate") == 0 and oz2mod.oz2_get_mode() == oz2mod.OZ2_MODE_ACCURATE
 
 
 def test_argument_errors_before_device(oz2mod):

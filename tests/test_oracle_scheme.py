@@ -285,15 +285,24 @@ def test_entries_match_full_oracle():
 
 # ------------------------------------------------------------------ fast mode (NEXT-1)
 
-def test_fast_exponent_definition():
-    """e = max{e : 2^(2e) n2 <= H}: brute-force over a window, powers of two, zero row."""
+def test_fast_offset_definition():
+    """t = max{t : 2^(2t) S <= H}: bracketing check, including exact powers of two."""
     from fractions import Fraction as F
-    H = scheme.round_down64(F(2 ** 111 - 1, 2))
-    for ss in [F(1), F(3, 7), F(2) ** -40, F(123456789), F(2) ** 60 + 1]:
-        e = scheme.fast_exponent(ss, H)
-        n2 = scheme.round_up64(ss * scheme.FAST_INFLATE)
-        assert F(2) ** (2 * e) * n2 <= H < F(2) ** (2 * (e + 1)) * n2
-    assert scheme.fast_exponent(F(0), H) == 0
+    plan, _, _ = scheme.plan_constants(12)
+    H = scheme.fast_H(plan)
+    assert H <= F(plan.P - 1, 2) < H * (1 + F(1, 2 ** 52))
+    for S in [F(1), F(3, 7), F(2) ** -18, F(225, 2 ** 18), F(2) ** 38, H, H / 4, H * 4 + 1]:
+        t = scheme.fast_offset(S, H)
+        assert F(2) ** (2 * t) * S <= H < F(2) ** (2 * (t + 1)) * S
+    # S = H / 4 exactly -> t = 1 (boundary inclusive)
+    assert scheme.fast_offset(H / 4, H) == 1
+
+
+def test_fast_H_small_P():
+    """N = 2: P = 1089 * 1024, (P-1)/2 is exactly representable."""
+    from fractions import Fraction as F
+    plan, _, _ = scheme.plan_constants(2)
+    assert scheme.fast_H(plan) == F(1089 * 1024 - 1, 2)
 
 
 @pytest.mark.parametrize("phi", [0.0, 2.0])
@@ -308,7 +317,12 @@ def test_fast_mode_certified_and_less_accurate(phi):
     assert _certified(rf, A, B)
     exactP = rf.extra["Aint"].dot(rf.extra["BintT"].T)
     assert all(int(rf.extra["Cprime"][i, j]) == int(exactP[i, j]) for i in range(m) for j in range(n))
-    assert all(ef <= ea for ef, ea in zip(rf.e_mu, ra.e_mu))
+    # the bound is Cauchy-Schwarz over the FP8 upper bounds: recompute S_i by brute force
+    for i in range(m):
+        Si = sum(Fraction(fp8.decode(int(c))) ** 2 for c in rf.Abar[i])
+        H = scheme.fast_H(rf.plan)
+        t = rf.e_mu[i] - rf.e_prime_A[i]
+        assert Fraction(4) ** t * Si <= H < Fraction(4) ** (t + 1) * Si
     F = exact.exact_gemm_fraction(A, B)
     ex = np.array([[float(F[i, j]) for j in range(n)] for i in range(m)])
     ef = np.linalg.norm(rf.C - ex) / np.linalg.norm(ex)

@@ -24,7 +24,7 @@ def dev():
     return P
 
 
-def _run_sampled(P, m, k, n, N, phi, seed, I, J):
+def _run_sampled(P, m, k, n, N, phi, seed, I, J, mode="accurate"):
     import torch
     A = gen_device(m, k, "phi", phi=phi, seed=seed)
     B = gen_device(k, n, "phi", phi=phi, seed=seed + 1)
@@ -38,8 +38,12 @@ def _run_sampled(P, m, k, n, N, phi, seed, I, J):
     opt.residues = res.data_ptr()
     P.oz2_set_stream(torch.cuda.current_stream().cuda_stream)
     P.oz2_set_workspace(None, 0)
-    rc = P.oz2_dgemm_ex("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0,
-                        C.data_ptr(), m, N, opt)
+    assert P.oz2_set_mode(mode) == 0
+    try:
+        rc = P.oz2_dgemm_ex("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0,
+                            C.data_ptr(), m, N, opt)
+    finally:
+        P.oz2_set_mode("accurate")
     assert rc == 0
     torch.cuda.synchronize()
     It = torch.tensor(I, device="cuda")
@@ -61,10 +65,21 @@ def _run_sampled(P, m, k, n, N, phi, seed, I, J):
     return out
 
 
-def _check(out, N, I, J, ref_exps=None):
+def _fast_exps(X, rows, N):
+    """Oracle fast-mode exponents of the selected rows of X (R15: each is row-local)."""
+    plan, _, _ = scheme.plan_constants(N)
+    Xs = X[rows]
+    e_prime, codes = scheme.prescale_rows(Xs)
+    zero = [not np.any(r) for r in Xs]
+    return scheme.fast_exponents(e_prime, codes, plan, zero)
+
+
+def _check(out, N, I, J, ref_exps=None, mode="accurate"):
     A, B = out["A"], out["B"]
     k = A.shape[1]
-    if ref_exps is None:
+    if mode == "fast":
+        emu, enu = _fast_exps(A, I, N), _fast_exps(B.T, J, N)
+    elif ref_exps is None:
         _, emu, _ = scheme.row_exponents(A, I, B.T, N)
         _, enu, _ = scheme.row_exponents(B.T, J, A, N)
     else:
@@ -105,3 +120,19 @@ def test_config4_large_k_65536(dev, N, phi):
     I, J = [0, 2048, 4095], [7, 4000]
     out = _run_sampled(dev, 4096, 65536, 4096, N, phi, 31, I, J)
     _check(out, N, I, J)
+
+
+@pytest.mark.parametrize("N", [13, 16])
+def test_config3_16384_fast_mode(dev, N):
+    """Fast mode (R15) at the bench workload: exponents, residues and C bit-exact on the
+    sampled entries; fast mode with N = 13 stays within the FP64-level band."""
+    I, J = [3, 9000, 16383], [0, 12345]
+    out = _run_sampled(dev, 16384, 16384, 16384, N, 1.0, 21, I, J, mode="fast")
+    err = _check(out, N, I, J, mode="fast")
+    assert err < 1e-14
+
+
+def test_config4_large_k_65536_fast_mode(dev):
+    I, J = [0, 2048, 4095], [7, 4000]
+    out = _run_sampled(dev, 4096, 65536, 4096, 13, 4.0, 31, I, J, mode="fast")
+    _check(out, 13, I, J, mode="fast")
