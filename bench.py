@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--size", type=int, default=16384, help="m = n = k per GPU")
     ap.add_argument("--moduli", type=int, default=13)
     ap.add_argument("--phi", type=float, default=1.0)
+    ap.add_argument("--scheme", default="fp8", choices=["fp8", "int8"],
+                    help="fp8: the paper's method (default); int8: the INT8 Ozaki-II baseline (R16)")
     ap.add_argument("--mode", default="accurate", choices=["accurate", "fast"],
                     help="scaling mode (fast: Cauchy-Schwarz bound, no bound GEMM; DESIGN.md R15)")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e/cuBLAS/accuracy/sweep/cpu legs")
@@ -164,11 +166,12 @@ def run_oz2(args, rank, world, local_rank):
     C = torch.empty((n, m), dtype=torch.float64, device="cuda").t()
     stream = torch.cuda.current_stream()
     P.oz2_set_stream(stream.cuda_stream)
-    ws_bytes = P.oz2_workspace_size("N", "N", m, n, k, N)
+    P.oz2_set_scheme(args.scheme)
+    ws_bytes = max(P.oz2_workspace_size("N", "N", m, n, k, N), P.oz2_workspace_size("N", "N", m, n, k, 16))
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
     P.oz2_set_workspace(ws.data_ptr(), ws.numel())
-    if P.oz2_set_mode(args.mode) != 0:
-        raise RuntimeError("oz2_set_mode failed")
+    if P.oz2_set_mode(args.mode) != 0 or P.oz2_set_scheme(args.scheme) != 0:
+        raise RuntimeError("oz2_set_mode / oz2_set_scheme failed")
 
     Bt = B.t()                                   # contiguous (n x k) storage of column-major B
 
@@ -217,16 +220,21 @@ def run_oz2(args, rank, world, local_rank):
     peaks, peak_kind = measured_peaks()
     fp8_peak = 2.0 * peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
     gemm_ms = statistics.mean(phase_acc["residue_gemm"])
-    gemm_flops = 3 * N * 2.0 * m * n * k
+    n_prod = N if args.scheme == "int8" else 3 * N       # products per output element (Table 2)
+    gemm_flops = n_prod * 2.0 * m * n * k
     achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12
     traffic = None
     tr = ncu_traffic()
-    if tr and tr.get("m") == m and tr.get("num_moduli") == N:
+    if tr and tr.get("m") == m and tr.get("num_moduli") == N and tr.get("scheme", "fp8") == args.scheme:
         traffic = tr.get("dram_bytes_per_launch")
-    roofline = {"kernel": "gemm_kernel<MODE_RESIDUE> (3N tcgen05 FP8 GEMMs + modular epilogue)",
+    kname = ("gemm_kernel<MODE_RESIDUE_I8> (N tcgen05 kind::i8 GEMMs + modular epilogue)" if args.scheme == "int8"
+             else "gemm_kernel<MODE_RESIDUE> (3N tcgen05 FP8 GEMMs + modular epilogue)")
+    roofline = {"kernel": kname,
                 "bound": "tensor", "achieved": round(achieved, 1), "peak": round(fp8_peak, 1),
-                "unit": "TFLOP/s", "frac": round(achieved / fp8_peak, 4), "traffic": traffic,
-                "peak_source": f"{peak_kind}: 2 x bf16_tflops_sustained (nominal fp8/bf16 = 4.5/2.25)",
+                "unit": "TFLOP/s" if args.scheme == "fp8" else "TOP/s",
+                "frac": round(achieved / fp8_peak, 4), "traffic": traffic,
+                "peak_source": (f"{peak_kind}: 2 x bf16_tflops_sustained (nominal fp8/bf16 = int8/bf16 = "
+                                "4.5/2.25)"),
                 "algorithmic_flops_per_launch": gemm_flops,
                 "share_of_step": round(gemm_ms / phases["total"], 4)}
     # rowmax x2, cast x2, [bound GEMM], exps, digits x2, residue GEMM, [k_crt unless fused]
@@ -240,8 +248,9 @@ def run_oz2(args, rank, world, local_rank):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (paper generator (rand-0.5)*exp(randn*phi), seeded, on device)",
         "config": {"workload": (f"{'config3' if args.size == 16384 else 'custom'}: m=n=k={args.size} per GPU, "
-                               f"phi={args.phi}, N={N} hybrid moduli, {args.mode} mode"),
-                   "mode": args.mode,
+                               f"phi={args.phi}, N={N} {'hybrid' if args.scheme == 'fp8' else 'INT8'} moduli, "
+                               f"{args.scheme} scheme, {args.mode} mode"),
+                   "mode": args.mode, "scheme": args.scheme,
                    "m_per_gpu": m, "n": n, "k": k, "num_moduli": N, "phi": args.phi,
                    "l2": (f"no flush: A, B, C are {8 * m * k / 2**30:.2f}, {8 * k * n / 2**30:.2f}, "
                           f"{8 * m * n / 2**30:.2f} GiB (L2 is 126 MB)"),
@@ -325,6 +334,25 @@ def run_oz2(args, rank, world, local_rank):
         osweep[str(NN)] = {"tflops": round(flops_rank / (msN * 1e-3) / 1e12, 3), **errs(C[I][:, J].cpu().numpy())}
     P.oz2_set_mode(args.mode)
     acc[f"{other}_mode_sweep"] = osweep
+    # the other scheme (INT8 Ozaki-II baseline of P:151-202, or FP8), accurate mode
+    oscheme = "int8" if args.scheme == "fp8" else "fp8"
+    P.oz2_set_scheme(oscheme)
+    ssweep = {}
+    for NN in ([14, 15, 16] if oscheme == "int8" else [12, 13]):
+        if P.oz2_workspace_size("N", "N", m, n, k, NN) > ws.numel():
+            continue
+        f = lambda: P.oz2_dgemm("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0, C.data_ptr(), m, NN)
+        f()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(3):
+            f()
+        e1.record()
+        torch.cuda.synchronize()
+        msN = e0.elapsed_time(e1) / 3
+        ssweep[str(NN)] = {"tflops": round(flops_rank / (msN * 1e-3) / 1e12, 3), **errs(C[I][:, J].cpu().numpy())}
+    P.oz2_set_scheme(args.scheme)
+    acc[f"{oscheme}_scheme_sweep"] = ssweep
     extras["accuracy"] = acc
 
     # ---- e2e: host (pinned) buffers through the same C ABI
@@ -354,7 +382,7 @@ def cpu_baseline(args, sample_rows=16, seed_off=0):
     i.e. the paper's blocked call)."""
     import numpy as np
     from threadpoolctl import threadpool_limits
-    from oracle import scheme
+    from oracle import int8, scheme
     from synth import gen_host
     s = sample_rows
     k = args.size
@@ -362,7 +390,10 @@ def cpu_baseline(args, sample_rows=16, seed_off=0):
     B = gen_host(k, s, "phi", phi=args.phi, seed=60 + seed_off)
     with threadpool_limits(limits=1):
         t0 = time.perf_counter()
-        scheme.dgemm(A, B, args.moduli)
+        if args.scheme == "int8":
+            int8.dgemm(A, B, args.moduli, mode=args.mode)
+        else:
+            scheme.dgemm(A, B, args.moduli, mode=args.mode)
         dt = time.perf_counter() - t0
     return {"value": 2.0 * s * s * k / dt / 1e12, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"{s} x {k} x {s} sub-block, N={args.moduli} (full oracle pipeline, exact ints/Fractions)",

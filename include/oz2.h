@@ -30,6 +30,10 @@ extern "C" {
 #define OZ2_ERR_NOT_SUPPORTED  4   /* k > 2^22, mixed host/device pointers, no sm_100 */
 #define OZ2_ERR_NONFINITE      5   /* oz2_get_status(): A or B held NaN/Inf           */
 
+/* ---- schemes (see oz2_set_scheme) ---------------------------------------------- */
+#define OZ2_SCHEME_FP8         0   /* the paper's FP8 Ozaki-II, hybrid moduli (default) */
+#define OZ2_SCHEME_INT8        1   /* INT8 Ozaki-II, moduli <= 256 (R16)     */
+
 /* ---- scaling modes (see oz2_set_mode) ------------------------------- */
 #define OZ2_MODE_ACCURATE      0   /* bound GEMM on FP8 tensor cores       */
 #define OZ2_MODE_FAST          1   /* Cauchy-Schwarz bound, no bound GEMM (R15)       */
@@ -135,6 +139,19 @@ int oz2_set_stream(void* stream);
 int oz2_set_mode(int mode);
 int oz2_get_mode(void);
 
+/* Scheme for subsequent calls (and host-only queries: oz2_moduli, oz2_plan_query,
+ * oz2_workspace_size*) of this host thread.  OZ2_SCHEME_FP8 (default): the paper's method.
+ * OZ2_SCHEME_INT8: the INT8 Ozaki-II baseline of the paper's Sec. II on the
+ * tcgen05 kind::i8 tensor path -- moduli {256, 255, 253, 251, 247, ...} (eq. p_list), one
+ * exact S8 x S8 -> S32 GEMM per modulus (N GEMMs, +1 bound GEMM in accurate mode, Table 2);
+ * A-bar = ceil(2^e'|a|) <= 128 (e' = 6 - floor(log2 max|a|)), exact U8 bound GEMM, and
+ * log2 mu_i = e'_i + max{t : 2^(2t) R_i <= RD64((P-1)/2)} (reading R16).  k <= 2^16 (else
+ * OZ2_ERR_NOT_SUPPORTED).  In oz2_options the abar/bbar outputs then hold the U8 bounds,
+ * rmax/smax the exact S32 maxima (as uint32 bits) and digits_a/b the S8 residue planes.
+ * Returns -1 for any other value. */
+int oz2_set_scheme(int scheme);
+int oz2_get_scheme(void);
+
 /* Bytes of device workspace a call with these arguments needs (0 on invalid args). */
 size_t oz2_workspace_size(char transa, char transb, int64_t m, int64_t n, int64_t k,
                           int num_moduli);
@@ -142,8 +159,28 @@ size_t oz2_workspace_size(char transa, char transb, int64_t m, int64_t n, int64_
 /* Caller-owned device workspace for subsequent calls from this host thread; the
  * library keeps the pointer (not ownership) until replaced.  ptr == NULL reverts to
  * a library-owned buffer that grows on demand.  Must stay valid until all work
- * enqueued with it has completed. */
+ * enqueued with it has completed.
+ *
+ * If `bytes` is below oz2_workspace_size(), calls run steps 4-6 on m/n blocks of C that
+ * fit (block choice: oz2_plan_blocking), unless oz2_dgemm_ex asks for the
+ * whole-problem digit planes or residues.  Steps 1-3 always see the whole problem, so
+ * the scaling exponents -- and C, bit for bit -- equal those of the unblocked call. */
 int oz2_set_workspace(void* ptr, size_t bytes);
+
+/* m/n blocking (workspace reduction).  oz2_set_blocking forces block sizes
+ * (multiples of 256; 0 = automatic) for subsequent calls of this host thread;
+ * oz2_get_blocking reports the (mb, nb) the last call used (mb = m, nb = n: unblocked).
+ * oz2_workspace_size_blocked gives the bytes for given block sizes (0 = full extent);
+ * oz2_plan_blocking picks blocks for a workspace of `bytes` (host only): the largest
+ * column block nb (halving from n) admitting a row block mb >= min(m, nb); returns
+ * OZ2_ERR_WORKSPACE if not even 256 x 256 blocks fit.  Blocking recomputes A's digits
+ * once per column block when mb < m. */
+int oz2_set_blocking(int64_t mb, int64_t nb);
+int oz2_get_blocking(int64_t* mb, int64_t* nb);
+size_t oz2_workspace_size_blocked(int64_t m, int64_t n, int64_t k, int num_moduli,
+                                  int64_t mb, int64_t nb);
+int oz2_plan_blocking(int64_t m, int64_t n, int64_t k, int num_moduli, size_t bytes,
+                      int64_t* mb, int64_t* nb);
 
 /* Synchronises the current stream, returns the device status word of the last call
  * on it (OZ2_SUCCESS or OZ2_ERR_NONFINITE) in *status and clears it. */
@@ -199,6 +236,11 @@ const char* oz2_version(void);
  */
 int oz2_fp8_gemm_raw(const uint8_t* a, const uint8_t* b, float* C32,
                      int64_t m, int64_t n, int64_t k);
+
+/* The same on the INT8 path (kind::i8): C32[i][j] = sum_h a[i][h] b[j][h], S8 inputs,
+ * S32 accumulation (exact while |sum| < 2^31). */
+int oz2_int8_gemm_raw(const int8_t* a, const int8_t* b, int32_t* C32,
+                      int64_t m, int64_t n, int64_t k);
 
 #ifdef __cplusplus
 }

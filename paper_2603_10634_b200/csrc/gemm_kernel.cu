@@ -111,6 +111,14 @@ __device__ __forceinline__ void mma_f8f6f4_cg2(uint32_t d_tmem, uint64_t a_desc,
         "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}"
         ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
 }
+__device__ __forceinline__ void mma_i8_cg2(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                           uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
+}
 // arrive on the barrier at the same smem offset in every CTA of `mask`
 __device__ __forceinline__ void mma_commit_cg2(uint64_t* bar, uint16_t mask) {
     asm volatile(
@@ -133,10 +141,14 @@ __device__ __forceinline__ void tmem_dealloc_cg(uint32_t taddr, uint32_t ncols) 
     else asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
 
-template <int MODE, int CG, int FL, int MC>
+template <int MODE_, int CG, int FL, int MC>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
             const __grid_constant__ GemmParams P) {
+    // INT8 variants run the same pipeline on kind::i8 (S32 accumulators)
+    constexpr bool I8 = MODE_ >= MODE_RESIDUE_I8;
+    constexpr int MODE = I8 ? MODE_ - 3 : MODE_;
+    constexpr int NP = I8 ? 1 : 3;                    // products per modulus
     using Cfg = GemmCfg<CG>;
     constexpr int NS = Cfg::NSTAGE;
     extern __shared__ uint8_t smem_raw[];
@@ -195,7 +207,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     // the epilogue reduces each segment mod p and accumulates the residue (NEXT-2)
     const int nseg = (MODE == MODE_RESIDUE) ? P.num_kseg : 1;
     const int kseg = (MODE == MODE_RESIDUE) ? P.kseg_blocks : nkb;
-    const int prods = (MODE == MODE_RESIDUE) ? 3 * P.num_moduli * nseg : 1;
+    const int prods = (MODE == MODE_RESIDUE) ? NP * P.num_moduli * nseg : 1;
     const int unit = blockIdx.x / CS;            // tile-processing unit (cluster)
     const int units = gridDim.x / CS;
 
@@ -219,7 +231,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     int b_row = tn * BN + static_cast<int>(rank) * Cfg::B_ROWS;
                     int kb0 = 0, kb1 = nkb;
                     if (MODE == MODE_RESIDUE) {
-                        const int l = pr / (3 * nseg), rem = pr - l * 3 * nseg;
+                        const int l = pr / (NP * nseg), rem = pr - l * NP * nseg;
                         const int x = rem / nseg, seg = rem - x * nseg;
                         a_row += P.mod[l].a_plane[x] * P.rows_per_plane_a;
                         b_row += P.mod[l].b_plane[x] * P.rows_per_plane_b;
@@ -279,7 +291,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
         if (leader && elect_one()) {
-            constexpr uint32_t idesc = make_idesc_e4m3_f32(Cfg::TILE_M, BN);
+            constexpr uint32_t idesc = I8 ? make_idesc_i8_s32(Cfg::TILE_M, BN, MODE != MODE_BOUND)
+                                          : make_idesc_e4m3_f32(Cfg::TILE_M, BN);
             uint32_t stage = 0, phase = 0, g = 0;
             for (int tile = unit; tile < num_tiles; tile += units) {
                 for (int pr = 0; pr < prods; ++pr, ++g) {
@@ -298,8 +311,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         for (int kk = 0; kk < BK / 32; ++kk) {
                             // advance 32 bytes of K inside the 128-byte swizzle atom
                             const uint32_t acc = (kb > kb0 || kk > 0) ? 1u : 0u;
-                            if (CG == 1) mma_f8f6f4(d_tmem, a0 + 2 * kk, b0 + 2 * kk, idesc, acc);
-                            else mma_f8f6f4_cg2(d_tmem, a0 + 2 * kk, b0 + 2 * kk, idesc, acc);
+                            if (I8) {
+                                if (CG == 1) mma_i8(d_tmem, a0 + 2 * kk, b0 + 2 * kk, idesc, acc);
+                                else mma_i8_cg2(d_tmem, a0 + 2 * kk, b0 + 2 * kk, idesc, acc);
+                            } else {
+                                if (CG == 1) mma_f8f6f4(d_tmem, a0 + 2 * kk, b0 + 2 * kk, idesc, acc);
+                                else mma_f8f6f4_cg2(d_tmem, a0 + 2 * kk, b0 + 2 * kk, idesc, acc);
+                            }
                         }
                         if (CG == 1) mma_commit(&empty[stage]);
                         else mma_commit_cg2(&empty[stage], MC == 2 ? all_mask : pair_mask);
@@ -331,7 +349,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         // of an element were written by this same thread (program order).
         int64_t crt_row = -1, crt_col0 = 0;
         int crt_j = 128;
-        const int crt_per_prod = (MODE == MODE_RESIDUE) ? (128 + 3 * P.num_moduli - 1) / (3 * P.num_moduli) + 1 : 0;
+        const int crt_per_prod = (MODE == MODE_RESIDUE) ? (128 + NP * P.num_moduli - 1) / (NP * P.num_moduli) + 1 : 0;
         auto crt_steps = [&](int ncols) {
             if (FL == 0 || crt_j >= 128) return;
             if (crt_row >= P.m) { crt_j = 128; return; }
@@ -356,17 +374,17 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             const bool row_ok = row < P.m;
             if (MODE == MODE_RESIDUE) {
                 for (int l = 0; l < P.num_moduli; ++l) {
-                    const float p = P.mod[l].p, pinv = P.mod[l].pinv;
+                    const float p = P.mod[l].p, pinv = P.mod[l].pinv, w16 = P.mod[l].w16;
                     // running partial sum_x coef_x r_x, reduced mod p after every product
                     // (|.| <= p/2 + 1 <= 546), held exactly in binary16 pairs
                     __half2 part[64];
                     int16_t* out = P.residues + (static_cast<int64_t>(l) * P.n + col0) * P.m + row;
 #pragma unroll
-                    for (int x = 0; x < 3; ++x) {
+                    for (int x = 0; x < NP; ++x) {
                       const float coef = P.mod[l].coef[x];
                       for (int seg = 0; seg < nseg; ++seg, ++g) {
                         const bool first = (x == 0) && (seg == 0);
-                        const bool last = (x == 2) && (seg == nseg - 1);
+                        const bool last = (x == NP - 1) && (seg == nseg - 1);
                         const uint32_t slot = g & 1u, use = g >> 1;
                         mbar_wait(&tfull[slot], use & 1u);
                         tc_fence_after();
@@ -382,8 +400,20 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                                 float acc[2];
 #pragma unroll
                                 for (int u = 0; u < 2; ++u) {
-                                    const float f = __uint_as_float(v[j + u]);       // exact integer, |f| <= 2^24
-                                    const float r = fmaf(-rintf(f * pinv), p, f);    // f mod p, |r| <= p/2 + 1
+                                    float f;
+                                    if (I8) {
+                                        // S32 sum (|.| <= 2^30) == hi w16 + lo (mod p): both
+                                        // halves exact floats via the 2^23 exponent trick,
+                                        // |f| < 2^15 128 + 2^16 < 2^23 exact
+                                        const int iv = static_cast<int>(v[j + u]);
+                                        const float hi = __int_as_float(0x4B400000 + (iv >> 16)) - 12582912.0f;
+                                        const float lo = __int_as_float(0x4B000000 | (iv & 0xFFFF)) - 8388608.0f;
+                                        f = fmaf(hi, w16, lo);
+                                    } else {
+                                        f = __uint_as_float(v[j + u]);                // exact integer, |f| <= 2^24
+                                    }
+                                    // f mod p: |r| <= p/2 + 1 (FP8) or <= 3p/2 (INT8, reduced again below)
+                                    const float r = fmaf(-rintf(f * pinv), p, f);
                                     acc[u] = r;
                                 }
                                 const int idx = (c * 32 + j) >> 1;
@@ -428,7 +458,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 mbar_wait(&tfull[slot], use & 1u);
                 tc_fence_after();
                 const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + slot * BN + half * 128u;
-                float rowmax = 0.0f;
+                // non-negative FP32 and S32 values both order like their bit patterns
+                uint32_t rowmax = 0u;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     uint32_t v[32];
@@ -438,7 +469,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         uint32_t mycol = 0;
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
-                            rowmax = fmaxf(rowmax, __uint_as_float(v[j]));
+                            rowmax = max(rowmax, v[j]);
                             const uint32_t cm = __reduce_max_sync(0xffffffffu, v[j]);
                             if (lane == static_cast<uint32_t>(j)) mycol = cm;
                         }
@@ -454,8 +485,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 }
                 release_slot(slot);
                 ++g;
-                if (MODE == MODE_BOUND && row < P.m && rowmax > 0.0f)
-                    atomicMax(P.rmax + row, __float_as_uint(rowmax));
+                if (MODE == MODE_BOUND && row < P.m && rowmax > 0u)
+                    atomicMax(P.rmax + row, rowmax);
             }
         }
         crt_steps(128);                           // the last tile's CRT
@@ -532,6 +563,20 @@ static cudaError_t launch_cg(int mode, int fl, const CUtensorMap& ta, const CUte
                             const GemmParams& gp, int num_sms, cudaStream_t st) {
     if (mode == MODE_BOUND) return launch_one<MODE_BOUND, CG, 0, MC>(ta, tb, gp, num_sms, st);
     if (mode == MODE_RAW) return launch_one<MODE_RAW, CG, 0, MC>(ta, tb, gp, num_sms, st);
+    if (MC == 1) {   // INT8 scheme: CTA-pair (CG = 2) and single-CTA tiles
+        if (mode == MODE_BOUND_I8) return launch_one<MODE_BOUND_I8, CG, 0, MC>(ta, tb, gp, num_sms, st);
+        if (mode == MODE_RAW_I8) return launch_one<MODE_RAW_I8, CG, 0, MC>(ta, tb, gp, num_sms, st);
+        if (mode == MODE_RESIDUE_I8) {
+            switch (fl) {
+                case 4: return launch_one<MODE_RESIDUE_I8, CG, 4, MC>(ta, tb, gp, num_sms, st);
+                case 5: return launch_one<MODE_RESIDUE_I8, CG, 5, MC>(ta, tb, gp, num_sms, st);
+                case 6: return launch_one<MODE_RESIDUE_I8, CG, 6, MC>(ta, tb, gp, num_sms, st);
+                default: return launch_one<MODE_RESIDUE_I8, CG, 0, MC>(ta, tb, gp, num_sms, st);
+            }
+        }
+    } else if (mode >= MODE_RESIDUE_I8) {
+        return cudaErrorInvalidValue;
+    }
     switch (fl) {
         case 4: return launch_one<MODE_RESIDUE, CG, 4, MC>(ta, tb, gp, num_sms, st);
         case 5: return launch_one<MODE_RESIDUE, CG, 5, MC>(ta, tb, gp, num_sms, st);
@@ -545,7 +590,8 @@ static cudaError_t launch_cg(int mode, int fl, const CUtensorMap& ta, const CUte
 cudaError_t launch_gemm(int mode, int cg, int fused_limbs, const CUtensorMap& ta, const CUtensorMap& tb,
                         const GemmParams& gp, int num_sms, cudaStream_t st) {
     cudaError_t err;
-    if (cg == 4) err = launch_cg<2, 2>(mode, fused_limbs, ta, tb, gp, num_sms, st);
+    if (cg == 4 && mode < MODE_RESIDUE_I8) err = launch_cg<2, 2>(mode, fused_limbs, ta, tb, gp, num_sms, st);
+    else if (cg == 4) err = launch_cg<2, 1>(mode, fused_limbs, ta, tb, gp, num_sms, st);
     else if (cg == 2) err = launch_cg<2, 1>(mode, fused_limbs, ta, tb, gp, num_sms, st);
     else err = launch_cg<1, 1>(mode, fused_limbs, ta, tb, gp, num_sms, st);
     if (err != cudaSuccess) return err;

@@ -63,6 +63,17 @@ static int64_t inv_mod(int64_t a, int64_t p) {   // a^-1 mod p, gcd(a,p) = 1
 }
 static int gcd_i(int a, int b) { while (b) { const int t = a % b; a = b; b = t; } return a; }
 
+static std::vector<int> int8_moduli(int N) {
+    // greedy pairwise coprime from 256 down (eq. p_list)
+    std::vector<int> out;
+    for (int c = 256; c >= 2 && static_cast<int>(out.size()) < N; --c) {
+        bool ok = true;
+        for (int q : out) ok = ok && gcd_i(c, q) == 1;
+        if (ok) out.push_back(c);
+    }
+    return out;
+}
+
 static std::vector<int> hybrid_moduli(int N) {
     // squares s^2 > 513 (s <= 33) pairwise coprime, then greedy coprime from 513 down
     std::vector<int> out;
@@ -95,6 +106,7 @@ static float ru32(long double x) {
 
 struct Plan {
     int N = 0, nsq = 0, M = 0, L = 0;
+    int family = FAMILY_HYBRID_FP8;
     std::vector<int> p;
     float p_prime = 0, delta = 0;
     double log2P = 0;
@@ -108,12 +120,15 @@ struct Plan {
     std::vector<Big> w;
 };
 
-static Plan build_plan(int N) {
+static Plan build_plan(int N, int family) {
     Plan pl;
     pl.N = N;
-    pl.p = hybrid_moduli(N);
-    for (int p : pl.p) pl.nsq += is_square_i(p) ? 1 : 0;
-    pl.M = 2 * pl.nsq + 3 * (N - pl.nsq);
+    pl.family = family;
+    const bool i8 = family == FAMILY_INT8;
+    pl.p = i8 ? int8_moduli(N) : hybrid_moduli(N);
+    if (!i8)
+        for (int p : pl.p) pl.nsq += is_square_i(p) ? 1 : 0;
+    pl.M = i8 ? N : 2 * pl.nsq + 3 * (N - pl.nsq);
     Big P{1};
     for (int p : pl.p) big_mul_small(P, static_cast<uint32_t>(p));
     pl.P = P;
@@ -187,6 +202,13 @@ static Plan build_plan(int N) {
     std::memset(&dp, 0, sizeof(dp));
     dp.num_moduli = N;
     dp.num_planes = pl.M;
+    dp.int8 = i8 ? 1 : 0;
+    {
+        int pmin = pl.p[0];
+        for (int p : pl.p) pmin = p < pmin ? p : pmin;
+        dp.lim1 = std::ldexp(static_cast<double>(pmin), 50);
+        dp.lim2 = std::ldexp(static_cast<double>(pmin), 86);
+    }
     int plane = 0;
     for (int l = 0; l < N; ++l) {
         const int p = pl.p[l];
@@ -196,7 +218,17 @@ static Plan build_plan(int N) {
         md.p_f = static_cast<float>(p);
         md.pinv_f = 1.0f / static_cast<float>(p);
         md.hp_f = (p % 2 == 0) ? 0.5f / static_cast<float>(p) : 0.0f;
-        md.square = is_square_i(p) ? 1 : 0;
+        md.h_f = (p % 2 == 0) ? 0.5f : 0.0f;
+        {   // smod(2^(8i), p) in [-floor(p/2), ceil(p/2) - 1]
+            int64_t v = 1;
+            for (int i = 0; i < 8; ++i) {
+                int64_t sv = v % p;
+                if (sv >= (p + 1) / 2) sv -= p;
+                md.w8[i] = static_cast<float>(sv);
+                v = (v * 256) % p;
+            }
+        }
+        md.square = i8 ? 2 : (is_square_i(p) ? 1 : 0);
         const int s = md.square ? static_cast<int>(std::lround(std::sqrt(static_cast<double>(p)))) : 16;
         md.s_f = static_cast<float>(s);
         md.inv_s_f = 1.0f / static_cast<float>(s);
@@ -204,7 +236,16 @@ static Plan build_plan(int N) {
         ModEpi& me = pl.gemm_mod.mod[l];
         me.p = static_cast<float>(p);
         me.pinv = 1.0f / static_cast<float>(p);
-        if (md.square) {
+        {
+            int64_t w = 65536 % p;
+            if (w >= (p + 1) / 2) w -= p;
+            me.w16 = static_cast<float>(w);
+        }
+        if (i8) {
+            // one exact INT8 GEMM per modulus: C'_l = mod(A'_l B'_l, p_l) (eq. CRTmatmul)
+            me.coef[0] = 1.0f; me.a_plane[0] = plane; me.b_plane[0] = plane;
+            plane += 1;
+        } else if (md.square) {
             // C'_l = mod(s A1 B2 + s A2 B1 + A2 B2, p)  (eq. 3matmult-notKaratsuba)
             me.coef[0] = static_cast<float>(s); me.a_plane[0] = plane + 0; me.b_plane[0] = plane + 1;
             me.coef[1] = static_cast<float>(s); me.a_plane[1] = plane + 1; me.b_plane[1] = plane + 0;
@@ -248,6 +289,9 @@ struct ThreadState {
     int device = -1;
     int num_sms = 0;
     int mode = OZ2_MODE_ACCURATE;
+    int scheme = OZ2_SCHEME_FP8;          // FAMILY_HYBRID_FP8 / FAMILY_INT8
+    int64_t block_m = 0, block_n = 0;     // forced m/n blocking (0: automatic)
+    int64_t last_mb = 0, last_nb = 0;     // blocking used by the last call
     std::map<int, std::unique_ptr<Plan>> plans;
     bool timing = false;
     bool timed_last = false;
@@ -259,10 +303,14 @@ static thread_local ThreadState g_ts;
 static std::mutex g_plan_mutex;
 static std::map<int, std::unique_ptr<Plan>> g_host_plans;   // host-only queries
 
-static const Plan& host_plan(int N) {
+static int plan_key(int N, int family) { return N + 64 * family; }
+
+static const Plan& host_plan(int N) {   // for the calling thread's scheme
+    const int fam = g_ts.scheme;
     std::lock_guard<std::mutex> lk(g_plan_mutex);
-    auto it = g_host_plans.find(N);
-    if (it == g_host_plans.end()) it = g_host_plans.emplace(N, std::make_unique<Plan>(build_plan(N))).first;
+    auto it = g_host_plans.find(plan_key(N, fam));
+    if (it == g_host_plans.end())
+        it = g_host_plans.emplace(plan_key(N, fam), std::make_unique<Plan>(build_plan(N, fam))).first;
     return *it->second;
 }
 
@@ -286,9 +334,10 @@ static int ensure_device() {
 }
 
 static Plan* device_plan(int N, int* err) {
-    auto it = g_ts.plans.find(N);
+    const int key = plan_key(N, g_ts.scheme);
+    auto it = g_ts.plans.find(key);
     if (it != g_ts.plans.end()) return it->second.get();
-    auto pl = std::make_unique<Plan>(build_plan(N));
+    auto pl = std::make_unique<Plan>(build_plan(N, g_ts.scheme));
     const size_t bytes = pl->pow2tab.size() * sizeof(uint16_t);
     if (cudaMalloc(&pl->d_pow2tab, bytes) != cudaSuccess) { *err = OZ2_ERR_ALLOC; return nullptr; }
     if (cudaMemcpy(pl->d_pow2tab, pl->pow2tab.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
@@ -297,7 +346,7 @@ static Plan* device_plan(int N, int* err) {
     }
     pl->dig.pow2tab = pl->d_pow2tab;
     Plan* raw = pl.get();
-    g_ts.plans.emplace(N, std::move(pl));
+    g_ts.plans.emplace(key, std::move(pl));
     return raw;
 }
 
@@ -307,17 +356,29 @@ static Plan* device_plan(int N, int* err) {
 static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 static inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
+// Workspace of one call.  Steps 4-6 may run on (mb x nb) blocks of C (m/n blocking,
+// P:629-642): the digit planes then hold one row block of A and one column block of B,
+// the residues one block of C, and A-bar / B-bar get their own full-size buffers (steps 1-3
+// always run on the whole problem, so the exponents -- and hence C -- are identical to the
+// unblocked call).  mb = m and nb = n is the unblocked layout, where A-bar / B-bar live in
+// the first digit plane.
 struct Layout {
-    int64_t m_pad, n_pad, k_pad;
+    int64_t m_pad, n_pad, k_pad, mb, nb, mb_pad, nb_pad;
     int M;
-    size_t maxbits, eprime, rsmax, sumsq, eexp, digA, digB, res, total;
+    bool blocked;
+    size_t maxbits, eprime, rsmax, sumsq, eexp, abar, bbar, digA, digB, res, total;
 };
 
-static Layout make_layout(int64_t m, int64_t n, int64_t k, int N, int M) {
+static Layout make_layout(int64_t m, int64_t n, int64_t k, int N, int M, int64_t mb = 0, int64_t nb = 0) {
     Layout L{};
     L.m_pad = round_up(m, PAD_M);
     L.n_pad = round_up(n, PAD_N);
     L.k_pad = round_up(k, PAD_K);
+    L.mb = (mb <= 0 || mb >= m) ? m : mb;
+    L.nb = (nb <= 0 || nb >= n) ? n : nb;
+    L.mb_pad = round_up(L.mb, PAD_M);
+    L.nb_pad = round_up(L.nb, PAD_N);
+    L.blocked = L.mb < m || L.nb < n;
     L.M = M;
     size_t off = 0;
     const size_t mn = static_cast<size_t>(m + n);
@@ -325,12 +386,42 @@ static Layout make_layout(int64_t m, int64_t n, int64_t k, int N, int M) {
     L.eprime = off;  off = align_up(off + 4 * mn, 256);
     L.rsmax = off;   off = align_up(off + 4 * mn, 256);
     L.sumsq = off;   off = align_up(off + 8 * mn, 256);
-    L.eexp = off;    off = align_up(off + 4 * mn, 256);
-    L.digA = off;    off = align_up(off + static_cast<size_t>(M) * L.m_pad * L.k_pad, 1024);
-    L.digB = off;    off = align_up(off + static_cast<size_t>(M) * L.n_pad * L.k_pad, 1024);
-    L.res = off;     off = align_up(off + 2ull * N * static_cast<size_t>(m) * static_cast<size_t>(n), 256);
+    L.eexp = off;    off = align_up(off + 4 * mn, 1024);
+    if (L.blocked) {
+        L.abar = off; off = align_up(off + static_cast<size_t>(L.m_pad) * L.k_pad, 1024);
+        L.bbar = off; off = align_up(off + static_cast<size_t>(L.n_pad) * L.k_pad, 1024);
+    }
+    L.digA = off;    off = align_up(off + static_cast<size_t>(M) * L.mb_pad * L.k_pad, 1024);
+    L.digB = off;    off = align_up(off + static_cast<size_t>(M) * L.nb_pad * L.k_pad, 1024);
+    L.res = off;     off = align_up(off + 2ull * N * static_cast<size_t>(L.mb) * static_cast<size_t>(L.nb), 256);
     L.total = off;
+    if (!L.blocked) { L.abar = L.digA; L.bbar = L.digB; }
     return L;
+}
+
+// Block sizes for a workspace of `bytes` (multiples of 256, or the full extent): the
+// largest column block nb (from n down, halving) for which a row block mb >= min(m, nb)
+// fits; B's digits are then split least and A's are recomputed ceil(n/nb) times.
+// Returns false if not even 256 x 256 blocks fit.
+static bool choose_blocking(int64_t m, int64_t n, int64_t k, int N, int M, size_t bytes,
+                            int64_t* mb_out, int64_t* nb_out) {
+    if (make_layout(m, n, k, N, M).total <= bytes) { *mb_out = m; *nb_out = n; return true; }
+    for (int64_t nb = round_up(n, PAD_N);; nb = round_up(nb / 2, PAD_N)) {
+        const int64_t nbe = nb >= n ? n : nb;
+        // largest mb (multiple of 256) that fits with this nb
+        int64_t lo = 0, hi = round_up(m, PAD_M) / PAD_M;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) / 2;
+            const int64_t mbe = mid * PAD_M >= m ? m : mid * PAD_M;
+            if (make_layout(m, n, k, N, M, mbe, nbe).total <= bytes) lo = mid; else hi = mid - 1;
+        }
+        const int64_t mb = lo * PAD_M >= m ? m : lo * PAD_M;
+        if (lo > 0 && (mb >= m || mb >= nbe)) { *mb_out = mb; *nb_out = nbe; return true; }
+        if (nb <= PAD_N) {
+            if (lo > 0) { *mb_out = mb; *nb_out = nbe; return true; }
+            return false;
+        }
+    }
 }
 
 // =================================================================================
@@ -415,12 +506,21 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
     int err = OZ2_SUCCESS;
     Plan* pl = device_plan(N, &err);
     if (!pl) return err;
-    const Layout L = make_layout(m, n, k, N, pl->M);
+    // debug outputs of whole-problem digit planes / residues need the unblocked layout
+    const bool want_full = opt && (opt->digits_a || opt->digits_b || opt->residues);
+    int64_t mb = g_ts.block_m, nb = g_ts.block_n;
+    if (want_full) mb = nb = 0;
     uint8_t* ws = nullptr;
+    Layout L;
     if (g_ts.user_ws) {
+        if (mb <= 0 && nb <= 0 && !want_full) {
+            if (!choose_blocking(m, n, k, N, pl->M, g_ts.user_ws_bytes, &mb, &nb)) return OZ2_ERR_WORKSPACE;
+        }
+        L = make_layout(m, n, k, N, pl->M, mb, nb);
         if (g_ts.user_ws_bytes < L.total) return OZ2_ERR_WORKSPACE;
         ws = static_cast<uint8_t*>(g_ts.user_ws);
     } else {
+        L = make_layout(m, n, k, N, pl->M, mb, nb);
         if (g_ts.own_ws_bytes < L.total) {
             if (g_ts.own_ws) { cudaStreamSynchronize(st); cudaFree(g_ts.own_ws); g_ts.own_ws = nullptr; g_ts.own_ws_bytes = 0; }
             if (cudaMalloc(&g_ts.own_ws, L.total) != cudaSuccess) return OZ2_ERR_ALLOC;
@@ -428,17 +528,20 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
         }
         ws = static_cast<uint8_t*>(g_ts.own_ws);
     }
+    g_ts.last_mb = L.mb;
+    g_ts.last_nb = L.nb;
     auto* maxbits = reinterpret_cast<unsigned long long*>(ws + L.maxbits);
     auto* eprime = reinterpret_cast<int32_t*>(ws + L.eprime);
     auto* rsmax = reinterpret_cast<uint32_t*>(ws + L.rsmax);
     auto* sumsq = reinterpret_cast<unsigned long long*>(ws + L.sumsq);
     const bool fast = g_ts.mode == OZ2_MODE_FAST;
+    const bool i8 = pl->family == FAMILY_INT8;
     auto* eexp = reinterpret_cast<int32_t*>(ws + L.eexp);
     uint8_t* digA = ws + L.digA;
     uint8_t* digB = ws + L.digB;
     auto* res = reinterpret_cast<int16_t*>(ws + L.res);
-    uint8_t* abar = digA;      // A-bar / B-bar live in the first digit plane until step 4
-    uint8_t* bbar = digB;
+    uint8_t* abar = ws + L.abar;     // unblocked: the first digit plane, dead after step 3
+    uint8_t* bbar = ws + L.bbar;
     int32_t* e_mu = eexp;
     int32_t* e_nu = eexp + m;
 
@@ -454,9 +557,9 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
         OZ2_CK(launch_rowmax(B, n, k, ldb, b_kmajor, maxbits + m, st));
         if (fast) OZ2_CK(cudaMemsetAsync(sumsq, 0, 8 * static_cast<size_t>(m + n), st));
         OZ2_CK(launch_cast(A, m, k, lda, a_kmajor, maxbits, eprime, abar, L.m_pad, L.k_pad, g_ts.d_status,
-                           fast ? sumsq : nullptr, st));
+                           fast ? sumsq : nullptr, i8, st));
         OZ2_CK(launch_cast(B, n, k, ldb, b_kmajor, maxbits + m, eprime + m, bbar, L.n_pad, L.k_pad, g_ts.d_status,
-                           fast ? sumsq + m : nullptr, st));
+                           fast ? sumsq + m : nullptr, i8, st));
         if (opt && opt->e_prime_a) OZ2_CK(cudaMemcpyAsync(opt->e_prime_a, eprime, 4 * m, cudaMemcpyDeviceToDevice, st));
         if (opt && opt->e_prime_b) OZ2_CK(cudaMemcpyAsync(opt->e_prime_b, eprime + m, 4 * n, cudaMemcpyDeviceToDevice, st));
         if (opt && opt->abar && k && !fast)
@@ -477,15 +580,18 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             gp.m_tiles = static_cast<int>(L.m_pad / tile_m(cg)); gp.n_tiles = static_cast<int>(L.n_pad / BN);
             gp.rows_per_plane_a = static_cast<int>(L.m_pad); gp.rows_per_plane_b = static_cast<int>(L.n_pad);
             gp.rmax = rsmax; gp.smax = rsmax + m;
-            OZ2_CK(launch_gemm(MODE_BOUND, cg, 0, ta, tb, gp, g_ts.num_sms, st));
+            OZ2_CK(launch_gemm(i8 ? MODE_BOUND_I8 : MODE_BOUND, cg, 0, ta, tb, gp, g_ts.num_sms, st));
         }
         if (opt && opt->rmax && !fast) OZ2_CK(cudaMemcpyAsync(opt->rmax, rsmax, 4 * m, cudaMemcpyDeviceToDevice, st));
         if (opt && opt->smax && !fast) OZ2_CK(cudaMemcpyAsync(opt->smax, rsmax + m, 4 * n, cudaMemcpyDeviceToDevice, st));
         // ---- step 3: scaling exponents (eq. mu-computation / nu-computation)
         phase_mark(2);
         if (fast) {
-            // fast mode: Cauchy-Schwarz over the FP8 upper bounds, no bound GEMM (R15)
-            OZ2_CK(launch_exps_fast(maxbits, eprime, sumsq, m + n, pl->fast, eexp, st));
+            // fast mode: Cauchy-Schwarz over the FP8 / INT8 upper bounds, no bound GEMM (R15, R16)
+            OZ2_CK(launch_exps_fast(maxbits, eprime, sumsq, nullptr, m + n, pl->fast, i8 ? 0 : 18, eexp, st));
+        } else if (i8) {
+            // INT8 accurate mode: exact bound-GEMM row / column maxima (R16)
+            OZ2_CK(launch_exps_fast(maxbits, eprime, nullptr, rsmax, m + n, pl->fast, 0, eexp, st));
         } else {
             ExpParams ep{pl->p_prime, pl->delta, f_k_of(k)};
             OZ2_CK(launch_exps(maxbits, eprime, rsmax, m + n, ep, eexp, st));
@@ -499,64 +605,79 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
     if (opt && opt->e_mu) OZ2_CK(cudaMemcpyAsync(opt->e_mu, e_mu, 4 * m, cudaMemcpyDeviceToDevice, st));
     if (opt && opt->e_nu) OZ2_CK(cudaMemcpyAsync(opt->e_nu, e_nu, 4 * n, cudaMemcpyDeviceToDevice, st));
 
-    // ---- step 4: integers, residues, FP8 digits
-    phase_mark(3);
-    OZ2_CK(launch_digits(A, m, k, lda, a_kmajor, e_mu, pl->dig, digA, L.m_pad, L.k_pad, st));
-    OZ2_CK(launch_digits(B, n, k, ldb, b_kmajor, e_nu, pl->dig, digB, L.n_pad, L.k_pad, st));
-    if (opt && opt->digits_a && k)
-        for (int x = 0; x < pl->M; ++x)
-            OZ2_CK(cudaMemcpy2DAsync(opt->digits_a + static_cast<size_t>(x) * m * k, k,
-                                     digA + static_cast<size_t>(x) * L.m_pad * L.k_pad, L.k_pad, k, m,
-                                     cudaMemcpyDeviceToDevice, st));
-    if (opt && opt->digits_b && k)
-        for (int x = 0; x < pl->M; ++x)
-            OZ2_CK(cudaMemcpy2DAsync(opt->digits_b + static_cast<size_t>(x) * n * k, k,
-                                     digB + static_cast<size_t>(x) * L.n_pad * L.k_pad, L.k_pad, k, n,
-                                     cudaMemcpyDeviceToDevice, st));
-    // ---- step 5: 3N exact FP8 GEMMs with the modular epilogue
-    phase_mark(4);
-    int fused = 0;
-    {
-        const int cg = cta_group(L.n_pad);
-        CUtensorMap ta, tb;
-        if (!make_map(&ta, digA, L.k_pad, static_cast<uint64_t>(pl->M) * L.m_pad, L.k_pad, BK, a_box_rows(cg))) return OZ2_ERR_CUDA;
-        if (!make_map(&tb, digB, L.k_pad, static_cast<uint64_t>(pl->M) * L.n_pad, L.k_pad, BK, b_box_rows(cg))) return OZ2_ERR_CUDA;
-        GemmParams gp = pl->gemm_mod;
-        gp.m = static_cast<int>(m); gp.n = static_cast<int>(n);
-        gp.num_k_blocks = static_cast<int>(L.k_pad / BK);
-        gp.kseg_blocks = kMaxK / BK;                                  // 2^16 per segment
-        gp.num_kseg = (gp.num_k_blocks + gp.kseg_blocks - 1) / gp.kseg_blocks;
-        gp.m_tiles = static_cast<int>(L.m_pad / tile_m(cg)); gp.n_tiles = static_cast<int>(L.n_pad / BN);
-        gp.rows_per_plane_a = static_cast<int>(L.m_pad); gp.rows_per_plane_b = static_cast<int>(L.n_pad);
-        gp.num_moduli = N;
-        gp.residues = res;
-        gp.sync_lead = sync_lead();
-        {   // chunks must tile the 512-block K segments: a power of two in [1, 512]
-            int kc = env_int("OZ2_SYNC_CHUNK", 8);
-            int pw = 1;
-            while (pw * 2 <= kc && pw * 2 <= 512) pw *= 2;
-            gp.sync_chunk = pw;
-        }
-        if (gp.sync_lead > 0) {
-            gp.progress = reinterpret_cast<unsigned long long*>(maxbits);   // dead after step 3
-            OZ2_CK(cudaMemsetAsync(gp.progress, 0, 8, st));
-        }
-        // fuse the CRT into the epilogue for up to 6 limbs (N <= 20) unless OZ2_FUSED_CRT=0
-        // (k >= 8192: a product then lasts long enough to hide one CRT step per product)
-        fused = (pl->L <= 6 && k >= 8192 && env_int("OZ2_FUSED_CRT", 1) != 0) ? pl->L : 0;
-        if (fused) {
-            gp.crt = pl->crt;
-            gp.e_mu = e_mu; gp.e_nu = e_nu;
-            gp.alpha = alpha; gp.beta = beta;
-            gp.C = C; gp.ldc = ldc;
-        }
-        OZ2_CK(launch_gemm(MODE_RESIDUE, cg, fused, ta, tb, gp, g_ts.num_sms, st));
+    // fuse the CRT into the epilogue for up to 6 limbs (N <= 20) unless OZ2_FUSED_CRT=0
+    // (k >= 8192: a product then lasts long enough to hide one CRT step per product)
+    const int fused = (pl->L <= 6 && k >= 8192 && env_int("OZ2_FUSED_CRT", 1) != 0) ? pl->L : 0;
+    int sync_chunk = 1;
+    {   // chunks must tile the 512-block K segments: a power of two in [1, 512]
+        const int kc = env_int("OZ2_SYNC_CHUNK", 8);
+        while (sync_chunk * 2 <= kc && sync_chunk * 2 <= 512) sync_chunk *= 2;
     }
-    if (opt && opt->residues)
-        OZ2_CK(cudaMemcpyAsync(opt->residues, res, 2ull * N * m * n, cudaMemcpyDeviceToDevice, st));
-    // ---- step 6: CRT + inverse scaling (eqs. CRT_finalreduction, inversescaling)
-    phase_mark(5);
-    if (!fused) OZ2_CK(launch_crt(pl->L, res, m, n, pl->crt, e_mu, e_nu, alpha, beta, C, ldc, st));
+    // ---- steps 4-6 on blocks of C (one block when unblocked)
+    phase_mark(3);
+    if (L.blocked) phase_mark(4);     // blocked: the whole block loop counts as "residue GEMM"
+    for (int64_t j0 = 0; j0 < n; j0 += L.nb) {
+        const int64_t nbj = std::min(L.nb, n - j0), nbj_pad = round_up(nbj, PAD_N);
+        const double* Bj = b_kmajor ? B + j0 * ldb : B + j0;
+        // ---- step 4: integers, residues, FP8 digits
+        OZ2_CK(launch_digits(Bj, nbj, k, ldb, b_kmajor, e_nu + j0, pl->dig, digB, nbj_pad, L.k_pad, st));
+        for (int64_t i0 = 0; i0 < m; i0 += L.mb) {
+            const int64_t mbi = std::min(L.mb, m - i0), mbi_pad = round_up(mbi, PAD_M);
+            const double* Ai = a_kmajor ? A + i0 * lda : A + i0;
+            if (j0 == 0 || L.mb < m)      // one row block: A's digits survive across column blocks
+                OZ2_CK(launch_digits(Ai, mbi, k, lda, a_kmajor, e_mu + i0, pl->dig, digA, mbi_pad, L.k_pad, st));
+            if (!L.blocked) {
+                if (opt && opt->digits_a && k)
+                    for (int x = 0; x < pl->M; ++x)
+                        OZ2_CK(cudaMemcpy2DAsync(opt->digits_a + static_cast<size_t>(x) * m * k, k,
+                                                 digA + static_cast<size_t>(x) * L.m_pad * L.k_pad, L.k_pad, k, m,
+                                                 cudaMemcpyDeviceToDevice, st));
+                if (opt && opt->digits_b && k)
+                    for (int x = 0; x < pl->M; ++x)
+                        OZ2_CK(cudaMemcpy2DAsync(opt->digits_b + static_cast<size_t>(x) * n * k, k,
+                                                 digB + static_cast<size_t>(x) * L.n_pad * L.k_pad, L.k_pad, k, n,
+                                                 cudaMemcpyDeviceToDevice, st));
+                phase_mark(4);
+            }
+            // ---- step 5: 3N exact FP8 GEMMs with the modular epilogue
+            const int cg = cta_group(nbj_pad);
+            CUtensorMap ta, tb;
+            if (!make_map(&ta, digA, L.k_pad, static_cast<uint64_t>(pl->M) * mbi_pad, L.k_pad, BK, a_box_rows(cg))) return OZ2_ERR_CUDA;
+            if (!make_map(&tb, digB, L.k_pad, static_cast<uint64_t>(pl->M) * nbj_pad, L.k_pad, BK, b_box_rows(cg))) return OZ2_ERR_CUDA;
+            GemmParams gp = pl->gemm_mod;
+            gp.m = static_cast<int>(mbi); gp.n = static_cast<int>(nbj);
+            gp.num_k_blocks = static_cast<int>(L.k_pad / BK);
+            gp.kseg_blocks = kMaxK / BK;                                  // 2^16 per segment
+            gp.num_kseg = (gp.num_k_blocks + gp.kseg_blocks - 1) / gp.kseg_blocks;
+            gp.m_tiles = static_cast<int>(mbi_pad / tile_m(cg)); gp.n_tiles = static_cast<int>(nbj_pad / BN);
+            gp.rows_per_plane_a = static_cast<int>(mbi_pad); gp.rows_per_plane_b = static_cast<int>(nbj_pad);
+            gp.num_moduli = N;
+            gp.residues = res;
+            gp.sync_lead = sync_lead();
+            gp.sync_chunk = sync_chunk;
+            if (gp.sync_lead > 0) {
+                gp.progress = reinterpret_cast<unsigned long long*>(maxbits);   // dead after step 3
+                OZ2_CK(cudaMemsetAsync(gp.progress, 0, 8, st));
+            }
+            double* Cij = C + i0 + j0 * ldc;
+            if (fused) {
+                gp.crt = pl->crt;
+                gp.e_mu = e_mu + i0; gp.e_nu = e_nu + j0;
+                gp.alpha = alpha; gp.beta = beta;
+                gp.C = Cij; gp.ldc = ldc;
+            }
+            OZ2_CK(launch_gemm(i8 ? MODE_RESIDUE_I8 : MODE_RESIDUE, cg, fused, ta, tb, gp, g_ts.num_sms, st));
+            if (!L.blocked) {
+                if (opt && opt->residues)
+                    OZ2_CK(cudaMemcpyAsync(opt->residues, res, 2ull * N * m * n, cudaMemcpyDeviceToDevice, st));
+                phase_mark(5);
+            }
+            // ---- step 6: CRT + inverse scaling (eqs. CRT_finalreduction, inversescaling)
+            if (!fused)
+                OZ2_CK(launch_crt(pl->L, res, mbi, nbj, pl->crt, e_mu + i0, e_nu + j0, alpha, beta, Cij, ldc, st));
+        }
+    }
+    if (L.blocked) phase_mark(5);
     phase_mark(6);
     g_ts.timed_last = g_ts.timing;
     return OZ2_SUCCESS;
@@ -593,6 +714,7 @@ int dgemm_impl(char transa, char transb, int64_t m, int64_t n, int64_t k, double
     int e = ensure_device();
     if (e) return e;
     if (k > kMaxKTotal) return OZ2_ERR_NOT_SUPPORTED;      // f_k = 1/(1 - k 2^-23) needs k << 2^23
+    if (g_ts.scheme == OZ2_SCHEME_INT8 && k > kMaxK) return OZ2_ERR_NOT_SUPPORTED;   // exact S32 bound (R16)
     if (m > (1ll << 30) || n > (1ll << 30)) return OZ2_ERR_NOT_SUPPORTED;
     cudaStream_t st = g_ts.stream;
     const bool quick = (alpha == 0.0 || k == 0);
@@ -670,6 +792,51 @@ int oz2_set_mode(int mode) {
 }
 
 int oz2_get_mode(void) { return g_ts.mode; }
+
+int oz2_set_scheme(int scheme) {
+    if (scheme != OZ2_SCHEME_FP8 && scheme != OZ2_SCHEME_INT8) return -1;
+    g_ts.scheme = scheme;
+    return OZ2_SUCCESS;
+}
+
+int oz2_get_scheme(void) { return g_ts.scheme; }
+
+int oz2_set_blocking(int64_t mb, int64_t nb) {
+    if (mb < 0) return -1;
+    if (nb < 0) return -2;
+    if ((mb % PAD_M) != 0) return -1;
+    if ((nb % PAD_N) != 0) return -2;
+    g_ts.block_m = mb;
+    g_ts.block_n = nb;
+    return OZ2_SUCCESS;
+}
+
+int oz2_get_blocking(int64_t* mb, int64_t* nb) {
+    if (!mb) return -1;
+    if (!nb) return -2;
+    *mb = g_ts.last_mb;
+    *nb = g_ts.last_nb;
+    return OZ2_SUCCESS;
+}
+
+size_t oz2_workspace_size_blocked(int64_t m, int64_t n, int64_t k, int num_moduli, int64_t mb, int64_t nb) {
+    if (m < 0 || n < 0 || k < 0 || mb < 0 || nb < 0) return 0;
+    if (num_moduli < 2 || num_moduli > kMaxModuli) return 0;
+    const Plan& pl = host_plan(num_moduli);
+    return make_layout(m, n, k, num_moduli, pl.M, mb, nb).total;
+}
+
+int oz2_plan_blocking(int64_t m, int64_t n, int64_t k, int num_moduli, size_t bytes, int64_t* mb,
+                      int64_t* nb) {
+    if (m < 0) return -1;
+    if (n < 0) return -2;
+    if (k < 0) return -3;
+    if (num_moduli < 2 || num_moduli > kMaxModuli) return -4;
+    if (!mb) return -6;
+    if (!nb) return -7;
+    const Plan& pl = host_plan(num_moduli);
+    return choose_blocking(m, n, k, num_moduli, pl.M, bytes, mb, nb) ? OZ2_SUCCESS : OZ2_ERR_WORKSPACE;
+}
 
 int oz2_set_workspace(void* ptr, size_t bytes) {
     g_ts.user_ws = ptr;
@@ -751,7 +918,18 @@ int oz2_plan_query(int num_moduli, int64_t k, oz2_plan_info* out) {
 
 const char* oz2_version(void) { return "oz2 0.1.0 sm_100a"; }
 
+static int gemm_raw(int mode, const uint8_t* a, const uint8_t* b, float* C32, int64_t m, int64_t n, int64_t k);
+
 int oz2_fp8_gemm_raw(const uint8_t* a, const uint8_t* b, float* C32, int64_t m, int64_t n, int64_t k) {
+    return gemm_raw(MODE_RAW, a, b, C32, m, n, k);
+}
+
+int oz2_int8_gemm_raw(const int8_t* a, const int8_t* b, int32_t* C32, int64_t m, int64_t n, int64_t k) {
+    return gemm_raw(MODE_RAW_I8, reinterpret_cast<const uint8_t*>(a), reinterpret_cast<const uint8_t*>(b),
+                    reinterpret_cast<float*>(C32), m, n, k);
+}
+
+static int gemm_raw(int mode, const uint8_t* a, const uint8_t* b, float* C32, int64_t m, int64_t n, int64_t k) {
     if (m < 0) return -4;
     if (n < 0) return -5;
     if (k < 0 || (k % 16) != 0) return -6;
@@ -770,7 +948,7 @@ int oz2_fp8_gemm_raw(const uint8_t* a, const uint8_t* b, float* C32, int64_t m, 
     gp.num_k_blocks = static_cast<int>((k + BK - 1) / BK);
     gp.m_tiles = static_cast<int>((m + tile_m(cg) - 1) / tile_m(cg)); gp.n_tiles = static_cast<int>((n + BN - 1) / BN);
     gp.c32 = C32;
-    OZ2_CK(launch_gemm(MODE_RAW, cg, 0, ta, tb, gp, g_ts.num_sms, g_ts.stream));
+    OZ2_CK(launch_gemm(mode, cg, 0, ta, tb, gp, g_ts.num_sms, g_ts.stream));
     return OZ2_SUCCESS;
 }
 

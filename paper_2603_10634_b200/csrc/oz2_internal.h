@@ -27,7 +27,15 @@ constexpr int PAD_M = 256;       // row padding of operand planes (tile multiple
 constexpr int PAD_N = 256;
 constexpr int PAD_K = 128;
 
-enum GemmMode : int { MODE_RESIDUE = 0, MODE_BOUND = 1, MODE_RAW = 2 };
+// FP8 (kind::f8f6f4, E4M3 -> FP32) modes, and the same three on the INT8 tensor path
+// (kind::i8, S8/U8 -> S32) of the INT8 Ozaki-II scheme (NEXT-3): MODE_X_I8 = MODE_X + 3
+enum GemmMode : int {
+    MODE_RESIDUE = 0, MODE_BOUND = 1, MODE_RAW = 2,
+    MODE_RESIDUE_I8 = 3, MODE_BOUND_I8 = 4, MODE_RAW_I8 = 5
+};
+
+// moduli families (the scheme of the call)
+enum Family : int { FAMILY_HYBRID_FP8 = 0, FAMILY_INT8 = 1 };
 
 // ---- CRT ------------------------------------------------------------------------
 struct CrtParams {
@@ -42,7 +50,8 @@ struct CrtParams {
 
 struct ModEpi {          // per modulus, residue-GEMM epilogue
     float p, pinv;
-    float coef[3];       // square: (s, s, 1); non-square: (240, -15, 16)
+    float w16;           // smod(2^16, p): INT32 accumulators are split as hi 2^16 + lo
+    float coef[3];       // square: (s, s, 1); non-square: (240, -15, 16); INT8: (1)
     int a_plane[3];      // digit-plane index of the A operand of product x
     int b_plane[3];
 };
@@ -74,10 +83,14 @@ struct GemmParams {
 };
 
 // ---- residue / digit split ------------------------------------------------------
+constexpr int kNumSquares = 6;   // square moduli lead the hybrid list (33^2 ... 23^2)
+
 struct ModDig {
     double p_d, pinv_d;
     float p_f, pinv_f, s_f, inv_s_f;
     float hp_f;                  // (p even ? 1/2 : 0) / p: offset of the symmetric rounding
+    float h_f;                   // p even ? 1/2 : 0
+    float w8[8];                 // smod(2^(8i), p) as floats: byte-chunk weights
     int square;
     int plane0;                  // first digit plane of this modulus
 };
@@ -85,6 +98,10 @@ struct ModDig {
 struct DigitParams {
     int num_moduli;
     int num_planes;
+    int int8;                    // 1: INT8 scheme (one S8 residue plane per modulus)
+    // reduction-depth limits on |X'|: the 1.5 2^52 rounding trick needs |q| <= 2^51, so
+    // one FP64 step serves |X'| < 2^50 p_min and the p 2^36 pre-reduction |X'| < 2^86 p_min
+    double lim1, lim2;
     const uint16_t* pow2tab;     // [N][kPow2Tab]
     ModDig mod[kMaxModuli];
 };
@@ -106,10 +123,10 @@ cudaError_t launch_rowmax(const double* X, int64_t rows, int64_t k, int64_t ld, 
 cudaError_t launch_cast(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
                         const unsigned long long* maxbits, int32_t* eprime, uint8_t* xbar,
                         int64_t rows_pad, int64_t k_pad, int32_t* status,
-                        unsigned long long* sumsq, cudaStream_t st);
+                        unsigned long long* sumsq, bool i8, cudaStream_t st);
 cudaError_t launch_exps_fast(const unsigned long long* maxbits, const int32_t* eprime,
-                             const unsigned long long* sumsq, int64_t count, FastExpParams fp,
-                             int32_t* e_out, cudaStream_t st);
+                             const unsigned long long* sumsq, const uint32_t* u32, int64_t count,
+                             FastExpParams fp, int ushift, int32_t* e_out, cudaStream_t st);
 cudaError_t launch_exps(const unsigned long long* maxbits, const int32_t* eprime,
                         const uint32_t* rsmax, int64_t count, ExpParams ep, int32_t* e_out,
                         cudaStream_t st);

@@ -76,10 +76,12 @@ __device__ __forceinline__ int ilog2_bits(unsigned long long b) {
     return (63 - __clzll(static_cast<long long>(mant))) - 1074;
 }
 
+template <bool I8 = false>
 __device__ __forceinline__ int eprime_of(unsigned long long mb) {
-    // log2 mu' = 7 - floor(log2 max|x|) (eq. def:mu'nu'); zero row -> 0 (reading R3)
+    // log2 mu' = 7 - floor(log2 max|x|) (eq. def:mu'nu'); INT8 scheme: 6 - floor(...) so
+    // that ceil(|x| mu') <= 128 (R16); zero row -> 0 (reading R3)
     if (mb == 0ull || mb >= 0x7FF0000000000000ull) return 0;
-    return 7 - ilog2_bits(mb);
+    return (I8 ? 6 : 7) - ilog2_bits(mb);
 }
 
 // ---------------------------------------------------------------------------------
@@ -138,7 +140,9 @@ __device__ __forceinline__ unsigned long long fp8_sq_units(uint32_t c) {   // co
              : static_cast<unsigned long long>(mt * mt);
 }
 
-template <bool KMAJOR, bool FAST>
+// I8 (INT8 scheme, R16): X-bar = ceil(|x| 2^e') in [0, 128] as U8 (exact upper bounds),
+// squares accumulated in units of 1.
+template <bool KMAJOR, bool FAST, bool I8>
 __global__ void __launch_bounds__(256) k_cast(const double* __restrict__ X, int64_t rows, int64_t k,
                                               int64_t ld, const unsigned long long* __restrict__ maxbits,
                                               int32_t* __restrict__ eprime, uint8_t* __restrict__ xbar,
@@ -154,7 +158,7 @@ __global__ void __launch_bounds__(256) k_cast(const double* __restrict__ X, int6
         const int64_t r = r0 + t;
         if (r < rows) {
             const unsigned long long mb = maxbits[r];
-            eprime[r] = eprime_of(mb);
+            eprime[r] = eprime_of<I8>(mb);
             if (mb >= 0x7FF0000000000000ull) atomicOr(status, 1);
         }
     }
@@ -163,7 +167,7 @@ __global__ void __launch_bounds__(256) k_cast(const double* __restrict__ X, int6
     for (int j = 0; j < TR / 8; ++j) {
         const int rr = w + 8 * j;
         const int64_t r = r0 + rr;
-        const int e = (r < rows) ? eprime_of(maxbits[r]) : 0;
+        const int e = (r < rows) ? eprime_of<I8>(maxbits[r]) : 0;
         const double s1 = pow2d(e >> 1), s2 = pow2d(e - (e >> 1));   // 2^e in two exact steps
         uint32_t word = 0;
         unsigned long long sq = 0;
@@ -172,10 +176,14 @@ __global__ void __launch_bounds__(256) k_cast(const double* __restrict__ X, int6
             const double x = tile[rr * TP + lane * 4 + q];
             uint32_t c = 0;
             if (x != 0.0) {
-                c = fp8_ru_code((fabs(x) * s1) * s2);
-                c = c ? c : 1u;               // an underflowed nonzero still rounds up to 2^-9
+                if (I8) {
+                    c = static_cast<uint32_t>(ceil((fabs(x) * s1) * s2));   // exact: < 2^7 scaled
+                } else {
+                    c = fp8_ru_code((fabs(x) * s1) * s2);
+                    c = c ? c : 1u;           // an underflowed nonzero still rounds up to 2^-9
+                }
             }
-            if (FAST) sq += fp8_sq_units(c);
+            if (FAST) sq += I8 ? static_cast<unsigned long long>(c * c) : fp8_sq_units(c);
             else word |= c << (8 * q);
         }
         if (FAST) {
@@ -210,26 +218,31 @@ __global__ void k_exps(const unsigned long long* __restrict__ maxbits,
 // ---------------------------------------------------------------------------------
 // k_exps_fast: fast-mode exponents (reading R15)
 //   log2 mu_r = e'_r + t_r,  t_r = max{t : 2^(2t) S_r <= H},  H = h 2^th = RD64((P-1)/2)
-// decided exactly in integers: with S_r = U 2^-18 the test is U <= h 2^d, d = th + 18 - 2t.
+// decided exactly in integers: with S_r = U 2^-us (us = 18: FP8 squares) the test is
+// U <= h 2^d, d = th + us - 2t.
 
 __device__ __forceinline__ bool fast_fits(unsigned long long U, unsigned long long h, int hbits, int d) {
     if (d >= 0) return hbits + d > 63 || U <= (h << d);
     return -d < 64 && U <= (h >> -d);
 }
 
+// The same rule serves the INT8 scheme (R16) with U = R_r (exact bound-GEMM row max,
+// `u32`) or U = sum of squares (fast), both in units of 1 (ushift = 0).
 __global__ void k_exps_fast(const unsigned long long* __restrict__ maxbits,
                             const int32_t* __restrict__ eprime,
-                            const unsigned long long* __restrict__ sumsq, int64_t count,
-                            FastExpParams fp, int32_t* __restrict__ e_out) {
+                            const unsigned long long* __restrict__ sumsq,
+                            const uint32_t* __restrict__ u32, int64_t count,
+                            FastExpParams fp, int ushift, int32_t* __restrict__ e_out) {
     const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (r >= count) return;
-    const unsigned long long U = sumsq[r];
-    if (maxbits[r] == 0ull || U == 0ull) { e_out[r] = 0; return; }       // zero row (R3)
+    const unsigned long long U = sumsq ? sumsq[r] : static_cast<unsigned long long>(u32[r]);
+    if (maxbits[r] == 0ull) { e_out[r] = 0; return; }       // zero row (R3)
+    if (U == 0ull) { e_out[r] = eprime[r]; return; }        // no nonzero product (R3)
     const int hbits = 64 - __clzll(static_cast<long long>(fp.h));
     const int ubits = 64 - __clzll(static_cast<long long>(U));
     // U < 2^ubits <= h 2^(ubits - hbits + 1): start one step above the answer
-    int t = (fp.th + 18 - (ubits - hbits + 1)) / 2 + 2;
-    while (!fast_fits(U, fp.h, hbits, fp.th + 18 - 2 * t)) --t;
+    int t = (fp.th + ushift - (ubits - hbits + 1)) / 2 + 2;
+    while (!fast_fits(U, fp.h, hbits, fp.th + ushift - 2 * t)) --t;
     e_out[r] = eprime[r] + t;
 }
 
@@ -255,11 +268,15 @@ __device__ __forceinline__ double dfma_rn(double a, double b, double c) {   // k
     return d;
 }
 
-// residue and digits of one modulus for the 4 elements of a lane; NSTEP = 1: |y| < 2^59,
-// NSTEP = 2: |y| < 2^96 (first reduced modulo Q = p 2^36, exactly), NSTEP = 0: the
-// general M 2^E form with (2^E mod p) from the table (any |y|).
-template <int NSTEP>
-__device__ __forceinline__ void digits_one_modulus(const ModDig& md, int l, const double (&y)[4],
+// residue and digits of one modulus for the 4 elements of a lane; NSTEP = 1: |y| < 2^50 p_min
+// (~2^59 for the hybrid moduli), NSTEP = 2: |y| < 2^86 p_min (first reduced modulo
+// Q = p 2^36, exactly), NSTEP = 0: the general M 2^E form with (2^E mod p) from the
+// table (any |y|).  The limits keep every rounding quotient below 2^51, where the
+// 1.5 2^52 magic-number rounding is exact.
+// SQ: 1 square, 0 non-square, -1 read md.square at run time, 2 INT8 scheme (the residue
+// itself, as a two's-complement byte, is the single operand plane of the modulus)
+template <int NSTEP, int SQ>
+__device__ __forceinline__ void digits_one_modulus(const ModDig& md, int l, int plane0, const double (&y)[4],
                                                    const double (&M)[4], const int (&E)[4],
                                                    const uint16_t* __restrict__ pow2tab,
                                                    uint8_t* out, int64_t plane_stride) {
@@ -305,11 +322,19 @@ __device__ __forceinline__ void digits_one_modulus(const ModDig& md, int l, cons
             rf[q + 1] = rs.y;
         }
     }
-    uint8_t* o = out + static_cast<int64_t>(md.plane0) * plane_stride;
+    uint8_t* o = out + static_cast<int64_t>(plane0) * plane_stride;
+    if (SQ == 2) {
+        uint32_t w = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            w |= (static_cast<uint32_t>(__float_as_int(rf[q] + kMagic23) - 0x4B400000) & 0xFFu) << (8 * q);
+        *reinterpret_cast<uint32_t*>(o) = w;
+        return;
+    }
     // digit arithmetic on packed FP32 pairs (sm_100 FFMA2/FADD2); every value is an exact
     // small integer, the magic-number adds implement round / ceil
     const float2 M2 = make_float2(kMagic23, kMagic23), nM2 = make_float2(-kMagic23, -kMagic23);
-    if (md.square) {
+    if (SQ == 1 || (SQ < 0 && md.square)) {
         // D1 = round(r/s) ties-to-even, D2 = r - s D1 (R9)
         const float2 is2 = make_float2(md.inv_s_f, md.inv_s_f), ns2 = make_float2(-md.s_f, -md.s_f);
         uint32_t w1 = 0, w2 = 0;
@@ -345,22 +370,38 @@ __device__ __forceinline__ void digits_one_modulus(const ModDig& md, int l, cons
     }
 }
 
-template <int NSTEP, int NMOD>
+template <int NSTEP, int NMOD, bool I8>
 __device__ __forceinline__ void digits_all_moduli(const DigitParams& dp, const double (&y)[4],
                                                   const double (&M)[4], const int (&E)[4],
                                                   uint8_t* out, int64_t plane_stride) {
-    if (NMOD > 0) {
+    if (I8) {
+        // INT8 scheme: one S8 plane per modulus, plane l
+        if (NMOD > 0) {
 #pragma unroll
-        for (int l = 0; l < NMOD; ++l)
-            digits_one_modulus<NSTEP>(dp.mod[l], l, y, M, E, dp.pow2tab, out, plane_stride);
+            for (int l = 0; l < NMOD; ++l)
+                digits_one_modulus<NSTEP, 2>(dp.mod[l], l, l, y, M, E, dp.pow2tab, out, plane_stride);
+        } else {
+#pragma unroll 1
+            for (int l = 0; l < dp.num_moduli; ++l)
+                digits_one_modulus<NSTEP, 2>(dp.mod[l], l, l, y, M, E, dp.pow2tab, out, plane_stride);
+        }
+    } else if (NMOD > 0) {
+        // hybrid order (eq. p_list_hybrid): the first min(N, 6) moduli are the squares
+#pragma unroll
+        for (int l = 0; l < NMOD && l < kNumSquares; ++l)
+            digits_one_modulus<NSTEP, 1>(dp.mod[l], l, 2 * l, y, M, E, dp.pow2tab, out, plane_stride);
+#pragma unroll
+        for (int l = kNumSquares; l < NMOD; ++l)
+            digits_one_modulus<NSTEP, 0>(dp.mod[l], l, 2 * kNumSquares + 3 * (l - kNumSquares), y, M, E,
+                                         dp.pow2tab, out, plane_stride);
     } else {
 #pragma unroll 1
         for (int l = 0; l < dp.num_moduli; ++l)
-            digits_one_modulus<NSTEP>(dp.mod[l], l, y, M, E, dp.pow2tab, out, plane_stride);
+            digits_one_modulus<NSTEP, -1>(dp.mod[l], l, dp.mod[l].plane0, y, M, E, dp.pow2tab, out, plane_stride);
     }
 }
 
-template <bool KMAJOR, int NMOD>
+template <bool KMAJOR, int NMOD, bool I8>
 __global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, int64_t rows,
                                                 int64_t k, int64_t ld,
                                                 const int32_t* __restrict__ e_scale,
@@ -392,9 +433,13 @@ __global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, in
             amax = fmax(amax, a);
         }
         uint8_t* out = planes + r * k_pad + h0 + lane * 4;
+        // opaque per iteration: keeps the compiler from hoisting all M_N plane offsets
+        // (64-bit each) out of the row loop into registers
+        int64_t ps;
+        asm volatile("mov.b64 %0, %1;" : "=l"(ps) : "l"(plane_stride));
         // warp-uniform choice of the reduction depth
-        const bool need2 = __any_sync(0xffffffffu, amax >= 576460752303423488.0);   // 2^59
-        const bool need0 = __any_sync(0xffffffffu, amax >= 7.922816251426434e28);    // 2^96
+        const bool need2 = __any_sync(0xffffffffu, amax >= dp.lim1);   // 2^50 p_min (~2^59 hybrid)
+        const bool need0 = __any_sync(0xffffffffu, amax >= dp.lim2);   // 2^86 p_min
         if (need0) {
             // |X'| = M 2^E with M < 2^53 an integer (E = 0 below 2^53)
 #pragma unroll
@@ -408,11 +453,11 @@ __global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, in
                 M[q] = a;
                 E[q] = ee;
             }
-            digits_all_moduli<0, NMOD>(dp, y, M, E, out, plane_stride);
+            digits_all_moduli<0, NMOD, I8>(dp, y, M, E, out, ps);
         } else if (need2) {
-            digits_all_moduli<2, NMOD>(dp, y, M, E, out, plane_stride);
+            digits_all_moduli<2, NMOD, I8>(dp, y, M, E, out, ps);
         } else {
-            digits_all_moduli<1, NMOD>(dp, y, M, E, out, plane_stride);
+            digits_all_moduli<1, NMOD, I8>(dp, y, M, E, out, ps);
         }
     }
 }
@@ -443,23 +488,30 @@ cudaError_t launch_rowmax(const double* X, int64_t rows, int64_t k, int64_t ld, 
 cudaError_t launch_cast(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
                         const unsigned long long* maxbits, int32_t* eprime, uint8_t* xbar,
                         int64_t rows_pad, int64_t k_pad, int32_t* status,
-                        unsigned long long* sumsq, cudaStream_t st) {
+                        unsigned long long* sumsq, bool i8, cudaStream_t st) {
     dim3 grid(static_cast<unsigned>(k_pad / TH), static_cast<unsigned>(rows_pad / TR));
-    if (sumsq) {
-        if (kmajor) k_cast<true, true><<<grid, 256, 0, st>>>(X, rows, k, ld, maxbits, eprime, xbar, k_pad, status, sumsq);
-        else k_cast<false, true><<<grid, 256, 0, st>>>(X, rows, k, ld, maxbits, eprime, xbar, k_pad, status, sumsq);
-    } else {
-        if (kmajor) k_cast<true, false><<<grid, 256, 0, st>>>(X, rows, k, ld, maxbits, eprime, xbar, k_pad, status, sumsq);
-        else k_cast<false, false><<<grid, 256, 0, st>>>(X, rows, k, ld, maxbits, eprime, xbar, k_pad, status, sumsq);
+#define OZ2_CAST(KM, FA, I8_) k_cast<KM, FA, I8_><<<grid, 256, 0, st>>>(X, rows, k, ld, maxbits, eprime, xbar, k_pad, status, sumsq)
+    const int sel = (kmajor ? 4 : 0) | (sumsq ? 2 : 0) | (i8 ? 1 : 0);
+    switch (sel) {
+        case 0: OZ2_CAST(false, false, false); break;
+        case 1: OZ2_CAST(false, false, true); break;
+        case 2: OZ2_CAST(false, true, false); break;
+        case 3: OZ2_CAST(false, true, true); break;
+        case 4: OZ2_CAST(true, false, false); break;
+        case 5: OZ2_CAST(true, false, true); break;
+        case 6: OZ2_CAST(true, true, false); break;
+        default: OZ2_CAST(true, true, true); break;
     }
+#undef OZ2_CAST
     return cudaGetLastError();
 }
 
 cudaError_t launch_exps_fast(const unsigned long long* maxbits, const int32_t* eprime,
-                             const unsigned long long* sumsq, int64_t count, FastExpParams fp,
-                             int32_t* e_out, cudaStream_t st) {
+                             const unsigned long long* sumsq, const uint32_t* u32, int64_t count,
+                             FastExpParams fp, int ushift, int32_t* e_out, cudaStream_t st) {
     if (count == 0) return cudaSuccess;
-    k_exps_fast<<<static_cast<unsigned>((count + 255) / 256), 256, 0, st>>>(maxbits, eprime, sumsq, count, fp, e_out);
+    k_exps_fast<<<static_cast<unsigned>((count + 255) / 256), 256, 0, st>>>(maxbits, eprime, sumsq, u32, count, fp,
+                                                                          ushift, e_out);
     return cudaGetLastError();
 }
 
@@ -475,15 +527,24 @@ cudaError_t launch_digits(const double* X, int64_t rows, int64_t k, int64_t ld, 
                           const int32_t* e, const DigitParams& dp, uint8_t* planes,
                           int64_t rows_pad, int64_t k_pad, cudaStream_t st) {
     dim3 grid(static_cast<unsigned>(k_pad / TH), static_cast<unsigned>(rows_pad / TR));
-#define OZ2_DIG(NM)                                                                                  \
-    if (kmajor) k_digits<true, NM><<<grid, 256, 0, st>>>(X, rows, k, ld, e, dp, planes, rows_pad, k_pad); \
-    else k_digits<false, NM><<<grid, 256, 0, st>>>(X, rows, k, ld, e, dp, planes, rows_pad, k_pad);
-    switch (dp.num_moduli) {   // fully unrolled for the common moduli counts
-        case 12: OZ2_DIG(12) break;
-        case 13: OZ2_DIG(13) break;
-        case 14: OZ2_DIG(14) break;
-        case 16: OZ2_DIG(16) break;
-        default: OZ2_DIG(0) break;
+#define OZ2_DIG(NM, I8_)                                                                                     \
+    if (kmajor) k_digits<true, NM, I8_><<<grid, 256, 0, st>>>(X, rows, k, ld, e, dp, planes, rows_pad, k_pad); \
+    else k_digits<false, NM, I8_><<<grid, 256, 0, st>>>(X, rows, k, ld, e, dp, planes, rows_pad, k_pad);
+    if (dp.int8) {
+        switch (dp.num_moduli) {   // INT8 scheme: 14..16 moduli are the FP64-level counts
+            case 14: OZ2_DIG(14, true) break;
+            case 15: OZ2_DIG(15, true) break;
+            case 16: OZ2_DIG(16, true) break;
+            default: OZ2_DIG(0, true) break;
+        }
+    } else {
+        switch (dp.num_moduli) {   // fully unrolled for the common moduli counts
+            case 12: OZ2_DIG(12, false) break;
+            case 13: OZ2_DIG(13, false) break;
+            case 14: OZ2_DIG(14, false) break;
+            case 16: OZ2_DIG(16, false) break;
+            default: OZ2_DIG(0, false) break;
+        }
     }
 #undef OZ2_DIG
     return cudaGetLastError();

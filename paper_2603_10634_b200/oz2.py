@@ -17,6 +17,9 @@ OZ2_ERR_ALLOC = 2
 OZ2_ERR_WORKSPACE = 3
 OZ2_ERR_NOT_SUPPORTED = 4
 OZ2_ERR_NONFINITE = 5
+OZ2_SCHEME_FP8 = 0
+OZ2_SCHEME_INT8 = 1
+_SCHEMES = {"fp8": OZ2_SCHEME_FP8, "int8": OZ2_SCHEME_INT8}
 OZ2_MODE_ACCURATE = 0
 OZ2_MODE_FAST = 1
 _MODES = {"accurate": OZ2_MODE_ACCURATE, "fast": OZ2_MODE_FAST}
@@ -57,10 +60,17 @@ SIGNATURES = [
       _vp, _c_int64, ctypes.c_double, _vp, _c_int64, ctypes.c_int, ctypes.POINTER(oz2_options)]),
     ("oz2_set_stream", ctypes.c_int, [_vp]),
     ("oz2_set_mode", ctypes.c_int, [ctypes.c_int]),
+    ("oz2_set_scheme", ctypes.c_int, [ctypes.c_int]),
+    ("oz2_get_scheme", ctypes.c_int, []),
     ("oz2_get_mode", ctypes.c_int, []),
     ("oz2_workspace_size", ctypes.c_size_t,
      [ctypes.c_char, ctypes.c_char, _c_int64, _c_int64, _c_int64, ctypes.c_int]),
     ("oz2_set_workspace", ctypes.c_int, [_vp, ctypes.c_size_t]),
+    ("oz2_set_blocking", ctypes.c_int, [_c_int64, _c_int64]),
+    ("oz2_get_blocking", ctypes.c_int, [ctypes.POINTER(_c_int64), ctypes.POINTER(_c_int64)]),
+    ("oz2_workspace_size_blocked", ctypes.c_size_t, [_c_int64, _c_int64, _c_int64, ctypes.c_int, _c_int64, _c_int64]),
+    ("oz2_plan_blocking", ctypes.c_int,
+     [_c_int64, _c_int64, _c_int64, ctypes.c_int, ctypes.c_size_t, ctypes.POINTER(_c_int64), ctypes.POINTER(_c_int64)]),
     ("oz2_get_status", ctypes.c_int, [ctypes.POINTER(ctypes.c_int32)]),
     ("oz2_set_timing", ctypes.c_int, [ctypes.c_int]),
     ("oz2_get_timing", ctypes.c_int, [ctypes.POINTER(ctypes.c_float), ctypes.c_int]),
@@ -69,6 +79,7 @@ SIGNATURES = [
     ("oz2_plan_query", ctypes.c_int, [ctypes.c_int, _c_int64, ctypes.POINTER(oz2_plan_info)]),
     ("oz2_version", ctypes.c_char_p, []),
     ("oz2_fp8_gemm_raw", ctypes.c_int, [_vp, _vp, _vp, _c_int64, _c_int64, _c_int64]),
+    ("oz2_int8_gemm_raw", ctypes.c_int, [_vp, _vp, _vp, _c_int64, _c_int64, _c_int64]),
 ]
 
 _lib = None
@@ -126,12 +137,42 @@ def oz2_get_mode():
     return lib().oz2_get_mode()
 
 
+def oz2_set_scheme(scheme):
+    """scheme: OZ2_SCHEME_FP8 / OZ2_SCHEME_INT8 or "fp8" / "int8"."""
+    return lib().oz2_set_scheme(_SCHEMES.get(scheme, scheme))
+
+
+def oz2_get_scheme():
+    return lib().oz2_get_scheme()
+
+
 def oz2_workspace_size(transa, transb, m, n, k, num_moduli):
     return lib().oz2_workspace_size(_ch(transa), _ch(transb), m, n, k, num_moduli)
 
 
 def oz2_set_workspace(ptr, nbytes):
     return lib().oz2_set_workspace(ptr, nbytes)
+
+
+def oz2_set_blocking(mb, nb):
+    return lib().oz2_set_blocking(mb, nb)
+
+
+def oz2_get_blocking():
+    mb, nb = _c_int64(0), _c_int64(0)
+    _check(lib().oz2_get_blocking(ctypes.byref(mb), ctypes.byref(nb)), "oz2_get_blocking")
+    return mb.value, nb.value
+
+
+def oz2_workspace_size_blocked(m, n, k, num_moduli, mb, nb):
+    return lib().oz2_workspace_size_blocked(m, n, k, num_moduli, mb, nb)
+
+
+def oz2_plan_blocking(m, n, k, num_moduli, nbytes):
+    """(status, mb, nb) for a workspace of nbytes (host only)."""
+    mb, nb = _c_int64(0), _c_int64(0)
+    rc = lib().oz2_plan_blocking(m, n, k, num_moduli, nbytes, ctypes.byref(mb), ctypes.byref(nb))
+    return rc, mb.value, nb.value
 
 
 def oz2_get_status():
@@ -178,6 +219,10 @@ def oz2_fp8_gemm_raw(a, b, C32, m, n, k):
     return lib().oz2_fp8_gemm_raw(a, b, C32, m, n, k)
 
 
+def oz2_int8_gemm_raw(a, b, C32, m, n, k):
+    return lib().oz2_int8_gemm_raw(a, b, C32, m, n, k)
+
+
 # ---- torch convenience (still only marshalling) ----------------------------------
 
 _ws = {}
@@ -208,19 +253,22 @@ def _colmajor(X):
     return X, "N", X.stride(1)
 
 
-def dgemm(A, B, alpha=1.0, beta=0.0, C=None, num_moduli=13, mode=None):
+def dgemm(A, B, alpha=1.0, beta=0.0, C=None, num_moduli=13, mode=None, scheme=None):
     """C <- alpha A @ B + beta C on torch float64 CUDA tensors via oz2_dgemm.
 
     Any 2-D strided layout is accepted; the result is column-major (Fortran order).
-    ``mode`` ("accurate" / "fast") applies to this call only; None keeps the thread's."""
-    if mode is None:
-        return _dgemm(A, B, alpha, beta, C, num_moduli)
-    prev = oz2_get_mode()
-    _check(oz2_set_mode(mode), "oz2_set_mode")
+    ``mode`` ("accurate" / "fast") and ``scheme`` ("fp8" / "int8") apply to this call
+    only; None keeps the thread's setting."""
+    prev_mode, prev_scheme = oz2_get_mode(), oz2_get_scheme()
+    if mode is not None:
+        _check(oz2_set_mode(mode), "oz2_set_mode")
+    if scheme is not None:
+        _check(oz2_set_scheme(scheme), "oz2_set_scheme")
     try:
         return _dgemm(A, B, alpha, beta, C, num_moduli)
     finally:
-        oz2_set_mode(prev)
+        oz2_set_mode(prev_mode)
+        oz2_set_scheme(prev_scheme)
 
 
 def _dgemm(A, B, alpha, beta, C, num_moduli):

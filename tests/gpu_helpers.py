@@ -24,7 +24,8 @@ def store(X: np.ndarray, trans: str):
 
 
 def run(A, B, N, transa="N", transb="N", alpha=1.0, beta=0.0, C0=None, e_mu_in=None,
-        e_nu_in=None, want_digits=False, ldc_pad=0, mode="accurate"):
+        e_nu_in=None, want_digits=False, ldc_pad=0, mode="accurate", want_residues=True,
+        scheme="fp8"):
     """Full pipeline through oz2_dgemm_ex; returns dict of host numpy outputs."""
     t = torch()
     m, k = A.shape
@@ -46,9 +47,14 @@ def run(A, B, N, transa="N", transb="N", alpha=1.0, beta=0.0, C0=None, e_mu_in=N
         "smax": t.zeros(n, dtype=t.float32, device=dev),
         "e_mu": t.zeros(m, dtype=t.int32, device=dev),
         "e_nu": t.zeros(n, dtype=t.int32, device=dev),
-        "residues": t.zeros(N * m * n, dtype=t.int16, device=dev),
     }
-    M = oz2.oz2_plan_query(N, k).num_planes
+    if want_residues:    # whole-problem residues force the unblocked layout
+        out["residues"] = t.zeros(N * m * n, dtype=t.int16, device=dev)
+    assert oz2.oz2_set_scheme(scheme) == 0
+    try:
+        M = oz2.oz2_plan_query(N, k).num_planes
+    finally:
+        oz2.oz2_set_scheme("fp8")
     if want_digits:
         out["digits_a"] = t.zeros(M * m * k, dtype=t.uint8, device=dev)
         out["digits_b"] = t.zeros(M * n * k, dtype=t.uint8, device=dev)
@@ -64,18 +70,20 @@ def run(A, B, N, transa="N", transb="N", alpha=1.0, beta=0.0, C0=None, e_mu_in=N
         opt.e_nu_in = b.data_ptr()
     oz2.oz2_set_stream(t.cuda.current_stream().cuda_stream)
     oz2.oz2_set_workspace(None, 0)
-    assert oz2.oz2_set_mode(mode) == 0
+    assert oz2.oz2_set_mode(mode) == 0 and oz2.oz2_set_scheme(scheme) == 0
     try:
         rc = oz2.oz2_dgemm_ex(transa, transb, m, n, k, alpha, dA.data_ptr(), lda, dB.data_ptr(),
                               ldb, beta, dC.data_ptr(), ldc, N, opt)
     finally:
         oz2.oz2_set_mode("accurate")
+        oz2.oz2_set_scheme("fp8")
     assert rc == 0, rc
     t.cuda.synchronize()
     res = {key: v.cpu().numpy() for key, v in out.items()}
     res["abar"] = res["abar"][: m * k].reshape(m, k)
     res["bbar"] = res["bbar"][: n * k].reshape(n, k)
-    res["residues"] = res["residues"].reshape(N, n, m).transpose(0, 2, 1)   # [l][i][j]
+    if want_residues:
+        res["residues"] = res["residues"].reshape(N, n, m).transpose(0, 2, 1)   # [l][i][j]
     if want_digits:
         res["digits_a"] = res["digits_a"].reshape(M, m, k)
         res["digits_b"] = res["digits_b"].reshape(M, n, k)

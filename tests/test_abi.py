@@ -95,3 +95,59 @@ def test_argument_errors_before_device(oz2mod):
     assert oz2mod.oz2_dgemm("N", "N", 4, 1, 1, 1.0, 0, 4, 0, 1, 0.0, 0, 4, 1) == -14
     assert oz2mod.oz2_dgemm("N", "N", 0, 0, 0, 1.0, 0, 1, 0, 1, 0.0, 0, 1, 12) == 0   # quick return
     assert oz2mod.oz2_workspace_size("N", "N", 64, 64, 64, 14) > 0
+
+
+def test_blocking_planner(oz2mod):
+    """m/n blocking: full workspace -> unblocked; smaller -> blocks that fit,
+    multiples of 256 (or the full extent), with the largest column block first."""
+    for (m, n, k, N) in [(16384, 16384, 16384, 13), (5000, 3000, 777, 12), (300, 70000, 4096, 16)]:
+        full = oz2mod.oz2_workspace_size("N", "N", m, n, k, N)
+        assert oz2mod.oz2_workspace_size_blocked(m, n, k, N, 0, 0) == full
+        assert oz2mod.oz2_plan_blocking(m, n, k, N, full) == (0, m, n)
+        prev = None
+        for frac in [0.9, 0.5, 0.25, 0.1, 0.03]:
+            rc, mb, nb = oz2mod.oz2_plan_blocking(m, n, k, N, int(full * frac))
+            if rc != 0:
+                assert rc == oz2mod.OZ2_ERR_WORKSPACE
+                assert oz2mod.oz2_workspace_size_blocked(m, n, k, N, 256, 256) > int(full * frac)
+                continue
+            assert (mb == m or mb % 256 == 0) and (nb == n or nb % 256 == 0)
+            assert 0 < mb <= m and 0 < nb <= n and (mb, nb) != (m, n)
+            assert oz2mod.oz2_workspace_size_blocked(m, n, k, N, mb, nb) <= int(full * frac)
+            # maximal: one more 256-row slab of A would not fit (unless mb is already m)
+            if mb < m:
+                assert oz2mod.oz2_workspace_size_blocked(m, n, k, N, mb + 256, nb) > int(full * frac)
+            if prev:
+                assert mb * nb <= prev[0] * prev[1]
+            prev = (mb, nb)
+    # too small for anything
+    assert oz2mod.oz2_plan_blocking(4096, 4096, 4096, 13, 1 << 20)[0] == oz2mod.OZ2_ERR_WORKSPACE
+    assert oz2mod.oz2_set_blocking(100, 0) == -1 and oz2mod.oz2_set_blocking(0, 300) == -2
+    assert oz2mod.oz2_set_blocking(0, 0) == 0
+
+
+def test_int8_scheme_plan_matches_oracle(oz2mod):
+    """INT8 scheme (NEXT-3): moduli, planes (one per modulus), P, CRT weights and fast_H
+    of the host planner equal the oracle's; the scheme switch is per thread."""
+    from fractions import Fraction
+    from oracle import int8, moduli as mod, scheme
+    assert oz2mod.oz2_get_scheme() == oz2mod.OZ2_SCHEME_FP8
+    assert oz2mod.oz2_set_scheme(5) == -1
+    assert oz2mod.oz2_set_scheme("int8") == 0
+    try:
+        for N in [2, 14, 15, 16, 20, 33]:
+            assert oz2mod.oz2_moduli(N) == mod.int8_moduli(N)
+            info = oz2mod.oz2_plan_query(N, 4096)
+            pl = int8.plan(N)
+            assert info.num_planes == N and info.num_squares == 0
+            L = info.num_limbs
+            assert sum(info.P_limbs[t] << (32 * t) for t in range(L)) == pl.P
+            for l, w in enumerate(pl.w):
+                assert sum(info.w_limbs[l][t] << (32 * t) for t in range(L)) == w
+            assert Fraction(info.fast_H) == scheme.fast_H(pl)
+        # workspace: N planes per operand instead of M_N
+        w8 = oz2mod.oz2_workspace_size("N", "N", 4096, 4096, 4096, 14)
+    finally:
+        oz2mod.oz2_set_scheme("fp8")
+    w_fp8 = oz2mod.oz2_workspace_size("N", "N", 4096, 4096, 4096, 14)
+    assert w8 < w_fp8

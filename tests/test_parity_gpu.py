@@ -269,8 +269,9 @@ def test_torch_wrapper_layouts(dev):
 
 
 def test_workspace_and_timing_api(dev):
-    """Caller-owned workspace (too small -> OZ2_ERR_WORKSPACE, exact size works), the
-    per-phase timers, and the single-process path of the row-sharded driver."""
+    """Caller-owned workspace (below the full size -> m/n blocking, far too small ->
+    OZ2_ERR_WORKSPACE, exact size works unblocked), the per-phase timers, and the
+    single-process path of the row-sharded driver."""
     import torch
     from paper_2603_10634_b200.dist import dgemm_rowsharded
     m, k, n, N = 300, 520, 270, 13
@@ -282,6 +283,11 @@ def test_workspace_and_timing_api(dev):
     dev.oz2_set_stream(torch.cuda.current_stream().cuda_stream)
     dev.oz2_set_workspace(small.data_ptr(), small.numel())
     args = ("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0, C.data_ptr(), m, N)
+    assert dev.oz2_dgemm(*args) == 0
+    assert dev.oz2_get_blocking() != (m, n)
+    torch.cuda.synchronize()
+    C_blocked = C.cpu().numpy().copy()
+    dev.oz2_set_workspace(small.data_ptr(), 4096)
     assert dev.oz2_dgemm(*args) == dev.OZ2_ERR_WORKSPACE
     ws = torch.empty(need, dtype=torch.uint8, device="cuda")
     dev.oz2_set_workspace(ws.data_ptr(), ws.numel())
@@ -293,8 +299,10 @@ def test_workspace_and_timing_api(dev):
     parts = sum(v for key, v in ph.items() if key != "total")
     assert ph["total"] > 0 and abs(parts - ph["total"]) <= 0.05 * ph["total"] + 0.05
     dev.oz2_set_workspace(None, 0)
+    assert dev.oz2_get_blocking() == (m, n)
     ref = scheme.dgemm(A.cpu().numpy(), B.cpu().numpy(), N).C
     assert np.array_equal(C.cpu().numpy(), ref)
+    assert np.array_equal(C_blocked, ref)
     C2 = dgemm_rowsharded(A, B, num_moduli=N)          # no process group: plain call
     assert np.array_equal(C2.cpu().numpy(), ref)
 
@@ -311,3 +319,37 @@ def test_k_beyond_exactness_window(dev):
     for l in range(N):
         assert np.array_equal(res["residues"][l], ref.residues[l]), l
     assert np.array_equal(res["C"], ref.C)
+
+
+def _depth_edge_matrix(pmin, m=24, k=160, seed=0):
+    """Rows whose largest |entry| sits just below / at / above the reduction-depth limits
+    2^50 p_min and 2^86 p_min of the residue kernel (and far beyond), as exact integers."""
+    rng = np.random.default_rng(seed)
+    A = rng.integers(-1000, 1000, size=(m, k)).astype(np.float64)
+    lim1, lim2 = float(pmin) * 2.0 ** 50, float(pmin) * 2.0 ** 86
+    edges = [lim1 - 2 ** 12, lim1, lim1 + 2 ** 12, lim2 * (1 - 2.0 ** -40), lim2, lim2 * (1 + 2.0 ** -40),
+             2.0 ** 63 - 2 ** 11, 2.0 ** 64, 2.0 ** 96 - 2.0 ** 44, 2.0 ** 120 + 2.0 ** 70]
+    for i, v in enumerate(edges):
+        A[2 * i, 3 + i] = v
+        A[2 * i + 1, 5 + i] = -v
+        A[2 * i + 1, 7 + i] = np.floor(v / 3)
+    return A
+
+
+@pytest.mark.parametrize("sch,N", [("fp8", 12), ("fp8", 20), ("fp8", 33), ("int8", 15), ("int8", 33)])
+def test_residue_depth_boundaries(dev, sch, N):
+    """Imported zero exponents make A' = A: residues of integers straddling every
+    reduction-depth switch of k_digits must match mod(A'B', p) exactly (CRT output not
+    compared: the certified condition is deliberately violated)."""
+    from gpu_helpers import run
+    from oracle import moduli as mod
+    ps = mod.int8_moduli(N) if sch == "int8" else mod.hybrid_moduli(N)
+    A = _depth_edge_matrix(min(ps), seed=N)
+    rng = np.random.default_rng(N + 1)
+    B = rng.integers(-1000, 1000, size=(A.shape[1], 40)).astype(np.float64)
+    res = run(A, B, N, e_mu_in=[0] * A.shape[0], e_nu_in=[0] * B.shape[1], scheme=sch)
+    Aint = scheme.to_integral(A, [0] * A.shape[0])
+    BintT = scheme.to_integral(B.T.copy(), [0] * B.shape[1])
+    for l, p in enumerate(ps):
+        want = scheme.modprod_direct(scheme.residues(Aint, p), scheme.residues(BintT, p), p)
+        assert np.array_equal(res["residues"][l], want), p
