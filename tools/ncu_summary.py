@@ -21,12 +21,19 @@ METRICS = [
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM %"),
     ("smsp__inst_executed.sum", "warp instr"),
     ("launch__registers_per_thread", "regs"),
+    ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "stall long-sb"),
+    ("smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio", "stall math-throttle"),
 ]
 
 
 def load(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(out)))
+    if rep.endswith(".csv"):          # `ncu -i rep --page raw --csv` output saved on the box
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = [r for r in csv.reader(io.StringIO(out)) if r]
+    while rows and rows[0][0] != "ID":
+        rows = rows[1:]
     h, units = rows[0], rows[1]
     return h, units, rows[2:]
 
@@ -39,6 +46,7 @@ def main():
     ap.add_argument("--m", type=int, default=16384)
     ap.add_argument("--N", type=int, default=13)
     ap.add_argument("--title", default="")
+    ap.add_argument("--scheme", default="fp8")
     a = ap.parse_args()
     h, units, rows = load(a.rep)
     lines = [f"# ncu summary {a.title}", "", f"source: `{a.rep}` (ncu --set full --clock-control none)", ""]
@@ -50,7 +58,7 @@ def main():
         name = r[h.index("Kernel Name")]
         short = name.split("(")[0].replace("void ", "")
         lines.append(f"| `{short}` | " + " | ".join(r[i] for i, _, _ in cols) + " |")
-        if "gemm_kernel<0" in name and res is None:
+        if ("gemm_kernel<0" in name or "gemm_kernel<3" in name) and res is None:
             res = r
     with open(a.out_md, "w") as f:
         f.write("\n".join(lines) + "\n")
@@ -64,6 +72,7 @@ def main():
         tr = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
         with open(a.traffic_json, "w") as f:
             json.dump({"kernel": res[h.index("Kernel Name")].split("(")[0], "m": a.m, "num_moduli": a.N,
+                       "scheme": a.scheme,
                        "dram_bytes_per_launch": tr, "source": a.rep}, f, indent=1)
     print("\n".join(lines))
 

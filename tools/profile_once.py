@@ -8,9 +8,12 @@ from synth import gen_device
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 N = int(sys.argv[2]) if len(sys.argv) > 2 else 13
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+scheme = sys.argv[4] if len(sys.argv) > 4 else "fp8"
+mode = sys.argv[5] if len(sys.argv) > 5 else "accurate"
 A = gen_device(n, n, "phi", phi=1.0, seed=1)
 B = gen_device(n, n, "phi", phi=1.0, seed=2)
 C = torch.empty((n, n), dtype=torch.float64, device="cuda").t()
+assert P.oz2_set_scheme(scheme) == 0 and P.oz2_set_mode(mode) == 0
 ws = torch.empty(P.oz2_workspace_size("N", "N", n, n, n, N), dtype=torch.uint8, device="cuda")
 P.oz2_set_workspace(ws.data_ptr(), ws.numel())
 P.oz2_set_stream(torch.cuda.current_stream().cuda_stream)
