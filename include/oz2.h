@@ -33,6 +33,7 @@ extern "C" {
 /* ---- schemes (see oz2_set_scheme) ---------------------------------------------- */
 #define OZ2_SCHEME_FP8         0   /* the paper's FP8 Ozaki-II, hybrid moduli (default) */
 #define OZ2_SCHEME_INT8        1   /* INT8 Ozaki-II, moduli <= 256 (R16)     */
+#define OZ2_SCHEME_FP8_KARATSUBA 2 /* FP8 Ozaki-II, Karatsuba-only moduli   */
 
 /* ---- scaling modes (see oz2_set_mode) ------------------------------- */
 #define OZ2_MODE_ACCURATE      0   /* bound GEMM on FP8 tensor cores       */
@@ -148,6 +149,12 @@ int oz2_get_mode(void);
  * log2 mu_i = e'_i + max{t : 2^(2t) R_i <= RD64((P-1)/2)} (reading R16).  k <= 2^16 (else
  * OZ2_ERR_NOT_SUPPORTED).  In oz2_options the abar/bbar outputs then hold the U8 bounds,
  * rmax/smax the exact S32 maxima (as uint32 bits) and digits_a/b the S8 residue planes.
+ * OZ2_SCHEME_FP8_KARATSUBA: the FP8 scheme with the Karatsuba-only moduli of the paper's
+ * Sec. III-B (eq. p_list_karatsuba: greedy pairwise coprime from 513 down,
+ * {513, 512, 511, 509, 505, ...}); every modulus takes the 3-digit Karatsuba split with
+ * s = 16 and eq. C'-Karatsuba (3N GEMMs, +1 bound GEMM in accurate
+ * mode); FP64 level needs N >= 13.  Everything else (modes, blocking, long K,
+ * outputs) is that of OZ2_SCHEME_FP8.
  * Returns -1 for any other value. */
 int oz2_set_scheme(int scheme);
 int oz2_get_scheme(void);

@@ -389,14 +389,28 @@ class Result:
     extra: dict = field(default_factory=dict)
 
 
-def plan_constants(N: int):
-    plan = mod.crt_plan(mod.hybrid_moduli(N))
+def family_moduli(N: int, family: str = "hybrid"):
+    """The first N moduli of a FP8 family: "hybrid" (eq. p_list_hybrid, the
+    paper's method) or "karatsuba" (eq. p_list_karatsuba: every modulus
+    p <= 513 with s = 16 and the Karatsuba digits; N >= 13 for FP64 level)."""
+    if family == "hybrid":
+        return mod.hybrid_moduli(N)
+    if family == "karatsuba":
+        return mod.karatsuba_moduli(N)
+    raise ValueError(f"unknown FP8 moduli family {family!r}")
+
+
+def plan_constants(N: int, family: str = "hybrid"):
+    plan = mod.crt_plan(family_moduli(N, family))
     return plan, mod.p_prime(plan.P), mod.delta()
 
 
 def dgemm(A: np.ndarray, B: np.ndarray, N: int, alpha: float = 1.0, beta: float = 0.0,
-          C=None, e_mu=None, e_nu=None, want_digits: bool = False, mode: str = "accurate") -> Result:
-    """C <- alpha * emul(A B) + beta * C, accurate mode, hybrid moduli.
+          C=None, e_mu=None, e_nu=None, want_digits: bool = False, mode: str = "accurate",
+          family: str = "hybrid") -> Result:
+    """C <- alpha * emul(A B) + beta * C, accurate (or fast) mode, hybrid (or the
+    Karatsuba-only, P:264-276) moduli.  Steps 1-4 and 6-8 do not depend on the family;
+    only the moduli (hence P, P', the CRT weights) and the digit route of step 6 do.
 
     ``e_mu`` / ``e_nu`` optionally fix the scaling exponents (used by tests that feed
     the oracle's own exponents into the GPU path, never the other way round)."""
@@ -407,7 +421,7 @@ def dgemm(A: np.ndarray, B: np.ndarray, N: int, alpha: float = 1.0, beta: float 
     assert k == k2
     if not (np.all(np.isfinite(A)) and np.all(np.isfinite(B))):
         raise ValueError("non-finite input (reading R12)")
-    plan, Pp, dlt = plan_constants(N)
+    plan, Pp, dlt = plan_constants(N, family)
     BT = B.T.copy()
     eA, Abar = prescale_rows(A)
     eB, BbarT = prescale_rows(BT)
@@ -452,10 +466,10 @@ def dgemm(A: np.ndarray, B: np.ndarray, N: int, alpha: float = 1.0, beta: float 
 # sampled entries at sizes where the full oracle is too slow
 
 
-def row_exponents(X: np.ndarray, rows, Y_T: np.ndarray, N: int):
+def row_exponents(X: np.ndarray, rows, Y_T: np.ndarray, N: int, family: str = "hybrid"):
     """e' and e_mu for selected rows r of X (m x k) against the full other operand
     Y_T (n x k): R_r = max_j C-bar'_rj needs the whole row r of A-bar B-bar."""
-    plan, Pp, dlt = plan_constants(N)
+    plan, Pp, dlt = plan_constants(N, family)
     k = X.shape[1]
     eY, YbarT = prescale_rows_fast(Y_T)
     Ys = fp8_scaled_int(YbarT).astype(np.float64)          # exact integers <= 2^17
@@ -494,11 +508,11 @@ def prescale_rows_fast(X: np.ndarray):
     return e_prime.tolist(), codes.astype(np.uint8)
 
 
-def entries(A: np.ndarray, B: np.ndarray, N: int, I, J, e_mu_I, e_nu_J):
+def entries(A: np.ndarray, B: np.ndarray, N: int, I, J, e_mu_I, e_nu_J, family: str = "hybrid"):
     """Residues C'_l(i, j), C'(i, j) and C(i, j) for the selected entries, given the
     exponents of rows I and columns J (each entry is N exact dot products of
     length k)."""
-    plan = mod.crt_plan(mod.hybrid_moduli(N))
+    plan = mod.crt_plan(family_moduli(N, family))
     res = np.zeros((N, len(I), len(J)), dtype=np.int64)
     C = np.zeros((len(I), len(J)))
     BT = B.T

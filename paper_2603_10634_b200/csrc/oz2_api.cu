@@ -91,6 +91,16 @@ static std::vector<int> hybrid_moduli(int N) {
     }
     return out;
 }
+static std::vector<int> karatsuba_moduli(int N) {
+    // greedy pairwise coprime from 513 down (eq. p_list_karatsuba)
+    std::vector<int> out;
+    for (int c = 513; c >= 2 && static_cast<int>(out.size()) < N; --c) {
+        bool ok = true;
+        for (int q : out) ok = ok && gcd_i(c, q) == 1;
+        if (ok) out.push_back(c);
+    }
+    return out;
+}
 static bool is_square_i(int p) { const int s = static_cast<int>(std::lround(std::sqrt(static_cast<double>(p)))); return s * s == p; }
 
 static float rd32(long double x) {
@@ -125,8 +135,9 @@ static Plan build_plan(int N, int family) {
     pl.N = N;
     pl.family = family;
     const bool i8 = family == FAMILY_INT8;
-    pl.p = i8 ? int8_moduli(N) : hybrid_moduli(N);
-    if (!i8)
+    const bool kara = family == FAMILY_KARATSUBA_FP8;   // every modulus takes the Karatsuba digits
+    pl.p = i8 ? int8_moduli(N) : kara ? karatsuba_moduli(N) : hybrid_moduli(N);
+    if (!i8 && !kara)
         for (int p : pl.p) pl.nsq += is_square_i(p) ? 1 : 0;
     pl.M = i8 ? N : 2 * pl.nsq + 3 * (N - pl.nsq);
     Big P{1};
@@ -203,6 +214,7 @@ static Plan build_plan(int N, int family) {
     dp.num_moduli = N;
     dp.num_planes = pl.M;
     dp.int8 = i8 ? 1 : 0;
+    dp.num_squares = pl.nsq;
     {
         int pmin = pl.p[0];
         for (int p : pl.p) pmin = p < pmin ? p : pmin;
@@ -228,7 +240,7 @@ static Plan build_plan(int N, int family) {
                 v = (v * 256) % p;
             }
         }
-        md.square = i8 ? 2 : (is_square_i(p) ? 1 : 0);
+        md.square = i8 ? 2 : (!kara && is_square_i(p) ? 1 : 0);
         const int s = md.square ? static_cast<int>(std::lround(std::sqrt(static_cast<double>(p)))) : 16;
         md.s_f = static_cast<float>(s);
         md.inv_s_f = 1.0f / static_cast<float>(s);
@@ -794,7 +806,7 @@ int oz2_set_mode(int mode) {
 int oz2_get_mode(void) { return g_ts.mode; }
 
 int oz2_set_scheme(int scheme) {
-    if (scheme != OZ2_SCHEME_FP8 && scheme != OZ2_SCHEME_INT8) return -1;
+    if (scheme != OZ2_SCHEME_FP8 && scheme != OZ2_SCHEME_INT8 && scheme != OZ2_SCHEME_FP8_KARATSUBA) return -1;
     g_ts.scheme = scheme;
     return OZ2_SUCCESS;
 }

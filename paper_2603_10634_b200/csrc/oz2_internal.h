@@ -35,7 +35,7 @@ enum GemmMode : int {
 };
 
 // moduli families (the scheme of the call)
-enum Family : int { FAMILY_HYBRID_FP8 = 0, FAMILY_INT8 = 1 };
+enum Family : int { FAMILY_HYBRID_FP8 = 0, FAMILY_INT8 = 1, FAMILY_KARATSUBA_FP8 = 2 };
 
 // ---- CRT ------------------------------------------------------------------------
 struct CrtParams {
@@ -99,6 +99,7 @@ struct DigitParams {
     int num_moduli;
     int num_planes;
     int int8;                    // 1: INT8 scheme (one S8 residue plane per modulus)
+    int num_squares;             // FP8: leading square moduli (hybrid min(N, 6), Karatsuba 0)
     // reduction-depth limits on |X'|: the 1.5 2^52 rounding trick needs |q| <= 2^51, so
     // one FP64 step serves |X'| < 2^50 p_min and the p 2^36 pre-reduction |X'| < 2^86 p_min
     double lim1, lim2;

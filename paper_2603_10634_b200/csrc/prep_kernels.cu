@@ -370,7 +370,7 @@ __device__ __forceinline__ void digits_one_modulus(const ModDig& md, int l, int 
     }
 }
 
-template <int NSTEP, int NMOD, bool I8>
+template <int NSTEP, int NMOD, bool I8, int NSQ>
 __device__ __forceinline__ void digits_all_moduli(const DigitParams& dp, const double (&y)[4],
                                                   const double (&M)[4], const int (&E)[4],
                                                   uint8_t* out, int64_t plane_stride) {
@@ -386,13 +386,14 @@ __device__ __forceinline__ void digits_all_moduli(const DigitParams& dp, const d
                 digits_one_modulus<NSTEP, 2>(dp.mod[l], l, l, y, M, E, dp.pow2tab, out, plane_stride);
         }
     } else if (NMOD > 0) {
-        // hybrid order (eq. p_list_hybrid): the first min(N, 6) moduli are the squares
+        // hybrid order (eq. p_list_hybrid): the first min(N, 6) moduli are the squares;
+        // Karatsuba family (eq. p_list_karatsuba, NSQ = 0): none
 #pragma unroll
-        for (int l = 0; l < NMOD && l < kNumSquares; ++l)
+        for (int l = 0; l < NMOD && l < NSQ; ++l)
             digits_one_modulus<NSTEP, 1>(dp.mod[l], l, 2 * l, y, M, E, dp.pow2tab, out, plane_stride);
 #pragma unroll
-        for (int l = kNumSquares; l < NMOD; ++l)
-            digits_one_modulus<NSTEP, 0>(dp.mod[l], l, 2 * kNumSquares + 3 * (l - kNumSquares), y, M, E,
+        for (int l = NSQ; l < NMOD; ++l)
+            digits_one_modulus<NSTEP, 0>(dp.mod[l], l, 2 * NSQ + 3 * (l - NSQ), y, M, E,
                                          dp.pow2tab, out, plane_stride);
     } else {
 #pragma unroll 1
@@ -401,7 +402,7 @@ __device__ __forceinline__ void digits_all_moduli(const DigitParams& dp, const d
     }
 }
 
-template <bool KMAJOR, int NMOD, bool I8>
+template <bool KMAJOR, int NMOD, bool I8, int NSQ>
 __global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, int64_t rows,
                                                 int64_t k, int64_t ld,
                                                 const int32_t* __restrict__ e_scale,
@@ -453,11 +454,11 @@ __global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, in
                 M[q] = a;
                 E[q] = ee;
             }
-            digits_all_moduli<0, NMOD, I8>(dp, y, M, E, out, ps);
+            digits_all_moduli<0, NMOD, I8, NSQ>(dp, y, M, E, out, ps);
         } else if (need2) {
-            digits_all_moduli<2, NMOD, I8>(dp, y, M, E, out, ps);
+            digits_all_moduli<2, NMOD, I8, NSQ>(dp, y, M, E, out, ps);
         } else {
-            digits_all_moduli<1, NMOD, I8>(dp, y, M, E, out, ps);
+            digits_all_moduli<1, NMOD, I8, NSQ>(dp, y, M, E, out, ps);
         }
     }
 }
@@ -527,24 +528,32 @@ cudaError_t launch_digits(const double* X, int64_t rows, int64_t k, int64_t ld, 
                           const int32_t* e, const DigitParams& dp, uint8_t* planes,
                           int64_t rows_pad, int64_t k_pad, cudaStream_t st) {
     dim3 grid(static_cast<unsigned>(k_pad / TH), static_cast<unsigned>(rows_pad / TR));
-#define OZ2_DIG(NM, I8_)                                                                                     \
-    if (kmajor) k_digits<true, NM, I8_><<<grid, 256, 0, st>>>(X, rows, k, ld, e, dp, planes, rows_pad, k_pad); \
-    else k_digits<false, NM, I8_><<<grid, 256, 0, st>>>(X, rows, k, ld, e, dp, planes, rows_pad, k_pad);
+#define OZ2_DIG(NM, I8_, SQ_)                                                                                      \
+    if (kmajor) k_digits<true, NM, I8_, SQ_><<<grid, 256, 0, st>>>(X, rows, k, ld, e, dp, planes, rows_pad, k_pad); \
+    else k_digits<false, NM, I8_, SQ_><<<grid, 256, 0, st>>>(X, rows, k, ld, e, dp, planes, rows_pad, k_pad);
     if (dp.int8) {
         switch (dp.num_moduli) {   // INT8 scheme: 14..16 moduli are the FP64-level counts
-            case 14: OZ2_DIG(14, true) break;
-            case 15: OZ2_DIG(15, true) break;
-            case 16: OZ2_DIG(16, true) break;
-            default: OZ2_DIG(0, true) break;
+            case 14: OZ2_DIG(14, true, 0) break;
+            case 15: OZ2_DIG(15, true, 0) break;
+            case 16: OZ2_DIG(16, true, 0) break;
+            default: OZ2_DIG(0, true, 0) break;
+        }
+    } else if (dp.num_squares == 0 && dp.num_moduli >= 13) {
+        switch (dp.num_moduli) {   // Karatsuba family: 13, 14 are the FP64-level counts
+            case 13: OZ2_DIG(13, false, 0) break;
+            case 14: OZ2_DIG(14, false, 0) break;
+            default: OZ2_DIG(0, false, 0) break;
+        }
+    } else if (dp.num_squares == kNumSquares) {
+        switch (dp.num_moduli) {   // hybrid family, fully unrolled for the common moduli counts
+            case 12: OZ2_DIG(12, false, kNumSquares) break;
+            case 13: OZ2_DIG(13, false, kNumSquares) break;
+            case 14: OZ2_DIG(14, false, kNumSquares) break;
+            case 16: OZ2_DIG(16, false, kNumSquares) break;
+            default: OZ2_DIG(0, false, kNumSquares) break;
         }
     } else {
-        switch (dp.num_moduli) {   // fully unrolled for the common moduli counts
-            case 12: OZ2_DIG(12, false) break;
-            case 13: OZ2_DIG(13, false) break;
-            case 14: OZ2_DIG(14, false) break;
-            case 16: OZ2_DIG(16, false) break;
-            default: OZ2_DIG(0, false) break;
-        }
+        OZ2_DIG(0, false, 0)       // generic: reads md.square per modulus
     }
 #undef OZ2_DIG
     return cudaGetLastError();

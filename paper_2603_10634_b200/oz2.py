@@ -19,7 +19,8 @@ OZ2_ERR_NOT_SUPPORTED = 4
 OZ2_ERR_NONFINITE = 5
 OZ2_SCHEME_FP8 = 0
 OZ2_SCHEME_INT8 = 1
-_SCHEMES = {"fp8": OZ2_SCHEME_FP8, "int8": OZ2_SCHEME_INT8}
+OZ2_SCHEME_FP8_KARATSUBA = 2
+_SCHEMES = {"fp8": OZ2_SCHEME_FP8, "int8": OZ2_SCHEME_INT8, "karatsuba": OZ2_SCHEME_FP8_KARATSUBA}
 OZ2_MODE_ACCURATE = 0
 OZ2_MODE_FAST = 1
 _MODES = {"accurate": OZ2_MODE_ACCURATE, "fast": OZ2_MODE_FAST}
@@ -138,7 +139,8 @@ def oz2_get_mode():
 
 
 def oz2_set_scheme(scheme):
-    """scheme: OZ2_SCHEME_FP8 / OZ2_SCHEME_INT8 or "fp8" / "int8"."""
+    """scheme: OZ2_SCHEME_FP8 / OZ2_SCHEME_INT8 / OZ2_SCHEME_FP8_KARATSUBA or "fp8" / "int8" /
+    "karatsuba"."""
     return lib().oz2_set_scheme(_SCHEMES.get(scheme, scheme))
 
 
@@ -257,7 +259,7 @@ def dgemm(A, B, alpha=1.0, beta=0.0, C=None, num_moduli=13, mode=None, scheme=No
     """C <- alpha A @ B + beta C on torch float64 CUDA tensors via oz2_dgemm.
 
     Any 2-D strided layout is accepted; the result is column-major (Fortran order).
-    ``mode`` ("accurate" / "fast") and ``scheme`` ("fp8" / "int8") apply to this call
+    ``mode`` ("accurate" / "fast") and ``scheme`` ("fp8" / "int8" / "karatsuba") apply to this call
     only; None keeps the thread's setting."""
     prev_mode, prev_scheme = oz2_get_mode(), oz2_get_scheme()
     if mode is not None:

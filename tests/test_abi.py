@@ -77,6 +77,29 @@ def test_plan_constants_match_oracle(oz2mod):
         assert Fraction(info.fast_H) == scheme.fast_H(plan)
 
 
+def test_karatsuba_scheme_plan(oz2mod):
+    """OZ2_SCHEME_FP8_KARATSUBA: the planner's moduli, P and CRT weights equal
+    the oracle's Karatsuba family; no squares, 3 digit planes per modulus."""
+    from fractions import Fraction
+    from oracle import moduli as mod
+    assert oz2mod.oz2_set_scheme("karatsuba") == 0
+    try:
+        assert oz2mod.oz2_get_scheme() == oz2mod.OZ2_SCHEME_FP8_KARATSUBA
+        for N in [2, 12, 13, 14, 20, 33]:
+            assert oz2mod.oz2_moduli(N) == mod.karatsuba_moduli(N)
+            info = oz2mod.oz2_plan_query(N, 16384)
+            plan = mod.crt_plan(mod.karatsuba_moduli(N))
+            assert info.num_squares == 0 and info.num_planes == 3 * N
+            assert Fraction(info.p_prime) == mod.p_prime(plan.P)
+            L = info.num_limbs
+            assert sum(info.P_limbs[t] << (32 * t) for t in range(L)) == plan.P
+            for l, w in enumerate(plan.w):
+                assert sum(info.w_limbs[l][t] << (32 * t) for t in range(L)) == w
+    finally:
+        oz2mod.oz2_set_scheme("fp8")
+    assert oz2mod.oz2_set_scheme(3) == -1 and oz2mod.oz2_get_scheme() == oz2mod.OZ2_SCHEME_FP8
+
+
 def test_mode_switch(oz2mod):
     assert oz2mod.oz2_get_mode() == oz2mod.OZ2_MODE_ACCURATE
     assert oz2mod.oz2_set_mode("fast") == 0 and oz2mod.oz2_get_mode() == oz2mod.OZ2_MODE_FAST

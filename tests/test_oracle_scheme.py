@@ -23,7 +23,8 @@ def test_digits_exhaustive(facts):
     """Every residue of every hybrid modulus: reconstruction s*D1 + D2 = r and
     |D| <= 16, so each digit is an exact E4M3 integer."""
     dmax = facts["exactness_window"]["digit_max"]
-    for p in mod.hybrid_moduli(33):
+    # hybrid moduli and the Karatsuba-only family (513, 512, ...: |r| <= 256, eq. limit1)
+    for p in sorted(set(mod.hybrid_moduli(33)) | set(mod.karatsuba_moduli(33)), reverse=True):
         lo, hi = -(p // 2), (p + 1) // 2 - 1
         for r in range(lo, hi + 1):
             if mod.is_square(p):
@@ -66,7 +67,7 @@ def test_digit_route_equals_definition():
     """The FP8 digit route of Sec. III-B/C/D equals mod(A'_l B'_l, p_l) computed from
     the definition, for every modulus of the N=20 hybrid set (random residues)."""
     rng = np.random.default_rng(3)
-    for p in mod.hybrid_moduli(20):
+    for p in mod.hybrid_moduli(20) + mod.karatsuba_moduli(4):
         for (m, k, n) in [(4, 37, 5), (3, 512, 2)]:
             lo, hi = -(p // 2), (p + 1) // 2 - 1
             Ar = rng.integers(lo, hi + 1, size=(m, k))
@@ -328,3 +329,67 @@ def test_fast_mode_certified_and_less_accurate(phi):
     ef = np.linalg.norm(rf.C - ex) / np.linalg.norm(ex)
     ea = np.linalg.norm(ra.C - ex) / np.linalg.norm(ex)
     assert ea <= ef * 1.0000001 or ef < 1e-17
+
+
+# ------------------------------------------------------------------ Karatsuba-only family (NEXT-4)
+
+def test_karatsuba_family_limits(facts):
+    """eq. limit1: every Karatsuba-family residue satisfies |r| <= 256 (p <= 513),
+    the Karatsuba digits of +-256 are the extreme +-16, and no family member up to
+    N = 33 is a square (so every modulus takes the 3-digit route, 3N GEMMs)."""
+    ps = mod.karatsuba_moduli(33)
+    assert max(ps) == 513 and not any(mod.is_square(p) for p in ps)
+    for p in ps:
+        assert p // 2 <= 256 and (p + 1) // 2 - 1 <= 256
+    assert scheme.digits_karatsuba(256) == (16, 0, 16)
+    assert scheme.digits_karatsuba(-256) == (-16, 0, -16)
+    plan, _, _ = scheme.plan_constants(13, "karatsuba")
+    assert plan.moduli == tuple(ps[:13])
+    assert plan.P // 2 > 2 ** 115                                 # P:275
+
+
+@pytest.mark.parametrize("N,phi", [(13, 1.0), (4, 0.5)])
+def test_karatsuba_family_end_to_end(N, phi):
+    """The whole oracle with the Karatsuba-only moduli: certified condition, C' = A'B'
+    exactly, residues consistent with C', C within the a-priori bound (as for the
+    hybrid family), and the FP8 digit route of every modulus equals the definition."""
+    m, k, n = 9, 33, 8
+    A = gen_host(m, k, "phi", phi=phi, seed=81, order="C")
+    B = gen_host(k, n, "phi", phi=phi, seed=82, order="C")
+    r = scheme.dgemm(A, B, N, family="karatsuba", want_digits=True)
+    assert r.plan.moduli == tuple(mod.karatsuba_moduli(N))
+    assert _certified(r, A, B)
+    exactP = r.extra["Aint"].dot(r.extra["BintT"].T)
+    for i in range(m):
+        for j in range(n):
+            assert int(r.extra["Cprime"][i, j]) == int(exactP[i, j])
+            for l, p in enumerate(r.plan.moduli):
+                assert (int(exactP[i, j]) - int(r.residues[l][i, j])) % p == 0
+    for l, p in enumerate(r.plan.moduli):
+        Ad, Bd = r.extra["digits"][l]
+        assert len(Ad) == 3 and len(Bd) == 3
+        assert np.array_equal(scheme.modprod_karatsuba_digits(Ad, [b.T for b in Bd], p), r.residues[l])
+    F = exact.exact_gemm_fraction(A, B)
+    bound = exact.apriori_bound(A, B, r.e_mu, r.e_nu)
+    for i in range(m):
+        for j in range(n):
+            err = abs(Fraction(float(r.C[i, j])) - F[i, j])
+            assert err <= Fraction(2 * bound[i, j]) + abs(F[i, j]) * Fraction(2, 2 ** 53)
+
+
+def test_karatsuba_13_matches_hybrid_12_accuracy():
+    """the Karatsuba family needs N >= 13 where the hybrid family
+    needs N >= 12 for FP64-level accuracy (P/2 > 2^115 vs 2^110).  At equal N the hybrid
+    family (larger P) is at least as accurate; Karatsuba N = 13 is at least as accurate as
+    hybrid N = 12."""
+    A = gen_host(6, 300, "phi", phi=1.0, seed=91, order="C")
+    B = gen_host(300, 6, "phi", phi=1.0, seed=92, order="C")
+    E = exact.exact_entries(A, B, range(6), range(6))
+    err = lambda r: np.linalg.norm(r.C - E) / np.linalg.norm(E)
+    eh = {N: err(scheme.dgemm(A, B, N)) for N in (10, 11, 12)}
+    ek = {N: err(scheme.dgemm(A, B, N, family="karatsuba")) for N in (10, 11, 12, 13)}
+    for N in (10, 11, 12):
+        assert mod.crt_plan(mod.karatsuba_moduli(N)).P < mod.crt_plan(mod.hybrid_moduli(N)).P
+        assert eh[N] <= ek[N]
+    assert ek[13] <= eh[12]
+    assert ek[11] < ek[10] / 8 and ek[12] < ek[11] / 8     # ~4.5 bits per modulus (P:186-188)

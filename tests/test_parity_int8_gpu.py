@@ -192,4 +192,7 @@ def test_int8_16384_sampled(dev):
         pl), emu, enu)
     assert np.array_equal(C[I][:, J].cpu().numpy(), Cref)
     ex = exact.exact_entries(Ah, Bh, I, J)
-    assert np.linalg.norm(Cref - ex) / np.linalg.norm(ex) < 1e-15
+    # accuracy (not parity): INT8 N = 14 is "FP64 level" only approximately; at
+    # k = 16384 its normwise error is a few 1e-15 (bench int8 sweep: 5.3e-15; cuBLAS DGEMM
+    # 1.9e-15), so the bar is the same 2e-14 as the 4096-size test above
+    assert np.linalg.norm(Cref - ex) / np.linalg.norm(ex) < 2e-14
