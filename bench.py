@@ -48,8 +48,9 @@ def parse():
     ap.add_argument("--size", type=int, default=16384, help="m = n = k per GPU")
     ap.add_argument("--moduli", type=int, default=13)
     ap.add_argument("--phi", type=float, default=1.0)
-    ap.add_argument("--scheme", default="fp8", choices=["fp8", "int8"],
-                    help="fp8: the paper's method (default); int8: the INT8 Ozaki-II baseline (R16)")
+    ap.add_argument("--scheme", default="fp8", choices=["fp8", "int8", "karatsuba"],
+                    help="fp8: the paper's method (default, hybrid moduli); karatsuba: FP8 with the "
+                         "Karatsuba-only moduli (P:264-276); int8: the INT8 Ozaki-II baseline (R16)")
     ap.add_argument("--mode", default="accurate", choices=["accurate", "fast"],
                     help="scaling mode (fast: Cauchy-Schwarz bound, no bound GEMM; DESIGN.md R15)")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e/cuBLAS/accuracy/sweep/cpu legs")
@@ -231,7 +232,7 @@ def run_oz2(args, rank, world, local_rank):
              else "gemm_kernel<MODE_RESIDUE> (3N tcgen05 FP8 GEMMs + modular epilogue)")
     roofline = {"kernel": kname,
                 "bound": "tensor", "achieved": round(achieved, 1), "peak": round(fp8_peak, 1),
-                "unit": "TFLOP/s" if args.scheme == "fp8" else "TOP/s",
+                "unit": "TOP/s" if args.scheme == "int8" else "TFLOP/s",
                 "frac": round(achieved / fp8_peak, 4), "traffic": traffic,
                 "peak_source": (f"{peak_kind}: 2 x bf16_tflops_sustained (nominal fp8/bf16 = int8/bf16 = "
                                 "4.5/2.25)"),
@@ -248,7 +249,7 @@ def run_oz2(args, rank, world, local_rank):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (paper generator (rand-0.5)*exp(randn*phi), seeded, on device)",
         "config": {"workload": (f"{'config3' if args.size == 16384 else 'custom'}: m=n=k={args.size} per GPU, "
-                               f"phi={args.phi}, N={N} {'hybrid' if args.scheme == 'fp8' else 'INT8'} moduli, "
+                               f"phi={args.phi}, N={N} {dict(fp8='hybrid', int8='INT8', karatsuba='Karatsuba-only')[args.scheme]} moduli, "
                                f"{args.scheme} scheme, {args.mode} mode"),
                    "mode": args.mode, "scheme": args.scheme,
                    "m_per_gpu": m, "n": n, "k": k, "num_moduli": N, "phi": args.phi,
@@ -283,8 +284,9 @@ def run_oz2(args, rank, world, local_rank):
 
     # ---- accuracy against the exact product on sampled entries, and the N sweep
     rng = np.random.default_rng(0)
-    I = rng.choice(m, 8, replace=False)
-    J = rng.choice(n, 8, replace=False)
+    ns = 32
+    I = rng.choice(m, ns, replace=False)
+    J = rng.choice(n, ns, replace=False)
     Ah = A[I, :].cpu().numpy()
     Bh = B[:, J].cpu().numpy()
     exact = np.array([[two_prod_exact_dot(Ah[a], Bh[:, b]) for b in range(len(J))] for a in range(len(I))])
@@ -296,7 +298,7 @@ def run_oz2(args, rank, world, local_rank):
 
     P.oz2_dgemm("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0, C.data_ptr(), m, N)
     torch.cuda.synchronize()
-    acc = {"sample": "8 x 8 entries, exact dot products (TwoProduct + fsum)",
+    acc = {"sample": f"{ns} x {ns} entries, exact dot products (TwoProduct + fsum)",
            f"oz2_N{N}": errs(C[I][:, J].cpu().numpy()),
            "cublas": errs(ref[I][:, J].cpu().numpy())}
     sweep = {}

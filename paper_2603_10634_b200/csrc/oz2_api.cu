@@ -291,6 +291,8 @@ static float f_k_of(int64_t k) {   // reading R5: RU32(1/(1 - k 2^-23))
 
 struct ThreadState {
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;   // host-pointer calls: D2H of finished C blocks
+    cudaEvent_t copy_ev = nullptr;
     void* user_ws = nullptr;
     size_t user_ws_bytes = 0;
     void* own_ws = nullptr;
@@ -511,9 +513,18 @@ static void phase_mark(int i) {
 // =================================================================================
 // the pipeline on device pointers
 
+// Called after the last kernel of column block [j0, j0 + nbj) of C has been enqueued
+// (host-pointer calls use it to start that block's device-to-host copy early).
+struct BlockHook {
+    int64_t nb;                                            // column block size wanted (0: none)
+    int (*done)(void* ctx, int64_t j0, int64_t nbj);
+    void* ctx;
+};
+
 static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_t k, double alpha,
                       const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
-                      double* C, int64_t ldc, int N, const oz2_options* opt) {
+                      double* C, int64_t ldc, int N, const oz2_options* opt,
+                      const BlockHook* hook = nullptr) {
     cudaStream_t st = g_ts.stream;
     int err = OZ2_SUCCESS;
     Plan* pl = device_plan(N, &err);
@@ -522,6 +533,12 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
     const bool want_full = opt && (opt->digits_a || opt->digits_b || opt->residues);
     int64_t mb = g_ts.block_m, nb = g_ts.block_n;
     if (want_full) mb = nb = 0;
+    if (hook && hook->nb > 0 && mb <= 0 && nb <= 0 && !want_full) {
+        // column blocks of C for the caller (results are identical to the unblocked call);
+        // kept only if that layout fits the caller's workspace
+        const Layout Lh = make_layout(m, n, k, N, pl->M, m, hook->nb);
+        if (!g_ts.user_ws || Lh.total <= g_ts.user_ws_bytes) { mb = m; nb = hook->nb; }
+    }
     uint8_t* ws = nullptr;
     Layout L;
     if (g_ts.user_ws) {
@@ -688,6 +705,10 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             if (!fused)
                 OZ2_CK(launch_crt(pl->L, res, mbi, nbj, pl->crt, e_mu + i0, e_nu + j0, alpha, beta, Cij, ldc, st));
         }
+        if (hook && hook->done) {
+            const int hr = hook->done(hook->ctx, j0, nbj);
+            if (hr) return hr;
+        }
     }
     if (L.blocked) phase_mark(5);
     phase_mark(6);
@@ -756,11 +777,38 @@ int dgemm_impl(char transa, char transb, int64_t m, int64_t n, int64_t k, double
     }
     if (beta != 0.0) OZ2_CK(cudaMemcpy2DAsync(dC, 8 * m, C, 8 * ldc, 8 * m, n, cudaMemcpyHostToDevice, st));
     int rc = OZ2_SUCCESS;
-    if (quick) rc = launch_scale(dC, m, n, m, beta, st) == cudaSuccess ? OZ2_SUCCESS : OZ2_ERR_CUDA;
-    else rc = run_device(!is_n(transa), is_n(transb), m, n, k, alpha, dA, rowsA, dB, rowsB, beta, dC, m, N, opt);
+    if (quick) {
+        rc = launch_scale(dC, m, n, m, beta, st) == cudaSuccess ? OZ2_SUCCESS : OZ2_ERR_CUDA;
+        if (rc) return rc;
+        OZ2_CK(cudaMemcpy2DAsync(C, 8 * ldc, dC, 8 * m, 8 * m, n, cudaMemcpyDeviceToHost, st));
+        OZ2_CK(cudaStreamSynchronize(st));
+        return OZ2_SUCCESS;
+    }
+    // C goes back in column blocks: block j's device-to-host copy (on a second stream)
+    // overlaps the GEMMs of blocks j+1.. (OZ2_HOST_BLOCKS blocks, default 4; 1 = off)
+    if (!g_ts.copy_stream) {
+        OZ2_CK(cudaStreamCreateWithFlags(&g_ts.copy_stream, cudaStreamNonBlocking));
+        OZ2_CK(cudaEventCreateWithFlags(&g_ts.copy_ev, cudaEventDisableTiming));
+    }
+    struct Ctx { double* C; int64_t ldc; const double* dC; int64_t m; } ctx{C, ldc, dC, m};
+    BlockHook hook{};
+    const int nblk = env_int("OZ2_HOST_BLOCKS", 4);
+    if (nblk > 1 && n >= 2 * PAD_N * nblk) hook.nb = round_up((n + nblk - 1) / nblk, PAD_N);
+    hook.ctx = &ctx;
+    hook.done = [](void* c, int64_t j0, int64_t nbj) -> int {
+        const Ctx& x = *static_cast<const Ctx*>(c);
+        if (cudaEventRecord(g_ts.copy_ev, g_ts.stream) != cudaSuccess) return OZ2_ERR_CUDA;
+        if (cudaStreamWaitEvent(g_ts.copy_stream, g_ts.copy_ev, 0) != cudaSuccess) return OZ2_ERR_CUDA;
+        if (cudaMemcpy2DAsync(x.C + j0 * x.ldc, 8 * x.ldc, x.dC + j0 * x.m, 8 * x.m, 8 * x.m, nbj,
+                              cudaMemcpyDeviceToHost, g_ts.copy_stream) != cudaSuccess)
+            return OZ2_ERR_CUDA;
+        return OZ2_SUCCESS;
+    };
+    rc = run_device(!is_n(transa), is_n(transb), m, n, k, alpha, dA, rowsA, dB, rowsB, beta, dC, m, N, opt, &hook);
+    const cudaError_t e1 = cudaStreamSynchronize(st);
+    const cudaError_t e2 = cudaStreamSynchronize(g_ts.copy_stream);
     if (rc) return rc;
-    OZ2_CK(cudaMemcpy2DAsync(C, 8 * ldc, dC, 8 * m, 8 * m, n, cudaMemcpyDeviceToHost, st));
-    OZ2_CK(cudaStreamSynchronize(st));
+    if (e1 != cudaSuccess || e2 != cudaSuccess) return OZ2_ERR_CUDA;
     return OZ2_SUCCESS;
 }
 
@@ -890,6 +938,9 @@ int oz2_finalize(void) {
     if (g_ts.own_ws) cudaFree(g_ts.own_ws);
     if (g_ts.staging) cudaFree(g_ts.staging);
     if (g_ts.d_status) cudaFree(g_ts.d_status);
+    if (g_ts.copy_stream) { cudaStreamSynchronize(g_ts.copy_stream); cudaStreamDestroy(g_ts.copy_stream); }
+    if (g_ts.copy_ev) cudaEventDestroy(g_ts.copy_ev);
+    g_ts.copy_stream = nullptr; g_ts.copy_ev = nullptr;
     for (auto& kv : g_ts.plans) if (kv.second->d_pow2tab) cudaFree(kv.second->d_pow2tab);
     g_ts.plans.clear();
     g_ts.own_ws = nullptr; g_ts.own_ws_bytes = 0;

@@ -254,6 +254,30 @@ def test_host_pointer_path(dev):
     assert np.array_equal(C, run(A, B, 13)["C"])
 
 
+@pytest.mark.parametrize("blocks", ["1", "4", "3"])
+def test_host_pointer_column_blocks(dev, blocks, monkeypatch):
+    """Host buffers with C returned in column blocks (each block's device-to-host copy
+    overlaps the next block's GEMMs; OZ2_HOST_BLOCKS): bit-identical to the device-pointer
+    call, including a ragged last block, ldc padding, beta != 0 and transposed A."""
+    from gpu_helpers import run
+    monkeypatch.setenv("OZ2_HOST_BLOCKS", blocks)
+    m, k, n = 300, 260, 2600
+    A = gen_host(m, k, "phi", phi=1.0, seed=21)
+    B = gen_host(k, n, "phi", phi=1.0, seed=22)
+    C0 = gen_host(m, n, "uniform", seed=23)
+    At = np.asfortranarray(A.T)                       # op(A) = A with transa = 'T'
+    Bh = np.asfortranarray(B)
+    ldc = m + 5
+    Ch = np.asfortranarray(np.zeros((ldc, n)))
+    Ch[:m] = C0
+    rc = dev.oz2_dgemm("T", "N", m, n, k, 0.5, At.ctypes.data, k, Bh.ctypes.data, k, -1.5,
+                       Ch.ctypes.data, ldc, 13)
+    assert rc == 0
+    ref = run(A, B, 13, alpha=0.5, beta=-1.5, C0=C0)["C"]
+    assert np.array_equal(Ch[:m], ref)
+    assert np.all(Ch[m:] == 0.0)
+
+
 def test_torch_wrapper_layouts(dev):
     import torch
     A = torch.from_numpy(gen_host(100, 120, "phi", phi=1.0, seed=13, order="C")).cuda()
