@@ -215,6 +215,7 @@ static Plan build_plan(int N, int family) {
     dp.num_planes = pl.M;
     dp.int8 = i8 ? 1 : 0;
     dp.num_squares = pl.nsq;
+    dp.even_index = -1;
     {
         int pmin = pl.p[0];
         for (int p : pl.p) pmin = p < pmin ? p : pmin;
@@ -231,6 +232,12 @@ static Plan build_plan(int N, int family) {
         md.pinv_f = 1.0f / static_cast<float>(p);
         md.hp_f = (p % 2 == 0) ? 0.5f / static_cast<float>(p) : 0.0f;
         md.h_f = (p % 2 == 0) ? 0.5f : 0.0f;
+        {   // paired residue constants: Q = p_l p_(l+1) <= 1089 * 1024 < 2^21 (exact in FP64)
+            const double q2 = (l % 2 == 0 && l + 1 < N) ? static_cast<double>(p) * pl.p[l + 1] : static_cast<double>(p);
+            md.q2_d = q2;
+            md.q2inv_d = 1.0 / q2;
+        }
+        if (p % 2 == 0) dp.even_index = l;
         {   // smod(2^(8i), p) in [-floor(p/2), ceil(p/2) - 1]
             int64_t v = 1;
             for (int i = 0; i < 8; ++i) {

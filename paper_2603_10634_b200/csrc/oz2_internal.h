@@ -93,6 +93,8 @@ struct ModDig {
     float w8[8];                 // smod(2^(8i), p) as floats: byte-chunk weights
     int square;
     int plane0;                  // first digit plane of this modulus
+    double q2_d, q2inv_d;        // paired residues (k_digits, |X'| < lim1): Q = p_l p_(l+1)
+                                 // for even l < N-1 (else Q = p_l), and RN(1/Q)
 };
 
 struct DigitParams {
@@ -100,6 +102,7 @@ struct DigitParams {
     int num_planes;
     int int8;                    // 1: INT8 scheme (one S8 residue plane per modulus)
     int num_squares;             // FP8: leading square moduli (hybrid min(N, 6), Karatsuba 0)
+    int even_index;              // index of the (single, by coprimality) even modulus, or -1
     // reduction-depth limits on |X'|: the 1.5 2^52 rounding trick needs |q| <= 2^51, so
     // one FP64 step serves |X'| < 2^50 p_min and the p 2^36 pre-reduction |X'| < 2^86 p_min
     double lim1, lim2;

@@ -275,6 +275,10 @@ __device__ __forceinline__ double dfma_rn(double a, double b, double c) {   // k
 // 1.5 2^52 magic-number rounding is exact.
 // SQ: 1 square, 0 non-square, -1 read md.square at run time, 2 INT8 scheme (the residue
 // itself, as a two's-complement byte, is the single operand plane of the modulus)
+template <int SQ>
+__device__ __forceinline__ void emit_digits(const ModDig& md, const float (&rf)[4], uint8_t* o,
+                                            int64_t plane_stride);
+
 template <int NSTEP, int SQ>
 __device__ __forceinline__ void digits_one_modulus(const ModDig& md, int l, int plane0, const double (&y)[4],
                                                    const double (&M)[4], const int (&E)[4],
@@ -322,7 +326,14 @@ __device__ __forceinline__ void digits_one_modulus(const ModDig& md, int l, int 
             rf[q + 1] = rs.y;
         }
     }
-    uint8_t* o = out + static_cast<int64_t>(plane0) * plane_stride;
+    emit_digits<SQ>(md, rf, out + static_cast<int64_t>(plane0) * plane_stride, plane_stride);
+}
+
+// the digit planes (or the INT8 residue plane) of one modulus from the exact symmetric
+// residues rf[4] of the lane's 4 elements
+template <int SQ>
+__device__ __forceinline__ void emit_digits(const ModDig& md, const float (&rf)[4], uint8_t* o,
+                                            int64_t plane_stride) {
     if (SQ == 2) {
         uint32_t w = 0;
 #pragma unroll
@@ -402,6 +413,58 @@ __device__ __forceinline__ void digits_all_moduli(const DigitParams& dp, const d
     }
 }
 
+// The common case |X'| < 2^50 p_min with the moduli taken in pairs: ONE FP64 reduction
+// modulo Q = p_l p_(l+1) (< 2^21; Q = p_l for a last odd one out) -- |y/Q| < 2^50, so the
+// magic-number quotient is round(y/Q) of an argument within 2^-3 of y/Q and
+// |r_Q| = |y - qQ| < Q (1/2 + 2^-3) < 2^21 is exact -- then each modulus' symmetric residue
+// (R2) in ONE FP32 step r = r_Q - p rint((r_Q + h)/p), h = 1/2 for the even modulus (index
+// EVEN), else 0: the computed quotient is within 2^-3/p of (r_Q + h)/p, which is never
+// closer than 1/(2p) to a half-integer, so the rounding is exact.  Bit-identical to
+// digits_one_modulus<1, .> (same residues, same digit code).
+template <int NMOD, bool I8, int NSQ, int EVEN>
+__device__ __forceinline__ void digits_paired(const DigitParams& dp, const double (&y)[4], uint8_t* out,
+                                              int64_t plane_stride) {
+    const float2 M2 = make_float2(kMagic23, kMagic23), nM2 = make_float2(-kMagic23, -kMagic23);
+#pragma unroll
+    for (int l = 0; l < NMOD; l += 2) {
+        const double Q = dp.mod[l].q2_d, Qi = dp.mod[l].q2inv_d, magic = kMagic52;
+        float rq[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double qq = dfma_rn(y[q], Qi, magic) - magic;
+            const double rd = fma(-qq, Q, y[q]);                             // exact, |rd| < 2^21
+            rq[q] = __int_as_float(0x4B400000 + __double2loint(rd + magic));  // r_Q + 1.5 2^23
+        }
+        const float2 ra = __fadd2_rn(make_float2(rq[0], rq[1]), nM2);
+        const float2 rb = __fadd2_rn(make_float2(rq[2], rq[3]), nM2);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int lm = l + u;
+            if (lm >= NMOD) break;
+            const ModDig& md = dp.mod[lm];
+            const float2 pi2 = make_float2(md.pinv_f, md.pinv_f), np2 = make_float2(-md.p_f, -md.p_f);
+            float rf[4];
+            {
+                const float2 xa = (lm == EVEN) ? __fadd2_rn(ra, make_float2(0.5f, 0.5f)) : ra;
+                const float2 xb = (lm == EVEN) ? __fadd2_rn(rb, make_float2(0.5f, 0.5f)) : rb;
+                const float2 qa = __fadd2_rn(__ffma2_rn(xa, pi2, M2), nM2);
+                const float2 qb = __fadd2_rn(__ffma2_rn(xb, pi2, M2), nM2);
+                const float2 sa = __ffma2_rn(qa, np2, ra);
+                const float2 sb = __ffma2_rn(qb, np2, rb);
+                rf[0] = sa.x; rf[1] = sa.y; rf[2] = sb.x; rf[3] = sb.y;
+            }
+            if (I8) {
+                emit_digits<2>(md, rf, out + static_cast<int64_t>(lm) * plane_stride, plane_stride);
+            } else if (lm < NSQ) {
+                emit_digits<1>(md, rf, out + static_cast<int64_t>(2 * lm) * plane_stride, plane_stride);
+            } else {
+                emit_digits<0>(md, rf, out + static_cast<int64_t>(2 * NSQ + 3 * (lm - NSQ)) * plane_stride,
+                               plane_stride);
+            }
+        }
+    }
+}
+
 template <bool KMAJOR, int NMOD, bool I8, int NSQ>
 __global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, int64_t rows,
                                                 int64_t k, int64_t ld,
@@ -457,6 +520,8 @@ __global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, in
             digits_all_moduli<0, NMOD, I8, NSQ>(dp, y, M, E, out, ps);
         } else if (need2) {
             digits_all_moduli<2, NMOD, I8, NSQ>(dp, y, M, E, out, ps);
+        } else if (NMOD > 0) {
+            digits_paired<NMOD, I8, NSQ, I8 ? 0 : 1>(dp, y, out, ps);   // the even modulus: 256 / 1024 / 512
         } else {
             digits_all_moduli<1, NMOD, I8, NSQ>(dp, y, M, E, out, ps);
         }
@@ -531,7 +596,10 @@ cudaError_t launch_digits(const double* X, int64_t rows, int64_t k, int64_t ld, 
 #define OZ2_DIG(NM, I8_, SQ_)                                                                                      \
     if (kmajor) k_digits<true, NM, I8_, SQ_><<<grid, 256, 0, st>>>(X, rows, k, ld, e, dp, planes, rows_pad, k_pad); \
     else k_digits<false, NM, I8_, SQ_><<<grid, 256, 0, st>>>(X, rows, k, ld, e, dp, planes, rows_pad, k_pad);
-    if (dp.int8) {
+    if (dp.even_index != (dp.int8 ? 0 : 1)) {
+        // generic (never for the planner's families, whose even modulus is 256 / 1024 / 512)
+        if (dp.int8) { OZ2_DIG(0, true, 0) } else { OZ2_DIG(0, false, 0) }
+    } else if (dp.int8) {
         switch (dp.num_moduli) {   // INT8 scheme: 14..16 moduli are the FP64-level counts
             case 14: OZ2_DIG(14, true, 0) break;
             case 15: OZ2_DIG(15, true, 0) break;
