@@ -168,7 +168,9 @@ def run_oz2(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     P.oz2_set_stream(stream.cuda_stream)
     P.oz2_set_scheme(args.scheme)
-    ws_bytes = max(P.oz2_workspace_size("N", "N", m, n, k, N), P.oz2_workspace_size("N", "N", m, n, k, 16))
+    ws_bytes = P.oz2_workspace_size("N", "N", m, n, k, N)
+    if not args.no_extras:       # room for the moduli sweeps of the extras (N up to 16)
+        ws_bytes = max(ws_bytes, P.oz2_workspace_size("N", "N", m, n, k, 16))
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
     P.oz2_set_workspace(ws.data_ptr(), ws.numel())
     if P.oz2_set_mode(args.mode) != 0 or P.oz2_set_scheme(args.scheme) != 0:

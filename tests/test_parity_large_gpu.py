@@ -136,3 +136,64 @@ def test_config4_large_k_65536_fast_mode(dev):
     I, J = [0, 2048, 4095], [7, 4000]
     out = _run_sampled(dev, 4096, 65536, 4096, 13, 4.0, 31, I, J, mode="fast")
     _check(out, 13, I, J, mode="fast")
+
+
+def _run_fast_light(P, m, k, n, N, phi, seed, I, J, rows=None):
+    """Fast mode without debug outputs (the bench's launch configuration, whatever blocking
+    the library picks); returns the sampled rows/columns of A, B and C.  rows = (r0, r1)
+    runs only that row block of A (a rank's shard of the row-sharded driver)."""
+    import torch
+    A = gen_device(m, k, "phi", phi=phi, seed=seed)
+    B = gen_device(k, n, "phi", phi=phi, seed=seed + 1)
+    r0, r1 = rows if rows else (0, m)
+    mm = r1 - r0
+    C = torch.empty((n, mm), dtype=torch.float64, device="cuda").t()
+    P.oz2_set_stream(torch.cuda.current_stream().cuda_stream)
+    P.oz2_set_workspace(None, 0)
+    assert P.oz2_set_mode("fast") == 0
+    try:
+        rc = P.oz2_dgemm("N", "N", mm, n, k, 1.0, A[r0:].data_ptr(), m, B.data_ptr(), k, 0.0,
+                         C.data_ptr(), mm, N)
+    finally:
+        P.oz2_set_mode("accurate")
+    assert rc == 0
+    torch.cuda.synchronize()
+    It = torch.tensor([i - r0 for i in I], device="cuda")
+    Jt = torch.tensor(J, device="cuda")
+    out = {"C": C[It][:, Jt].cpu().numpy(), "A_rows": A[torch.tensor(I, device="cuda")].cpu().numpy(),
+           "B_cols": B[:, Jt].cpu().numpy()}
+    del A, B, C
+    torch.cuda.empty_cache()
+    P.oz2_finalize()
+    return out
+
+
+def _check_light(out, N, nI, nJ):
+    Ar, Bc = out["A_rows"], out["B_cols"]
+    emu, enu = _fast_exps(Ar, list(range(nI)), N), _fast_exps(Bc.T.copy(), list(range(nJ)), N)
+    _, Cref = scheme.entries(Ar, Bc, N, list(range(nI)), list(range(nJ)), list(emu), list(enu))
+    assert np.array_equal(out["C"], Cref)
+    ex = exact.exact_entries(Ar, Bc, range(nI), range(nJ))
+    bound = exact.apriori_bound(Ar, Bc, list(emu), list(enu))
+    assert np.all(np.abs(out["C"] - ex) <= 2 * bound + np.abs(ex) * 2.0 ** -52)
+    return float(np.linalg.norm(out["C"] - ex) / np.linalg.norm(ex))
+
+
+def test_config5_32768_fast_sampled(dev):
+    """BASELINE config 5's problem (m=n=k=32768, N=13) on one B200 in fast mode (both
+    scaling vectors row/column-local, R15): sampled C bit-exact against the oracle."""
+    I, J = [0, 20000, 32767], [5, 32760]
+    out = _run_fast_light(dev, 32768, 32768, 32768, 13, 1.0, 41, I, J)
+    assert _check_light(out, 13, len(I), len(J)) < 1e-15
+
+
+def test_config5_rank_shard_fast_equals_unsharded(dev):
+    """One rank's shard of the row-sharded driver (rows [8192, 16384) of a G=4 split): in
+    fast mode mu and nu are row/column-local, so the shard's C equals the same rows of
+    the unsharded call bit for bit (in accurate mode nu is block-local instead, R13)."""
+    m = n = k = 8192 * 2
+    I, J = [8192, 12000, 16383], [3, 16000]
+    shard = _run_fast_light(dev, m * 2, k, n, 13, 1.0, 43, I, J, rows=(8192, 16384))
+    full = _run_fast_light(dev, m * 2, k, n, 13, 1.0, 43, I, J)
+    assert np.array_equal(shard["C"], full["C"])
+    _check_light(full, 13, len(I), len(J))
