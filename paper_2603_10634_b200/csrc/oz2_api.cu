@@ -130,6 +130,8 @@ struct Plan {
     std::vector<Big> w;
 };
 
+static int env_int(const char* name, int dflt);
+
 static Plan build_plan(int N, int family) {
     Plan pl;
     pl.N = N;
@@ -266,9 +268,18 @@ static Plan build_plan(int N, int family) {
             plane += 1;
         } else if (md.square) {
             // C'_l = mod(s A1 B2 + s A2 B1 + A2 B2, p)  (eq. 3matmult-notKaratsuba)
-            me.coef[0] = static_cast<float>(s); me.a_plane[0] = plane + 0; me.b_plane[0] = plane + 1;
-            me.coef[1] = static_cast<float>(s); me.a_plane[1] = plane + 1; me.b_plane[1] = plane + 0;
-            me.coef[2] = 1.0f;                  me.a_plane[2] = plane + 1; me.b_plane[2] = plane + 1;
+            if (env_int("OZ2_SQ_ORDER", 1) == 1) {
+                // A1 B2, A2 B2, A2 B1: consecutive products share B2, then A2, so their
+                // operand panels are still in L2 (residue-GEMM DRAM reads 187 -> 178 GB at
+                // 16384^3, N = 13); OZ2_SQ_ORDER=0 restores the order of the equation
+                me.coef[0] = static_cast<float>(s); me.a_plane[0] = plane + 0; me.b_plane[0] = plane + 1;
+                me.coef[1] = 1.0f;                  me.a_plane[1] = plane + 1; me.b_plane[1] = plane + 1;
+                me.coef[2] = static_cast<float>(s); me.a_plane[2] = plane + 1; me.b_plane[2] = plane + 0;
+            } else {
+                me.coef[0] = static_cast<float>(s); me.a_plane[0] = plane + 0; me.b_plane[0] = plane + 1;
+                me.coef[1] = static_cast<float>(s); me.a_plane[1] = plane + 1; me.b_plane[1] = plane + 0;
+                me.coef[2] = 1.0f;                  me.a_plane[2] = plane + 1; me.b_plane[2] = plane + 1;
+            }
             plane += 2;
         } else {
             // A'B' = 256 C1 + C2 + 16 (C3 - C1 - C2)  (eq. C'-Karatsuba)

@@ -1,0 +1,4 @@
+#!/bin/bash
+for O in 0 1 0 1; do echo "order=$O"; OZ2_SQ_ORDER=$O timeout 300 python tools/profile_once.py 16384 13 5 | tail -3; done > gpurun_out/sq_order.log 2>&1
+for O in 0 1; do OZ2_SQ_ORDER=$O timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,sm__cycles_elapsed.avg.per_second,lts__t_sector_hit_rate.pct --clock-control none -k regex:"gemm_kernel<0" -c 1 --csv python tools/profile_once.py 16384 13 1 > gpurun_out/sq_order_ncu_$O.csv 2>&1; done
+echo done
