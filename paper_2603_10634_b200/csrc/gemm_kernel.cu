@@ -207,7 +207,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     // the epilogue reduces each segment mod p and accumulates the residue (NEXT-2)
     const int nseg = (MODE == MODE_RESIDUE) ? P.num_kseg : 1;
     const int kseg = (MODE == MODE_RESIDUE) ? P.kseg_blocks : nkb;
-    const int prods = (MODE == MODE_RESIDUE) ? NP * P.num_moduli * nseg : 1;
+    // work items: a tile with all its moduli (tile-major, the default), or -- mod_split,
+    // for grids with few tiles -- one (tile, modulus) pair, modulus-major over the tiles so
+    // that concurrently running units share that modulus' operand panels; the residue of
+    // every modulus is independent, only the (then separate) CRT needs them all
+    const int mod_split = (MODE == MODE_RESIDUE) ? P.mod_split : 0;
+    const int num_items = mod_split ? num_tiles * P.num_moduli : num_tiles;
+    const int mods_per_item = (MODE == MODE_RESIDUE) ? (mod_split ? 1 : P.num_moduli) : 0;
+    const int prods = (MODE == MODE_RESIDUE) ? NP * mods_per_item * nseg : 1;
     const int unit = blockIdx.x / CS;            // tile-processing unit (cluster)
     const int units = gridDim.x / CS;
 
@@ -222,7 +229,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             const long long chunks_per_prod = (nkb + kc - 1) / kc;
             const uint32_t full0 = smem_u32(&full[0]) & 0xFEFFFFFFu;   // pair leader's barrier (TMA operand)
             const uint32_t full_leader = (CS > 1) ? mapa_shared(smem_u32(&full[0]), crank & ~(CG - 1u)) : 0u;
-            for (int tile = unit; tile < num_tiles; tile += units) {
+            for (int it = unit; it < num_items; it += units) {
+                const int tile = mod_split ? it % num_tiles : it;
+                const int l0 = mod_split ? it / num_tiles : 0;
                 int tm, tn;
                 tile_coords<16 / CG>(tile, P.m_tiles, n_super, tm, tn);
                 tn = tn * MC + static_cast<int>(pairi);
@@ -231,7 +240,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     int b_row = tn * BN + static_cast<int>(rank) * Cfg::B_ROWS;
                     int kb0 = 0, kb1 = nkb;
                     if (MODE == MODE_RESIDUE) {
-                        const int l = pr / (NP * nseg), rem = pr - l * NP * nseg;
+                        const int lr = pr / (NP * nseg), rem = pr - lr * NP * nseg;
+                        const int l = l0 + lr;
                         const int x = rem / nseg, seg = rem - x * nseg;
                         a_row += P.mod[l].a_plane[x] * P.rows_per_plane_a;
                         b_row += P.mod[l].b_plane[x] * P.rows_per_plane_b;
@@ -284,7 +294,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             }
             if (P.sync_lead > 0 && crank == 0) {
                 // finished: count as having started every product so nobody waits on us
-                const long long gmax = static_cast<long long>((num_tiles + units - 1) / units) * prods * chunks_per_prod;
+                const long long gmax = static_cast<long long>((num_items + units - 1) / units) * prods * chunks_per_prod;
                 if (gmax > g) atomicAdd(P.progress, static_cast<unsigned long long>(gmax - g));
             }
         }
@@ -294,7 +304,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             constexpr uint32_t idesc = I8 ? make_idesc_i8_s32(Cfg::TILE_M, BN, MODE != MODE_BOUND)
                                           : make_idesc_e4m3_f32(Cfg::TILE_M, BN);
             uint32_t stage = 0, phase = 0, g = 0;
-            for (int tile = unit; tile < num_tiles; tile += units) {
+            for (int it = unit; it < num_items; it += units) {
                 for (int pr = 0; pr < prods; ++pr, ++g) {
                     const uint32_t slot = g & 1u, use = g >> 1;
                     mbar_wait(&tempty[slot], (use & 1u) ^ 1u);
@@ -365,7 +375,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             }
         };
         uint32_t g = 0;
-        for (int tile = unit; tile < num_tiles; tile += units) {
+        for (int it = unit; it < num_items; it += units) {
+            const int tile = mod_split ? it % num_tiles : it;
+            const int l0 = mod_split ? it / num_tiles : 0;
             int tm, tn;
             tile_coords<16 / CG>(tile, P.m_tiles, n_super, tm, tn);
             tn = tn * MC + static_cast<int>(pairi);
@@ -373,7 +385,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             const int64_t col0 = static_cast<int64_t>(tn) * BN + half * 128u;
             const bool row_ok = row < P.m;
             if (MODE == MODE_RESIDUE) {
-                for (int l = 0; l < P.num_moduli; ++l) {
+                for (int l = l0; l < l0 + mods_per_item; ++l) {
                     const float p = P.mod[l].p, pinv = P.mod[l].pinv, w16 = P.mod[l].w16;
                     // running partial sum_x coef_x r_x, reduced mod p after every product
                     // (|.| <= p/2 + 1 <= 546), held exactly in binary16 pairs
@@ -510,6 +522,8 @@ static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, cons
     constexpr int CS = CG * MC;
     const int num_tiles = gp.m_tiles * (gp.n_tiles / MC);
     if (num_tiles == 0) return cudaSuccess;
+    const int num_items = (MODE == MODE_RESIDUE || MODE == MODE_RESIDUE_I8) && gp.mod_split
+                              ? num_tiles * gp.num_moduli : num_tiles;
     static int max_clusters = 0;               // co-resident clusters of this configuration
     if (!attr_set) {
         cudaError_t err = cudaFuncSetAttribute(gemm_kernel<MODE, CG, FL, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -542,7 +556,7 @@ static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, cons
     // throttle assumes every unit runs concurrently)
     int max_units = num_sms / CS;
     if (max_clusters < max_units) max_units = max_clusters;
-    const int units = num_tiles < max_units ? num_tiles : max_units;
+    const int units = num_items < max_units ? num_items : max_units;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(units * CS);
     cfg.blockDim = dim3(GEMM_THREADS);

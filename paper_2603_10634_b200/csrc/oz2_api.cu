@@ -699,6 +699,13 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             gp.m_tiles = static_cast<int>(mbi_pad / tile_m(cg)); gp.n_tiles = static_cast<int>(nbj_pad / BN);
             gp.rows_per_plane_a = static_cast<int>(mbi_pad); gp.rows_per_plane_b = static_cast<int>(nbj_pad);
             gp.num_moduli = N;
+            {   // few tiles (< 8 per persistent unit): one work item per (tile, modulus)
+                const int64_t tiles = static_cast<int64_t>(gp.m_tiles) * gp.n_tiles;
+                const int64_t units = g_ts.num_sms / (cg == 1 ? 1 : 2);
+                const int ms = env_int("OZ2_MOD_SPLIT", -1);
+                gp.mod_split = (ms >= 0) ? (ms > 0 ? 1 : 0) : (tiles < 8 * units ? 1 : 0);
+            }
+            const int fused_blk = gp.mod_split ? 0 : fused;      // the CRT needs every modulus of a tile
             gp.residues = res;
             gp.sync_lead = sync_lead();
             gp.sync_chunk = sync_chunk;
@@ -707,20 +714,20 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
                 OZ2_CK(cudaMemsetAsync(gp.progress, 0, 8, st));
             }
             double* Cij = C + i0 + j0 * ldc;
-            if (fused) {
+            if (fused_blk) {
                 gp.crt = pl->crt;
                 gp.e_mu = e_mu + i0; gp.e_nu = e_nu + j0;
                 gp.alpha = alpha; gp.beta = beta;
                 gp.C = Cij; gp.ldc = ldc;
             }
-            OZ2_CK(launch_gemm(i8 ? MODE_RESIDUE_I8 : MODE_RESIDUE, cg, fused, ta, tb, gp, g_ts.num_sms, st));
+            OZ2_CK(launch_gemm(i8 ? MODE_RESIDUE_I8 : MODE_RESIDUE, cg, fused_blk, ta, tb, gp, g_ts.num_sms, st));
             if (!L.blocked) {
                 if (opt && opt->residues)
                     OZ2_CK(cudaMemcpyAsync(opt->residues, res, 2ull * N * m * n, cudaMemcpyDeviceToDevice, st));
                 phase_mark(5);
             }
             // ---- step 6: CRT + inverse scaling (eqs. CRT_finalreduction, inversescaling)
-            if (!fused)
+            if (!fused_blk)
                 OZ2_CK(launch_crt(pl->L, res, mbi, nbj, pl->crt, e_mu + i0, e_nu + j0, alpha, beta, Cij, ldc, st));
         }
         if (hook && hook->done) {

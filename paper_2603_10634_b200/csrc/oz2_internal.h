@@ -65,6 +65,7 @@ struct GemmParams {
     int rows_per_plane_a;        // m_pad
     int rows_per_plane_b;        // n_pad
     int num_moduli;
+    int mod_split;               // residue mode: one work item per (tile, modulus) (no fused CRT)
     int16_t* residues;           // [N][n][m]
     uint32_t* rmax;              // [m] float bits (bound)
     uint32_t* smax;              // [n]

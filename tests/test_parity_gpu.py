@@ -206,6 +206,51 @@ def test_imported_exponents_bit_exact(dev, N):
     assert np.array_equal(res["C"], ref.C)
 
 
+_SCHED_REF = {}
+
+
+@pytest.mark.parametrize("split", ["0", "1"])
+@pytest.mark.parametrize("sch", ["fp8", "int8"])
+def test_work_item_schedules(dev, split, sch, monkeypatch):
+    """Both residue-GEMM schedules -- tile-major (every modulus of a tile in one work item,
+    CRT fused into the epilogue for k >= 8192) and modulus-split (one (tile, modulus) item,
+    separate CRT; automatic for grids with few tiles) -- give the oracle's residues and C
+    bit for bit (imported exponents), with alpha/beta and k >= 8192."""
+    from gpu_helpers import run
+    from oracle import int8
+    monkeypatch.setenv("OZ2_MOD_SPLIT", split)
+    m, k, n, N = 16, 8200, 24, 13
+    A = gen_host(m, k, "phi", phi=1.0, seed=51)
+    B = gen_host(k, n, "phi", phi=1.0, seed=52)
+    if sch not in _SCHED_REF:
+        _SCHED_REF[sch] = int8.dgemm(A, B, N) if sch == "int8" else scheme.dgemm(A, B, N)
+    ref = _SCHED_REF[sch]
+    res = run(A, B, N, e_mu_in=ref.e_mu, e_nu_in=ref.e_nu, scheme=sch, alpha=2.0, beta=0.5,
+              C0=np.ones((m, n)))
+    for l in range(N):
+        assert np.array_equal(res["residues"][l], ref.residues[l]), l
+    want = np.array([[float(Fraction(2) * Fraction(float(ref.C[i, j])) + Fraction(0.5))
+                      for j in range(n)] for i in range(m)])
+    assert np.array_equal(res["C"], want)
+
+
+@pytest.mark.parametrize("sch", ["fp8", "int8", "karatsuba"])
+def test_work_item_schedules_agree_many_tiles(dev, sch, monkeypatch):
+    """Tile-major (fused CRT) and modulus-split schedules on a grid of 4 x 5 CTA-pair tiles
+    with ragged edges: identical residues and C (both are exact)."""
+    from gpu_helpers import run
+    m, k, n, N = 1000, 8192, 1100, 14
+    A = gen_host(m, k, "phi", phi=2.0, seed=53)
+    B = gen_host(k, n, "phi", phi=2.0, seed=54)
+    outs = []
+    for split in ["0", "1"]:
+        monkeypatch.setenv("OZ2_MOD_SPLIT", split)
+        outs.append(run(A, B, N, scheme=sch))
+    assert np.array_equal(outs[0]["e_mu"], outs[1]["e_mu"])
+    assert np.array_equal(outs[0]["residues"], outs[1]["residues"])
+    assert np.array_equal(outs[0]["C"], outs[1]["C"])
+
+
 def test_alpha_beta_and_quick_returns(dev):
     from gpu_helpers import run
     m, k, n = 70, 90, 80
