@@ -62,6 +62,10 @@ __device__ __forceinline__ void crt_stage_constants(CrtShared* s, const CrtParam
     }
 }
 
+template <int L>
+__device__ __forceinline__ double crt_finish(const uint64_t (&acc)[L], uint64_t tacc, const CrtParams& cp,
+                                             int escale);
+
 // value of C'(i,j) * 2^-escale, rounded once to nearest binary64; rp points at the
 // residue of modulus 0 of the element, residues of modulus l at rp + l * lstride
 template <int L>
@@ -80,6 +84,14 @@ __device__ __forceinline__ double crt_element(const int16_t* rp, int64_t lstride
 #pragma unroll
         for (int t = 0; t < L; ++t) acc[t] += static_cast<uint64_t>(u) * s->w[l][t];
     }
+    return crt_finish<L>(acc, tacc, cp, escale);
+}
+
+// the rest of the reconstruction from the accumulated S (L limbs of 64-bit partial sums)
+// and the fixed-point quotient estimate
+template <int L>
+__device__ __forceinline__ double crt_finish(const uint64_t (&acc)[L], uint64_t tacc, const CrtParams& cp,
+                                             int escale) {
     const uint32_t tq = static_cast<uint32_t>(tacc >> 32);   // t = round(S / P) (+-1)
     uint32_t r[L];
     uint64_t carry = 0;

@@ -27,12 +27,65 @@ __global__ void __launch_bounds__(256) k_crt(const int16_t* __restrict__ res, in
     }
 }
 
+// Specialised for the common (limbs, moduli) pairs: two consecutive rows per thread (one
+// 32-bit load per modulus), all NM residue loads issued before the arithmetic, and the
+// CRT weights read straight from the kernel-parameter constant bank (fully unrolled).
+template <int L, int NM>
+__global__ void __launch_bounds__(256) k_crt_n(const int16_t* __restrict__ res, int64_t m, int64_t n,
+                                               const __grid_constant__ CrtParams cp,
+                                               const int32_t* __restrict__ e_mu,
+                                               const int32_t* __restrict__ e_nu, double alpha,
+                                               double beta, double* __restrict__ C, int64_t ldc) {
+    const int64_t i = 2 * (static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x);   // m is even
+    if (i >= m) return;
+    const int emu0 = e_mu[i], emu1 = e_mu[i + 1];
+    const int64_t lstride = n * m;
+    for (int64_t j = blockIdx.y; j < n; j += gridDim.y) {
+        const int16_t* rp = res + j * m + i;
+        uint32_t rr[NM];
+#pragma unroll
+        for (int l = 0; l < NM; ++l) rr[l] = __ldcs(reinterpret_cast<const unsigned int*>(rp + l * lstride));
+        const int enu = e_nu[j];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint64_t acc[L];
+#pragma unroll
+            for (int t = 0; t < L; ++t) acc[t] = 0;
+            uint64_t tacc = 0x80000000ull;
+#pragma unroll
+            for (int l = 0; l < NM; ++l) {
+                const int c = static_cast<int16_t>(h ? (rr[l] >> 16) : (rr[l] & 0xFFFFu));
+                const uint32_t u = static_cast<uint32_t>(c) + (c < 0 ? static_cast<uint32_t>(cp.p[l]) : 0u);
+                tacc += static_cast<uint64_t>(u) * cp.qp32[l];
+#pragma unroll
+                for (int t = 0; t < L; ++t) acc[t] += static_cast<uint64_t>(u) * cp.w[l][t];
+            }
+            const double v = crt_finish<L>(acc, tacc, cp, (h ? emu1 : emu0) + enu);
+            store_alpha_beta(C + i + h + j * ldc, v, alpha, beta);
+        }
+    }
+}
+
 cudaError_t launch_crt(int limbs, const int16_t* res, int64_t m, int64_t n, const CrtParams& cp,
                        const int32_t* e_mu, const int32_t* e_nu, double alpha, double beta,
                        double* C, int64_t ldc, cudaStream_t st) {
     if (m == 0 || n == 0) return cudaSuccess;
     // ~2048 blocks in total, each looping over many columns (amortises the staging of
     // the CRT constants in shared memory)
+    if (m % 2 == 0) {
+        const int64_t gx2 = (m / 2 + 255) / 256;
+        int64_t gy2 = 2048 / gx2;
+        gy2 = gy2 < 1 ? 1 : (gy2 > n ? n : gy2);
+        dim3 grid2(static_cast<unsigned>(gx2), static_cast<unsigned>(gy2 < 65535 ? gy2 : 65535));
+#define OZ2_CRTN(LL, NN)                                                                            \
+        if (limbs == LL && cp.num_moduli == NN) {                                                   \
+            k_crt_n<LL, NN><<<grid2, 256, 0, st>>>(res, m, n, cp, e_mu, e_nu, alpha, beta, C, ldc); \
+            return cudaGetLastError();                                                              \
+        }
+        OZ2_CRTN(4, 12) OZ2_CRTN(4, 13) OZ2_CRTN(4, 14) OZ2_CRTN(4, 15) OZ2_CRTN(5, 15)
+        OZ2_CRTN(5, 16) OZ2_CRTN(4, 16) OZ2_CRTN(5, 17) OZ2_CRTN(5, 18) OZ2_CRTN(6, 20)
+#undef OZ2_CRTN
+    }
     const int64_t gx = (m + 255) / 256;
     int64_t gy = 2048 / gx;
     gy = gy < 1 ? 1 : (gy > n ? n : gy);
