@@ -243,8 +243,9 @@ def run_oz2(args, rank, world, local_rank):
     # rowmax x2, cast x2, [bound GEMM], exps, digits x2, residue GEMM, [k_crt unless fused]
     tiles = ((m + 255) // 256) * ((n + 255) // 256)
     mod_split = tiles < 8 * (torch.cuda.get_device_properties(dev).multi_processor_count // 2)
+    fenv = int(os.environ.get("OZ2_FUSED_CRT", "-1"))
     fused = (P.oz2_plan_query(N, k).num_limbs <= 6 and k >= 8192 and not mod_split
-             and os.environ.get("OZ2_FUSED_CRT", "1") != "0")
+             and (fenv > 0 or (fenv < 0 and k >= (49152 if args.scheme == "int8" else 16384))))
     launches_per_step = 8 + (args.mode == "accurate") + (not fused)
 
     out = {

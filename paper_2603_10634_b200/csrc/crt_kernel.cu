@@ -41,10 +41,14 @@ __global__ void __launch_bounds__(256) k_crt_n(const int16_t* __restrict__ res, 
     const int emu0 = e_mu[i], emu1 = e_mu[i + 1];
     const int64_t lstride = n * m;
     for (int64_t j = blockIdx.y; j < n; j += gridDim.y) {
-        const int16_t* rp = res + j * m + i;
+        const unsigned int* rp = reinterpret_cast<const unsigned int*>(res + j * m + i);
+        const int64_t ls2 = lstride / 2;                 // in 32-bit words (lstride is even)
         uint32_t rr[NM];
 #pragma unroll
-        for (int l = 0; l < NM; ++l) rr[l] = __ldcs(reinterpret_cast<const unsigned int*>(rp + l * lstride));
+        for (int l = 0; l < NM; ++l) {
+            rr[l] = __ldcs(rp);
+            rp += ls2;
+        }
         const int enu = e_nu[j];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {

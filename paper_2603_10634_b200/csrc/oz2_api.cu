@@ -652,9 +652,14 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
     if (opt && opt->e_mu) OZ2_CK(cudaMemcpyAsync(opt->e_mu, e_mu, 4 * m, cudaMemcpyDeviceToDevice, st));
     if (opt && opt->e_nu) OZ2_CK(cudaMemcpyAsync(opt->e_nu, e_nu, 4 * n, cudaMemcpyDeviceToDevice, st));
 
-    // fuse the CRT into the epilogue for up to 6 limbs (N <= 20) unless OZ2_FUSED_CRT=0
-    // (k >= 8192: a product then lasts long enough to hide one CRT step per product)
-    const int fused = (pl->L <= 6 && k >= 8192 && env_int("OZ2_FUSED_CRT", 1) != 0) ? pl->L : 0;
+    // fuse the CRT into the epilogue for up to 6 limbs (N <= 20) when a product lasts long
+    // enough to hide the CRT steps spread over it: measured (profiles/round1_fused_crt_ab.md)
+    // FP8 fused wins from k = 16384 on (+1-2 %) and loses 20 % at k = 8192; INT8 (one
+    // product per modulus, so 3x the CRT work per product) loses 23 % at k = 16384.
+    // OZ2_FUSED_CRT: -1 auto (default), 0 never, 1 whenever L <= 6 and k >= 8192.
+    const int fuse_env = env_int("OZ2_FUSED_CRT", -1);
+    const bool fuse_auto = i8 ? k >= 49152 : k >= 16384;
+    const int fused = (pl->L <= 6 && k >= 8192 && (fuse_env > 0 || (fuse_env < 0 && fuse_auto))) ? pl->L : 0;
     int sync_chunk = 1;
     {   // chunks must tile the 512-block K segments: a power of two in [1, 512]
         const int kc = env_int("OZ2_SYNC_CHUNK", 8);

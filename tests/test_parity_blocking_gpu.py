@@ -69,8 +69,10 @@ def test_blocked_layouts_alpha_beta(dev, ta, tb):
     assert np.array_equal(out["C_pad"], full["C_pad"])       # rows beyond m untouched
 
 
-def test_blocked_fused_crt_path(dev):
-    """k >= 8192 takes the CRT-in-epilogue path; blocks of 512 x 768."""
+def test_blocked_fused_crt_path(dev, monkeypatch):
+    """k >= 8192 with OZ2_FUSED_CRT=1 takes the CRT-in-epilogue path; blocks of 512 x 768."""
+    monkeypatch.setenv("OZ2_FUSED_CRT", "1")
+    monkeypatch.setenv("OZ2_MOD_SPLIT", "0")
     m, k, n = 1100, 8192, 1300
     A = gen_host(m, k, "phi", phi=0.5, seed=46, order="F")
     B = gen_host(k, n, "phi", phi=0.5, seed=47, order="F")

@@ -219,6 +219,7 @@ def test_work_item_schedules(dev, split, sch, monkeypatch):
     from gpu_helpers import run
     from oracle import int8
     monkeypatch.setenv("OZ2_MOD_SPLIT", split)
+    monkeypatch.setenv("OZ2_FUSED_CRT", "1")        # tile-major then fuses (k >= 8192)
     m, k, n, N = 16, 8200, 24, 13
     A = gen_host(m, k, "phi", phi=1.0, seed=51)
     B = gen_host(k, n, "phi", phi=1.0, seed=52)
@@ -243,9 +244,14 @@ def test_work_item_schedules_agree_many_tiles(dev, sch, monkeypatch):
     A = gen_host(m, k, "phi", phi=2.0, seed=53)
     B = gen_host(k, n, "phi", phi=2.0, seed=54)
     outs = []
+    monkeypatch.setenv("OZ2_FUSED_CRT", "1")        # tile-major then fuses (k >= 8192)
     for split in ["0", "1"]:
         monkeypatch.setenv("OZ2_MOD_SPLIT", split)
         outs.append(run(A, B, N, scheme=sch))
+    monkeypatch.setenv("OZ2_FUSED_CRT", "0")        # tile-major with the separate CRT
+    monkeypatch.setenv("OZ2_MOD_SPLIT", "0")
+    outs.append(run(A, B, N, scheme=sch))
+    assert np.array_equal(outs[0]["C"], outs[2]["C"])
     assert np.array_equal(outs[0]["e_mu"], outs[1]["e_mu"])
     assert np.array_equal(outs[0]["residues"], outs[1]["residues"])
     assert np.array_equal(outs[0]["C"], outs[1]["C"])
