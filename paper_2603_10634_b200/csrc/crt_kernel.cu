@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(256) k_crt(const int16_t* __restrict__ res, in
 // 32-bit load per modulus), all NM residue loads issued before the arithmetic, and the
 // CRT weights read straight from the kernel-parameter constant bank (fully unrolled).
 template <int L, int NM>
-__global__ void __launch_bounds__(256) k_crt_n(const int16_t* __restrict__ res, int64_t m, int64_t n,
+__global__ void __launch_bounds__(256, 4) k_crt_n(const int16_t* __restrict__ res, int64_t m, int64_t n,
                                                const __grid_constant__ CrtParams cp,
                                                const int32_t* __restrict__ e_mu,
                                                const int32_t* __restrict__ e_nu, double alpha,
