@@ -2,7 +2,7 @@
 // scaling (eq. CRT_finalreduction, eq. inversescaling), shared by
 // the standalone k_crt and the fused epilogue of the residue GEMM.
 //
-// With u_l = C'_l mod p_l in [0, p_l) and w_l = q_l P/p_l:
+// With u_l = C'_l mod p_l in [0, p_l) (the residue GEMM stores u_l) and w_l = q_l P/p_l:
 //   S = sum_l u_l w_l                     (exact, L 32-bit limbs, wrap-around mod 2^(32L))
 //   t = round(sum_l u_l q_l/p_l)          (fixed point, 2^-32 units: S/P to within 2^-19)
 //   C' = S - t P  (mod 2^(32L)), then one correction into [-P/2, P/2)   (symmetric, R2)
@@ -78,8 +78,8 @@ __device__ __forceinline__ double crt_element(const int16_t* rp, int64_t lstride
     uint64_t tacc = 0x80000000ull;                       // + 1/2: round-to-nearest of S/P
 #pragma unroll 4
     for (int l = 0; l < nm; ++l) {
-        const int c = streaming ? static_cast<int>(__ldcs(rp + l * lstride)) : static_cast<int>(__ldg(rp + l * lstride));
-        const uint32_t u = static_cast<uint32_t>(c) + (c < 0 ? s->p[l] : 0u);
+        const uint16_t* up = reinterpret_cast<const uint16_t*>(rp + l * lstride);   // u_l in [0, p_l)
+        const uint32_t u = streaming ? static_cast<uint32_t>(__ldcs(up)) : static_cast<uint32_t>(__ldg(up));
         tacc += static_cast<uint64_t>(u) * s->qp[l];    // sum u_l q_l/p_l in 2^-32 units
 #pragma unroll
         for (int t = 0; t < L; ++t) acc[t] += static_cast<uint64_t>(u) * s->w[l][t];
@@ -102,19 +102,25 @@ __device__ __forceinline__ double crt_finish(const uint64_t (&acc)[L], uint64_t 
         carry = v >> 32;
     }
     bool negv = (r[L - 1] >> 31) != 0;
-    if (!negv) {
-        if (cmp_limbs<L>(r, cp.halfP) >= 0) {             // C' >= P/2: subtract P
-            add_limbs<L>(r, cp.np);
-            negv = (r[L - 1] >> 31) != 0;
-        }
-    } else {
-        uint32_t a[L];
+    // fast path: with T the signed top limb and H_top that of P/2, -H_top <= T < H_top
+    // already puts C' in [-P/2, P/2) (the quotient estimate is almost never off by one)
+    const int T = static_cast<int>(r[L - 1]);
+    const int Ht = static_cast<int>(cp.halfP[L - 1]);
+    if (T >= Ht || T < -Ht) {
+        if (!negv) {
+            if (cmp_limbs<L>(r, cp.halfP) >= 0) {         // C' >= P/2: subtract P
+                add_limbs<L>(r, cp.np);
+                negv = (r[L - 1] >> 31) != 0;
+            }
+        } else {
+            uint32_t a[L];
 #pragma unroll
-        for (int t = 0; t < L; ++t) a[t] = r[t];
-        negate_limbs<L>(a);
-        if (cmp_limbs<L>(a, cp.halfP) > 0) {              // C' < -P/2: add P
-            add_limbs<L>(r, cp.P);
-            negv = (r[L - 1] >> 31) != 0;
+            for (int t = 0; t < L; ++t) a[t] = r[t];
+            negate_limbs<L>(a);
+            if (cmp_limbs<L>(a, cp.halfP) > 0) {          // C' < -P/2: add P
+                add_limbs<L>(r, cp.P);
+                negv = (r[L - 1] >> 31) != 0;
+            }
         }
     }
     if (negv) negate_limbs<L>(r);

@@ -2,6 +2,7 @@
 // (eq. CRT_finalreduction, eq. inversescaling); the arithmetic is in
 // crt_common.cuh (shared with the fused residue-GEMM epilogue).
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include "oz2_internal.h"
 #include "crt_common.cuh"
@@ -58,8 +59,7 @@ __global__ void __launch_bounds__(256, 4) k_crt_n(const int16_t* __restrict__ re
             uint64_t tacc = 0x80000000ull;
 #pragma unroll
             for (int l = 0; l < NM; ++l) {
-                const int c = static_cast<int16_t>(h ? (rr[l] >> 16) : (rr[l] & 0xFFFFu));
-                const uint32_t u = static_cast<uint32_t>(c) + (c < 0 ? static_cast<uint32_t>(cp.p[l]) : 0u);
+                const uint32_t u = h ? (rr[l] >> 16) : (rr[l] & 0xFFFFu);      // u_l in [0, p_l)
                 tacc += static_cast<uint64_t>(u) * cp.qp32[l];
 #pragma unroll
                 for (int t = 0; t < L; ++t) acc[t] += static_cast<uint64_t>(u) * cp.w[l][t];
@@ -70,13 +70,36 @@ __global__ void __launch_bounds__(256, 4) k_crt_n(const int16_t* __restrict__ re
     }
 }
 
+// debug output: the stored u_l in [0, p_l) back to the symmetric range of C'_l (R2)
+__global__ void k_res_symmetric(int16_t* __restrict__ out, const int16_t* __restrict__ in, int64_t per,
+                                const __grid_constant__ CrtParams cp) {
+    const int l = blockIdx.y;
+    const int p = cp.p[l];
+    const int half = (p + 1) / 2;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < per;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int u = static_cast<uint16_t>(in[l * per + e]);
+        out[l * per + e] = static_cast<int16_t>(u >= half ? u - p : u);
+    }
+}
+
+cudaError_t launch_res_symmetric(int16_t* out, const int16_t* in, int64_t per, const CrtParams& cp,
+                                 cudaStream_t st) {
+    if (per == 0) return cudaSuccess;
+    const int64_t bx = (per + 255) / 256;
+    dim3 grid(static_cast<unsigned>(bx < 4096 ? bx : 4096), static_cast<unsigned>(cp.num_moduli));
+    k_res_symmetric<<<grid, 256, 0, st>>>(out, in, per, cp);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_crt(int limbs, const int16_t* res, int64_t m, int64_t n, const CrtParams& cp,
                        const int32_t* e_mu, const int32_t* e_nu, double alpha, double beta,
                        double* C, int64_t ldc, cudaStream_t st) {
     if (m == 0 || n == 0) return cudaSuccess;
     // ~2048 blocks in total, each looping over many columns (amortises the staging of
     // the CRT constants in shared memory)
-    if (m % 2 == 0) {
+    const char* gen = std::getenv("OZ2_CRT_GENERIC");              // A/B knob: 1 = generic kernel
+    if (m % 2 == 0 && !(gen && gen[0] == '1')) {
         const int64_t gx2 = (m / 2 + 255) / 256;
         int64_t gy2 = 2048 / gx2;
         gy2 = gy2 < 1 ? 1 : (gy2 > n ? n : gy2);

@@ -442,12 +442,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                                 if (!last) {
                                     part[idx] = __floats2half2_rn(acc[0], acc[1]);  // exact (|acc| <= 546)
                                 } else {
-                                    // C'_l = mod(sum_x coef_x r_x, p), symmetric range (R2)
+                                    // C'_l mod p stored as u in [0, p) (|acc| <= p/2 + 1 here);
+                                    // the CRT consumes u directly, the debug output converts
+                                    // it back to the symmetric range (R2)
 #pragma unroll
                                     for (int u = 0; u < 2; ++u) {
                                         float r = acc[u];
-                                        if (2.0f * r >= p) r -= p;
-                                        else if (2.0f * r < -p) r += p;
+                                        if (r < 0.0f) r += p;
                                         const int jj = c * 32 + j + u;
                                         if (row_ok && col0 + jj < P.n)       // streamed: read once by the CRT
                                             __stcs(out + static_cast<int64_t>(jj) * P.m, static_cast<short>(r));

@@ -727,8 +727,8 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             }
             OZ2_CK(launch_gemm(i8 ? MODE_RESIDUE_I8 : MODE_RESIDUE, cg, fused_blk, ta, tb, gp, g_ts.num_sms, st));
             if (!L.blocked) {
-                if (opt && opt->residues)
-                    OZ2_CK(cudaMemcpyAsync(opt->residues, res, 2ull * N * m * n, cudaMemcpyDeviceToDevice, st));
+                if (opt && opt->residues)   // stored as u_l in [0, p_l): symmetric C'_l for the caller
+                    OZ2_CK(launch_res_symmetric(opt->residues, res, m * n, pl->crt, st));
                 phase_mark(5);
             }
             // ---- step 6: CRT + inverse scaling (eqs. CRT_finalreduction, inversescaling)
