@@ -283,9 +283,9 @@ def run_oz2(args, rank, world, local_rank):
                 if rank == 0:
                     Bt.copy_(Bhost.t(), non_blocking=True)
                 dist.broadcast(Bt, src=0)
-                torch.cuda.current_stream().synchronize()
-                # per rank: A, C on the host; B already resident
-                rc = P.oz2_dgemm("N", "N", m, n, k, 1.0, Ahost.data_ptr(), m, B.data_ptr(), k, 0.0,
+                # per rank: its A block host -> device, the device-pointer call, C block back
+                A.copy_(Ahost, non_blocking=True)
+                rc = P.oz2_dgemm("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0,
                                  C.data_ptr(), m, N)
                 Chost.copy_(C)
             else:
@@ -312,8 +312,9 @@ def run_oz2(args, rank, world, local_rank):
                       "h2d_bytes_per_step": world * 8 * m * k + 8 * k * n,
                       "d2h_bytes_per_step": world * 8 * m * n,
                       "ms_per_step": round(e2e_s * 1e3, 3),
-                      "buffers": ("pinned host; mixed: A/C host pointers through oz2_dgemm, B host -> rank 0 "
-                                  "-> NCCL broadcast" if world > 1 else "pinned host (A, B, C through oz2_dgemm)")}
+                      "buffers": ("pinned host: B host -> rank 0 -> NCCL broadcast, each rank's A / C block "
+                                  "host <-> device around the device-pointer oz2_dgemm" if world > 1
+                                  else "pinned host (A, B, C through oz2_dgemm)")}
         del Ahost, Bhost, Chost
     if rank != 0 or args.no_extras:
         return out, None
