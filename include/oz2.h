@@ -87,7 +87,9 @@ extern "C" {
  * C <- beta C (C not read when beta == 0).
  * Non-finite entries in A or B: the call still returns 0 (no host sync on the fast
  * path); the device status word is set and oz2_get_status() reports
- * OZ2_ERR_NONFINITE (reading R12).
+ * OZ2_ERR_NONFINITE (reading R12).  Every entry of C in a row of op(A) or a column of
+ * op(B) holding a NaN or Inf is NaN (its scaling exponent, in the e_mu / e_nu outputs
+ * of oz2_dgemm_ex, is INT32_MIN); the other entries are computed normally.
  */
 int oz2_dgemm(char transa, char transb, int64_t m, int64_t n, int64_t k,
               double alpha, const double* A, int64_t lda,

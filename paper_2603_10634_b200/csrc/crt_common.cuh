@@ -164,6 +164,12 @@ __device__ __forceinline__ double crt_finish(const uint64_t (&acc)[L], uint64_t 
     return negv ? -v : v;
 }
 
+// inverse-scaling exponent of element (i, j), or the NaN marker when row i of op(A) or
+// column j of op(B) held a NaN / Inf (R12)
+__device__ __forceinline__ bool exps_finite(int emu, int enu) {
+    return emu != kExpNonFinite && enu != kExpNonFinite;
+}
+
 // C <- alpha v + beta C (R11; beta == 0 never reads C)
 __device__ __forceinline__ void store_alpha_beta(double* cptr, double v, double alpha, double beta) {
     if (beta == 0.0) *cptr = alpha * v;

@@ -23,7 +23,9 @@ __global__ void __launch_bounds__(256) k_crt(const int16_t* __restrict__ res, in
     const int emu = e_mu[i];
     const int64_t lstride = n * m;
     for (int64_t j = blockIdx.y; j < n; j += gridDim.y) {
-        const double v = crt_element<L>(res + j * m + i, lstride, &s, cp, emu + e_nu[j], false);
+        const int enu = e_nu[j];
+        const double v = exps_finite(emu, enu) ? crt_element<L>(res + j * m + i, lstride, &s, cp, emu + enu, false)
+                                               : __longlong_as_double(0x7FF8000000000000ll);
         store_alpha_beta(C + i + j * ldc, v, alpha, beta);
     }
 }
@@ -64,7 +66,9 @@ __global__ void __launch_bounds__(256, 4) k_crt_n(const int16_t* __restrict__ re
 #pragma unroll
                 for (int t = 0; t < L; ++t) acc[t] += static_cast<uint64_t>(u) * cp.w[l][t];
             }
-            const double v = crt_finish<L>(acc, tacc, cp, (h ? emu1 : emu0) + enu);
+            const int emu = h ? emu1 : emu0;
+            const double v = exps_finite(emu, enu) ? crt_finish<L>(acc, tacc, cp, emu + enu)
+                                                   : __longlong_as_double(0x7FF8000000000000ll);
             store_alpha_beta(C + i + h + j * ldc, v, alpha, beta);
         }
     }

@@ -369,8 +369,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             for (int s2 = 0; s2 < ncols && crt_j < 128; ++s2, ++crt_j) {
                 const int64_t col = crt_col0 + crt_j;
                 if (col >= P.n) { crt_j = 128; break; }
-                const double v = crt_element<(FL > 0 ? FL : 4)>(P.residues + col * P.m + crt_row, lstride, crt_s,
-                                                                 P.crt, emu + P.e_nu[col], true);
+                const int enu = P.e_nu[col];
+                const double v = exps_finite(emu, enu)
+                                     ? crt_element<(FL > 0 ? FL : 4)>(P.residues + col * P.m + crt_row, lstride,
+                                                                      crt_s, P.crt, emu + enu, true)
+                                     : __longlong_as_double(0x7FF8000000000000ll);      // R12
                 store_alpha_beta(P.C + crt_row + col * P.ldc, v, P.alpha, P.beta);
             }
         };

@@ -9,6 +9,8 @@
 namespace oz2 {
 
 constexpr int kMaxModuli = 33;   // N < 34
+// scaling exponent of a row / column holding NaN or Inf (R12): its entries of C are NaN
+constexpr int kExpNonFinite = -2147483647 - 1;
 constexpr int kMaxLimbs = 12;
 constexpr int kPow2Tab = 1024;   // 2^E mod p for E in [0, 1024)
 constexpr int kMaxK = 65536;     // exactness window of one FP32 accumulation

@@ -167,7 +167,10 @@ __global__ void __launch_bounds__(256) k_cast(const double* __restrict__ X, int6
     for (int j = 0; j < TR / 8; ++j) {
         const int rr = w + 8 * j;
         const int64_t r = r0 + rr;
-        const int e = (r < rows) ? eprime_of<I8>(maxbits[r]) : 0;
+        const unsigned long long mbr = (r < rows) ? maxbits[r] : 0ull;
+        const int e = eprime_of<I8>(mbr);
+        const bool bad = mbr >= 0x7FF0000000000000ull;     // NaN / Inf row: zero bounds, so it
+                                                           // cannot disturb other rows' exponents (R12)
         const double s1 = pow2d(e >> 1), s2 = pow2d(e - (e >> 1));   // 2^e in two exact steps
         uint32_t word = 0;
         unsigned long long sq = 0;
@@ -175,7 +178,7 @@ __global__ void __launch_bounds__(256) k_cast(const double* __restrict__ X, int6
         for (int q = 0; q < 4; ++q) {
             const double x = tile[rr * TP + lane * 4 + q];
             uint32_t c = 0;
-            if (x != 0.0) {
+            if (x != 0.0 && !bad) {
                 if (I8) {
                     c = static_cast<uint32_t>(ceil((fabs(x) * s1) * s2));   // exact: < 2^7 scaled
                 } else {
@@ -206,6 +209,7 @@ __global__ void k_exps(const unsigned long long* __restrict__ maxbits,
     if (r >= count) return;
     const unsigned long long mb = maxbits[r];
     if (mb == 0ull) { e_out[r] = 0; return; }               // zero row (R3)
+    if (mb >= 0x7FF0000000000000ull) { e_out[r] = kExpNonFinite; return; }   // NaN / Inf (R12)
     const float R = __uint_as_float(rsmax[r]);
     if (!(R > 0.0f)) { e_out[r] = eprime[r]; return; }       // no nonzero product
     const float cbar = __fmul_ru(ep.f_k, R);                 // RU(f_k C-bar') (eq. barCupper, R5)
@@ -237,6 +241,7 @@ __global__ void k_exps_fast(const unsigned long long* __restrict__ maxbits,
     if (r >= count) return;
     const unsigned long long U = sumsq ? sumsq[r] : static_cast<unsigned long long>(u32[r]);
     if (maxbits[r] == 0ull) { e_out[r] = 0; return; }       // zero row (R3)
+    if (maxbits[r] >= 0x7FF0000000000000ull) { e_out[r] = kExpNonFinite; return; }   // R12
     if (U == 0ull) { e_out[r] = eprime[r]; return; }        // no nonzero product (R3)
     const int hbits = 64 - __clzll(static_cast<long long>(fp.h));
     const int ubits = 64 - __clzll(static_cast<long long>(U));
@@ -268,7 +273,14 @@ __device__ __forceinline__ double dfma_rn(double a, double b, double c) {   // k
     return d;
 }
 
-// residue and digits of one modulus for the 4 elements of a lane; NSTEP = 1: |y| < 2^50 p_min
+// k_digits: each lane handles kEPL consecutive elements of a row and stores kEPL bytes per
+// digit plane (kEPL = 8 -- one 8-byte store per plane -- was measured: 4 % fewer
+// instructions but 17 % slower for the MN-major operand, 78 vs 50 registers)
+constexpr int kEPL = 4;
+using DWord = uint32_t;          // kEPL bytes of one digit plane
+static_assert(sizeof(DWord) == kEPL && TH % kEPL == 0 && 32 % (TH / kEPL) == 0, "k_digits lane map");
+
+// residue and digits of one modulus for the kEPL elements of a lane; NSTEP = 1: |y| < 2^50 p_min
 // (~2^59 for the hybrid moduli), NSTEP = 2: |y| < 2^86 p_min (first reduced modulo
 // Q = p 2^36, exactly), NSTEP = 0: the general M 2^E form with (2^E mod p) from the
 // table (any |y|).  The limits keep every rounding quotient below 2^51, where the
@@ -276,18 +288,18 @@ __device__ __forceinline__ double dfma_rn(double a, double b, double c) {   // k
 // SQ: 1 square, 0 non-square, -1 read md.square at run time, 2 INT8 scheme (the residue
 // itself, as a two's-complement byte, is the single operand plane of the modulus)
 template <int SQ>
-__device__ __forceinline__ void emit_digits(const ModDig& md, const float (&rf)[4], uint8_t* o,
+__device__ __forceinline__ void emit_digits(const ModDig& md, const float (&rf)[kEPL], uint8_t* o,
                                             int64_t plane_stride);
 
 template <int NSTEP, int SQ>
-__device__ __forceinline__ void digits_one_modulus(const ModDig& md, int l, int plane0, const double (&y)[4],
-                                                   const double (&M)[4], const int (&E)[4],
+__device__ __forceinline__ void digits_one_modulus(const ModDig& md, int l, int plane0, const double (&y)[kEPL],
+                                                   const double (&M)[kEPL], const int (&E)[kEPL],
                                                    const uint16_t* __restrict__ pow2tab,
                                                    uint8_t* out, int64_t plane_stride) {
     const double pinv = md.pinv_d, pd = md.p_d, magic = kMagic52;
-    float rf[4];
+    float rf[kEPL];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < kEPL; ++q) {
         int ri;
         if (NSTEP == 0) {
             const double qq = dfma_rn(M[q], pinv, magic) - magic;
@@ -318,7 +330,7 @@ __device__ __forceinline__ void digits_one_modulus(const ModDig& md, int l, int 
         const float2 pi2 = make_float2(md.pinv_f, md.pinv_f), hp2 = make_float2(md.hp_f, md.hp_f);
         const float2 np2 = make_float2(-md.p_f, -md.p_f);
 #pragma unroll
-        for (int q = 0; q < 4; q += 2) {
+        for (int q = 0; q < kEPL; q += 2) {
             const float2 r = __fadd2_rn(make_float2(rf[q], rf[q + 1]), nM2);
             const float2 qv = __fadd2_rn(__fadd2_rn(__ffma2_rn(r, pi2, hp2), M2), nM2);
             const float2 rs = __ffma2_rn(qv, np2, r);
@@ -330,16 +342,17 @@ __device__ __forceinline__ void digits_one_modulus(const ModDig& md, int l, int 
 }
 
 // the digit planes (or the INT8 residue plane) of one modulus from the exact symmetric
-// residues rf[4] of the lane's 4 elements
+// residues rf[kEPL] of the lane's kEPL consecutive elements
 template <int SQ>
-__device__ __forceinline__ void emit_digits(const ModDig& md, const float (&rf)[4], uint8_t* o,
+__device__ __forceinline__ void emit_digits(const ModDig& md, const float (&rf)[kEPL], uint8_t* o,
                                             int64_t plane_stride) {
     if (SQ == 2) {
-        uint32_t w = 0;
+        DWord w = 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-            w |= (static_cast<uint32_t>(__float_as_int(rf[q] + kMagic23) - 0x4B400000) & 0xFFu) << (8 * q);
-        *reinterpret_cast<uint32_t*>(o) = w;
+        for (int q = 0; q < kEPL; ++q)
+            w |= static_cast<DWord>((static_cast<uint32_t>(__float_as_int(rf[q] + kMagic23) - 0x4B400000) & 0xFFu))
+                 << (8 * q);
+        *reinterpret_cast<DWord*>(o) = w;
         return;
     }
     // digit arithmetic on packed FP32 pairs (sm_100 FFMA2/FADD2); every value is an exact
@@ -348,42 +361,42 @@ __device__ __forceinline__ void emit_digits(const ModDig& md, const float (&rf)[
     if (SQ == 1 || (SQ < 0 && md.square)) {
         // D1 = round(r/s) ties-to-even, D2 = r - s D1 (R9)
         const float2 is2 = make_float2(md.inv_s_f, md.inv_s_f), ns2 = make_float2(-md.s_f, -md.s_f);
-        uint32_t w1 = 0, w2 = 0;
+        DWord w1 = 0, w2 = 0;
 #pragma unroll
-        for (int q = 0; q < 4; q += 2) {
+        for (int q = 0; q < kEPL; q += 2) {
             const float2 r = make_float2(rf[q], rf[q + 1]);
             const float2 d1 = __fadd2_rn(__ffma2_rn(r, is2, M2), nM2);
             const float2 d2 = __ffma2_rn(d1, ns2, r);
-            w1 |= static_cast<uint32_t>(cvt_e4m3x2(d1.x, d1.y)) << (8 * q);
-            w2 |= static_cast<uint32_t>(cvt_e4m3x2(d2.x, d2.y)) << (8 * q);
+            w1 |= static_cast<DWord>(cvt_e4m3x2(d1.x, d1.y)) << (8 * q);
+            w2 |= static_cast<DWord>(cvt_e4m3x2(d2.x, d2.y)) << (8 * q);
         }
-        *reinterpret_cast<uint32_t*>(o) = w1;
-        *reinterpret_cast<uint32_t*>(o + plane_stride) = w2;
+        *reinterpret_cast<DWord*>(o) = w1;
+        *reinterpret_cast<DWord*>(o + plane_stride) = w2;
     } else {
         // D1 = sign(r) ceil(|r|/16), D2 = r - 16 D1, D3 = D1 + D2
         const float2 s16 = make_float2(0.0625f, 0.0625f), n16 = make_float2(-16.0f, -16.0f);
-        uint32_t w1 = 0, w2 = 0, w3 = 0;
+        DWord w1 = 0, w2 = 0, w3 = 0;
 #pragma unroll
-        for (int q = 0; q < 4; q += 2) {
+        for (int q = 0; q < kEPL; q += 2) {
             const float2 r = make_float2(rf[q], rf[q + 1]);
             const float2 a = make_float2(fabsf(rf[q]), fabsf(rf[q + 1]));
             const float2 c = __fadd2_rn(__ffma2_ru(a, s16, M2), nM2);          // ceil(|r|/16)
             const float2 d1 = make_float2(copysignf(c.x, r.x), copysignf(c.y, r.y));
             const float2 d2 = __ffma2_rn(d1, n16, r);
             const float2 d3 = __fadd2_rn(d1, d2);
-            w1 |= static_cast<uint32_t>(cvt_e4m3x2(d1.x, d1.y)) << (8 * q);
-            w2 |= static_cast<uint32_t>(cvt_e4m3x2(d2.x, d2.y)) << (8 * q);
-            w3 |= static_cast<uint32_t>(cvt_e4m3x2(d3.x, d3.y)) << (8 * q);
+            w1 |= static_cast<DWord>(cvt_e4m3x2(d1.x, d1.y)) << (8 * q);
+            w2 |= static_cast<DWord>(cvt_e4m3x2(d2.x, d2.y)) << (8 * q);
+            w3 |= static_cast<DWord>(cvt_e4m3x2(d3.x, d3.y)) << (8 * q);
         }
-        *reinterpret_cast<uint32_t*>(o) = w1;
-        *reinterpret_cast<uint32_t*>(o + plane_stride) = w2;
-        *reinterpret_cast<uint32_t*>(o + 2 * plane_stride) = w3;
+        *reinterpret_cast<DWord*>(o) = w1;
+        *reinterpret_cast<DWord*>(o + plane_stride) = w2;
+        *reinterpret_cast<DWord*>(o + 2 * plane_stride) = w3;
     }
 }
 
 template <int NSTEP, int NMOD, bool I8, int NSQ>
-__device__ __forceinline__ void digits_all_moduli(const DigitParams& dp, const double (&y)[4],
-                                                  const double (&M)[4], const int (&E)[4],
+__device__ __forceinline__ void digits_all_moduli(const DigitParams& dp, const double (&y)[kEPL],
+                                                  const double (&M)[kEPL], const int (&E)[kEPL],
                                                   uint8_t* out, int64_t plane_stride) {
     if (I8) {
         // INT8 scheme: one S8 plane per modulus, plane l
@@ -422,36 +435,36 @@ __device__ __forceinline__ void digits_all_moduli(const DigitParams& dp, const d
 // closer than 1/(2p) to a half-integer, so the rounding is exact.  Bit-identical to
 // digits_one_modulus<1, .> (same residues, same digit code).
 template <int NMOD, bool I8, int NSQ, int EVEN>
-__device__ __forceinline__ void digits_paired(const DigitParams& dp, const double (&y)[4], uint8_t* out,
+__device__ __forceinline__ void digits_paired(const DigitParams& dp, const double (&y)[kEPL], uint8_t* out,
                                               int64_t plane_stride) {
     const float2 M2 = make_float2(kMagic23, kMagic23), nM2 = make_float2(-kMagic23, -kMagic23);
 #pragma unroll
     for (int l = 0; l < NMOD; l += 2) {
         const double Q = dp.mod[l].q2_d, Qi = dp.mod[l].q2inv_d, magic = kMagic52;
-        float rq[4];
+        float rq[kEPL];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kEPL; ++q) {
             const double qq = dfma_rn(y[q], Qi, magic) - magic;
             const double rd = fma(-qq, Q, y[q]);                             // exact, |rd| < 2^21
             rq[q] = __int_as_float(0x4B400000 + __double2loint(rd + magic));  // r_Q + 1.5 2^23
         }
-        const float2 ra = __fadd2_rn(make_float2(rq[0], rq[1]), nM2);
-        const float2 rb = __fadd2_rn(make_float2(rq[2], rq[3]), nM2);
+        float2 r2[kEPL / 2];
+#pragma unroll
+        for (int q = 0; q < kEPL; q += 2) r2[q / 2] = __fadd2_rn(make_float2(rq[q], rq[q + 1]), nM2);
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             const int lm = l + u;
             if (lm >= NMOD) break;
             const ModDig& md = dp.mod[lm];
             const float2 pi2 = make_float2(md.pinv_f, md.pinv_f), np2 = make_float2(-md.p_f, -md.p_f);
-            float rf[4];
-            {
-                const float2 xa = (lm == EVEN) ? __fadd2_rn(ra, make_float2(0.5f, 0.5f)) : ra;
-                const float2 xb = (lm == EVEN) ? __fadd2_rn(rb, make_float2(0.5f, 0.5f)) : rb;
-                const float2 qa = __fadd2_rn(__ffma2_rn(xa, pi2, M2), nM2);
-                const float2 qb = __fadd2_rn(__ffma2_rn(xb, pi2, M2), nM2);
-                const float2 sa = __ffma2_rn(qa, np2, ra);
-                const float2 sb = __ffma2_rn(qb, np2, rb);
-                rf[0] = sa.x; rf[1] = sa.y; rf[2] = sb.x; rf[3] = sb.y;
+            float rf[kEPL];
+#pragma unroll
+            for (int q = 0; q < kEPL; q += 2) {
+                const float2 x = (lm == EVEN) ? __fadd2_rn(r2[q / 2], make_float2(0.5f, 0.5f)) : r2[q / 2];
+                const float2 qv = __fadd2_rn(__ffma2_rn(x, pi2, M2), nM2);
+                const float2 sv = __ffma2_rn(qv, np2, r2[q / 2]);
+                rf[q] = sv.x;
+                rf[q + 1] = sv.y;
             }
             if (I8) {
                 emit_digits<2>(md, rf, out + static_cast<int64_t>(lm) * plane_stride, plane_stride);
@@ -479,24 +492,28 @@ __global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, in
     __syncthreads();
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     const int64_t plane_stride = rows_pad * k_pad;
+    // a lane owns kEPL consecutive k of one row: kLPR lanes per row, 32 / kLPR rows per warp
+    constexpr int kLPR = TH / kEPL, kRPW = 32 / kLPR;
+    const int lrow = lane / kLPR, hl = (lane % kLPR) * kEPL;
 #pragma unroll 1
-    for (int j = 0; j < TR / 8; ++j) {
-        const int rr = w + 8 * j;
+    for (int j = 0; j < TR / (8 * kRPW); ++j) {
+        const int rr = (j * 8 + w) * kRPW + lrow;
         const int64_t r = r0 + rr;
-        const int e = (r < rows) ? e_scale[r] : 0;
+        int e = (r < rows) ? e_scale[r] : 0;
+        if (e == kExpNonFinite) e = 0;                    // NaN / Inf row: C gets NaN (R12)
         const double s1 = pow2d(e >> 1), s2 = pow2d(e - (e >> 1));
-        double y[4], M[4];
-        int E[4];
+        double y[kEPL], M[kEPL];
+        int E[kEPL];
         double amax = 0.0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const double v = (tile[rr * TP + lane * 4 + q] * s1) * s2;     // exact (eq. def:A')
+        for (int q = 0; q < kEPL; ++q) {
+            const double v = (tile[rr * TP + hl + q] * s1) * s2;           // exact (eq. def:A')
             double a = fabs(v);
             if (a < 4503599627370496.0) a = __dadd_rz(a, 4503599627370496.0) - 4503599627370496.0;  // trunc
             y[q] = copysign(a, v);
             amax = fmax(amax, a);
         }
-        uint8_t* out = planes + r * k_pad + h0 + lane * 4;
+        uint8_t* out = planes + r * k_pad + h0 + hl;
         // opaque per iteration: keeps the compiler from hoisting all M_N plane offsets
         // (64-bit each) out of the row loop into registers
         int64_t ps;
@@ -507,7 +524,7 @@ __global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, in
         if (need0) {
             // |X'| = M 2^E with M < 2^53 an integer (E = 0 below 2^53)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < kEPL; ++q) {
                 double a = fabs(y[q]);
                 int ee = 0;
                 if (a >= 9007199254740992.0) {

@@ -284,13 +284,23 @@ def test_identity_and_integer_exact(dev):
     assert np.array_equal(run(A, B, 12)["C"], want)
 
 
-def test_nonfinite_status(dev):
+@pytest.mark.parametrize("sch,mode", [("fp8", "accurate"), ("fp8", "fast"), ("int8", "accurate")])
+def test_nonfinite_status(dev, sch, mode):
+    """Reading R12: a NaN / Inf in row i of A (column j of B) sets the status word and
+    makes row i (column j) of C NaN; every other entry stays finite."""
     from gpu_helpers import run
     A = gen_host(20, 30, "uniform", seed=1)
     B = gen_host(30, 10, "uniform", seed=2)
     A[3, 4] = np.nan
-    res = run(A, B, 12)
+    B[7, 6] = np.inf
+    res = run(A, B, 12, scheme=sch, mode=mode)
     assert res["status"] == dev.OZ2_ERR_NONFINITE
+    C = res["C"]
+    assert np.all(np.isnan(C[3, :])) and np.all(np.isnan(C[:, 6]))
+    mask = np.ones(C.shape, dtype=bool)
+    mask[3, :] = False
+    mask[:, 6] = False
+    assert np.all(np.isfinite(C[mask]))
 
 
 def test_host_pointer_path(dev):
