@@ -239,6 +239,9 @@ def run_oz2(args, rank, world, local_rank):
                 "peak_source": (f"{peak_kind}: 2 x bf16_tflops_sustained (nominal fp8/bf16 = int8/bf16 = "
                                 "4.5/2.25)"),
                 "algorithmic_flops_per_launch": gemm_flops,
+                # the same against the spec-sheet dense peak (4.5 PFLOP/s FP8 = 4.5 POP/s INT8,
+                # P:85-86) at the boost clock; the power-capped step clock stays ~1.2-1.4 GHz
+                "frac_vs_nominal_4500": round(achieved / 4500.0, 4),
                 "share_of_step": round(gemm_ms / phases["total"], 4)}
     # rowmax x2, cast x2, [bound GEMM], exps, digits x2, residue GEMM, [k_crt unless fused]
     tiles = ((m + 255) // 256) * ((n + 255) // 256)

@@ -438,3 +438,42 @@ def test_residue_depth_boundaries(dev, sch, N):
     for l, p in enumerate(ps):
         want = scheme.modprod_direct(scheme.residues(Aint, p), scheme.residues(BintT, p), p)
         assert np.array_equal(res["residues"][l], want), p
+
+
+@pytest.mark.parametrize("sch", ["fp8", "int8"])
+def test_cuda_graph_capture(dev, sch):
+    """After a first call has built the plan and the workspace, oz2_dgemm only enqueues
+    asynchronous work on the library's stream, so it can be captured in a CUDA graph and
+    replayed (small shapes are launch-bound); replays give the direct call's bits."""
+    import torch
+    m, k, n, N = 384, 1000, 520, 13
+    A = torch.from_numpy(np.asfortranarray(gen_host(m, k, "phi", phi=1.0, seed=71))).cuda()
+    B = torch.from_numpy(np.asfortranarray(gen_host(k, n, "phi", phi=1.0, seed=72))).cuda()
+    Ad = A.t().contiguous().t()           # column-major storage
+    Bd = B.t().contiguous().t()
+    C_ref = torch.empty((n, m), dtype=torch.float64, device="cuda").t()
+    C_g = torch.empty((n, m), dtype=torch.float64, device="cuda").t()
+    assert dev.oz2_set_scheme(sch) == 0
+    try:
+        ws = torch.empty(dev.oz2_workspace_size("N", "N", m, n, k, N), dtype=torch.uint8, device="cuda")
+        dev.oz2_set_workspace(ws.data_ptr(), ws.numel())
+        call = lambda C: dev.oz2_dgemm("N", "N", m, n, k, 1.0, Ad.data_ptr(), m, Bd.data_ptr(), k, 0.0,
+                                       C.data_ptr(), m, N)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            dev.oz2_set_stream(s.cuda_stream)
+            assert call(C_ref) == 0                     # warm-up: plan + device constants
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            dev.oz2_set_stream(torch.cuda.current_stream().cuda_stream)
+            assert call(C_g) == 0
+        for _ in range(3):
+            C_g.zero_()
+            g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(C_g, C_ref)
+    finally:
+        dev.oz2_set_stream(torch.cuda.current_stream().cuda_stream)
+        dev.oz2_set_workspace(None, 0)
+        dev.oz2_set_scheme("fp8")
