@@ -53,22 +53,30 @@ __global__ void __launch_bounds__(256, 4) k_crt_n(const int16_t* __restrict__ re
             rp += ls2;
         }
         const int enu = e_nu[j];
+        // both rows accumulate in one pass over the moduli, so each CRT weight (a uniform
+        // constant) is fetched once per modulus for the two elements
+        uint64_t acc0[L], acc1[L];
+#pragma unroll
+        for (int t = 0; t < L; ++t) { acc0[t] = 0; acc1[t] = 0; }
+        uint64_t tacc0 = 0x80000000ull, tacc1 = 0x80000000ull;
+#pragma unroll
+        for (int l = 0; l < NM; ++l) {
+            const uint32_t u0 = rr[l] & 0xFFFFu, u1 = rr[l] >> 16;         // u_l in [0, p_l)
+            const uint32_t qp = cp.qp32[l];
+            tacc0 += static_cast<uint64_t>(u0) * qp;
+            tacc1 += static_cast<uint64_t>(u1) * qp;
+#pragma unroll
+            for (int t = 0; t < L; ++t) {
+                const uint32_t wv = cp.w[l][t];
+                acc0[t] += static_cast<uint64_t>(u0) * wv;
+                acc1[t] += static_cast<uint64_t>(u1) * wv;
+            }
+        }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            uint64_t acc[L];
-#pragma unroll
-            for (int t = 0; t < L; ++t) acc[t] = 0;
-            uint64_t tacc = 0x80000000ull;
-#pragma unroll
-            for (int l = 0; l < NM; ++l) {
-                const uint32_t u = h ? (rr[l] >> 16) : (rr[l] & 0xFFFFu);      // u_l in [0, p_l)
-                tacc += static_cast<uint64_t>(u) * cp.qp32[l];
-#pragma unroll
-                for (int t = 0; t < L; ++t) acc[t] += static_cast<uint64_t>(u) * cp.w[l][t];
-            }
             const int emu = h ? emu1 : emu0;
-            const double v = exps_finite(emu, enu) ? crt_finish<L>(acc, tacc, cp, emu + enu)
-                                                   : __longlong_as_double(0x7FF8000000000000ll);
+            const double v = !exps_finite(emu, enu) ? __longlong_as_double(0x7FF8000000000000ll)
+                           : h ? crt_finish<L>(acc1, tacc1, cp, emu + enu) : crt_finish<L>(acc0, tacc0, cp, emu + enu);
             store_alpha_beta(C + i + h + j * ldc, v, alpha, beta);
         }
     }
