@@ -87,8 +87,22 @@ __device__ __forceinline__ double crt_element(const int16_t* rp, int64_t lstride
     return crt_finish<L>(acc, tacc, cp, escale);
 }
 
+// rare path of crt_finish: the quotient estimate was off by one, C' outside [-P/2, P/2)
+template <int L>
+__device__ __noinline__ void crt_fix_range(uint32_t (&r)[L], const CrtParams& cp) {
+    if ((r[L - 1] >> 31) == 0u) {
+        if (cmp_limbs<L>(r, cp.halfP) >= 0) add_limbs<L>(r, cp.np);    // C' >= P/2: subtract P
+    } else {
+        uint32_t a[L];
+#pragma unroll
+        for (int t = 0; t < L; ++t) a[t] = r[t];
+        negate_limbs<L>(a);
+        if (cmp_limbs<L>(a, cp.halfP) > 0) add_limbs<L>(r, cp.P);       // C' < -P/2: add P
+    }
+}
+
 // the rest of the reconstruction from the accumulated S (L limbs of 64-bit partial sums)
-// and the fixed-point quotient estimate
+// and the fixed-point quotient estimate; branch-free on the common path
 template <int L>
 __device__ __forceinline__ double crt_finish(const uint64_t (&acc)[L], uint64_t tacc, const CrtParams& cp,
                                              int escale) {
@@ -101,60 +115,56 @@ __device__ __forceinline__ double crt_finish(const uint64_t (&acc)[L], uint64_t 
         r[t] = static_cast<uint32_t>(v);
         carry = v >> 32;
     }
-    bool negv = (r[L - 1] >> 31) != 0;
-    // fast path: with T the signed top limb and H_top that of P/2, -H_top <= T < H_top
-    // already puts C' in [-P/2, P/2) (the quotient estimate is almost never off by one)
-    const int T = static_cast<int>(r[L - 1]);
-    const int Ht = static_cast<int>(cp.halfP[L - 1]);
-    if (T >= Ht || T < -Ht) {
-        if (!negv) {
-            if (cmp_limbs<L>(r, cp.halfP) >= 0) {         // C' >= P/2: subtract P
-                add_limbs<L>(r, cp.np);
-                negv = (r[L - 1] >> 31) != 0;
-            }
-        } else {
-            uint32_t a[L];
+    // with T the signed top limb and H_top that of P/2, -H_top <= T < H_top already puts C'
+    // in [-P/2, P/2) (the quotient estimate is almost never off by one)
+    {
+        const int T = static_cast<int>(r[L - 1]);
+        const int Ht = static_cast<int>(cp.halfP[L - 1]);
+        if (T >= Ht || T < -Ht) crt_fix_range<L>(r, cp);
+    }
+    // |C'| in two's complement, branch-free: r ^= s, r += (s & 1) with s the sign mask
+    const uint32_t sm = static_cast<uint32_t>(static_cast<int>(r[L - 1]) >> 31);
+    const bool negv = sm != 0u;
+    {
+        uint64_t c = sm & 1u;
 #pragma unroll
-            for (int t = 0; t < L; ++t) a[t] = r[t];
-            negate_limbs<L>(a);
-            if (cmp_limbs<L>(a, cp.halfP) > 0) {          // C' < -P/2: add P
-                add_limbs<L>(r, cp.P);
-                negv = (r[L - 1] >> 31) != 0;
-            }
+        for (int t = 0; t < L; ++t) {
+            const uint64_t v = static_cast<uint64_t>(r[t] ^ sm) + c;
+            r[t] = static_cast<uint32_t>(v);
+            c = v >> 32;
         }
     }
-    if (negv) negate_limbs<L>(r);
-    uint32_t w2 = 0, w1 = r[1], w0 = r[0];
-    int top = 1;
-    bool found = false;
-    uint32_t below = 0;                                  // OR of limbs under the window
+    // 64-bit words, the top nonzero one found by selects
+    constexpr int NW = (L + 1) / 2;
+    uint64_t w[NW];
 #pragma unroll
-    for (int t = L - 1; t >= 2; --t) {
-        if (!found && r[t] != 0u) {
-            found = true;
-            top = t;
-            w2 = r[t];
-            w1 = r[t - 1];
-            w0 = r[t - 2];
-            uint32_t o = 0;
+    for (int q = 0; q < NW; ++q)
+        w[q] = static_cast<uint64_t>(r[2 * q]) | (2 * q + 1 < L ? static_cast<uint64_t>(r[2 * q + 1]) << 32 : 0ull);
+    uint64_t hiw = w[0], low = 0, below = 0;
+    int tp = 0;
 #pragma unroll
-            for (int u = 0; u < t - 2; ++u) o |= r[u];
+    for (int q = 1; q < NW; ++q) {
+        if (w[q] != 0ull) {                   // predicated selects (unrolled, no divergence)
+            tp = q;
+            hiw = w[q];
+            low = w[q - 1];
+            uint64_t o = 0;
+#pragma unroll
+            for (int u = 0; u + 1 < q; ++u) o |= w[u];
             below = o;
         }
     }
     double v;
     int ex;
-    if (!found) {
-        v = __ull2double_rn((static_cast<uint64_t>(w1) << 32) | w0);
+    if (tp == 0) {
+        v = __ull2double_rn(hiw);             // exact RNE of |C'| < 2^64
         ex = 0;
     } else {
-        const int lz = __clz(w2);
-        const uint64_t hi = (static_cast<uint64_t>(w2) << 32) | w1;
-        uint64_t top64 = lz ? (hi << lz) | (static_cast<uint64_t>(w0) >> (32 - lz)) : hi;
-        const bool sticky = (lz ? ((w0 << lz) != 0u) : (w0 != 0u)) || below != 0u;
-        top64 |= sticky ? 1ull : 0ull;
-        v = __ull2double_rn(top64);
-        ex = 32 * (top - 1) - lz;                        // |C'| ~ top64 * 2^ex
+        const int lz = __clzll(static_cast<long long>(hiw));
+        const uint64_t top64 = lz ? (hiw << lz) | (low >> (64 - lz)) : hiw;
+        const bool sticky = (lz ? ((low << lz) != 0ull) : (low != 0ull)) || below != 0ull;
+        v = __ull2double_rn(top64 | (sticky ? 1ull : 0ull));   // RNE from 64 bits + sticky
+        ex = 64 * tp - lz;                                     // |C'| ~ top64 * 2^ex
     }
     const int E = ex - escale;
     if (v != 0.0 && E >= -1022 && E <= 1023 - 64)
