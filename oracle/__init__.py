@@ -17,7 +17,9 @@ Modules
   fp8      E4M3 codec
   fp32     correctly directed rounding of rationals to binary32
   moduli   moduli families, P, q_l, CRT weights
-  scheme   the emulation steps in the paper's order
+  scheme   the emulation steps in the paper's order (P:151-182, P:220-381, P:501-524);
+           FP8 families: hybrid (the method) and Karatsuba-only
+  int8     the INT8 Ozaki-II baseline (bound and exponent rule: reading R16)
   exact    exact rational DGEMM references (for pins and accuracy metrics)
   models   matmul counts, M_N, workspace formulas (Table 2, eqs. M, W8i, W8f)
 

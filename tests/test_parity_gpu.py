@@ -477,3 +477,21 @@ def test_cuda_graph_capture(dev, sch):
         dev.oz2_set_stream(torch.cuda.current_stream().cuda_stream)
         dev.oz2_set_workspace(None, 0)
         dev.oz2_set_scheme("fp8")
+
+
+@pytest.mark.parametrize("m,k,n", [(1, 1, 1), (1, 257, 1), (300, 1, 2), (2, 3, 1), (1, 5000, 3), (257, 2, 255)])
+@pytest.mark.parametrize("sch", ["fp8", "int8", "karatsuba"])
+def test_degenerate_shapes(dev, m, k, n, sch):
+    """Vectors, k = 1 and sub-tile shapes: residues and C bit-exact against the oracle
+    (imported exponents, so the R6 rounding window cannot intervene)."""
+    from gpu_helpers import run
+    from oracle import int8
+    A = gen_host(m, k, "phi", phi=1.5, seed=m + 7 * k)
+    B = gen_host(k, n, "phi", phi=1.5, seed=n + 11 * k)
+    N = 13
+    ref = (int8.dgemm(A, B, N) if sch == "int8"
+           else scheme.dgemm(A, B, N, family="karatsuba" if sch == "karatsuba" else "hybrid"))
+    res = run(A, B, N, e_mu_in=ref.e_mu, e_nu_in=ref.e_nu, scheme=sch)
+    for l in range(N):
+        assert np.array_equal(res["residues"][l], ref.residues[l]), l
+    assert np.array_equal(res["C"], ref.C)
