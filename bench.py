@@ -242,7 +242,12 @@ def run_oz2(args, rank, world, local_rank):
                 # the same against the spec-sheet dense peak (4.5 PFLOP/s FP8 = 4.5 POP/s INT8,
                 # P:85-86) at the boost clock; the power-capped step clock stays ~1.2-1.4 GHz
                 "frac_vs_nominal_4500": round(achieved / 4500.0, 4),
-                "share_of_step": round(gemm_ms / phases["total"], 4)}
+                "share_of_step": round(gemm_ms / phases["total"], 4),
+                # compulsory DRAM bytes of the launch (every digit plane read once, residues
+                # written once); `traffic` (ncu) is higher because the 74 concurrent 256x256
+                # pair tiles re-read the panels of other tile rows/columns
+                "compulsory_bytes_per_launch": int(P.oz2_plan_query(N, k).num_planes * (m + n) * k
+                                                   + 2 * N * m * n)}
     # rowmax x2, cast x2, [bound GEMM], exps, digits x2, residue GEMM, [k_crt unless fused]
     tiles = ((m + 255) // 256) * ((n + 255) // 256)
     mod_split = tiles < 8 * (torch.cuda.get_device_properties(dev).multi_processor_count // 2)

@@ -25,8 +25,10 @@
 //                 each FP32 accumulator mod p (exact: entries are integers <= 2^24,
 //                 eq. error-free-FP8-matmult), accumulates the weighted partial in
 //                 registers (binary16 pairs, exact below 2048) and after the third
-//                 product stores C'_l = mod(.., p) as int16 [l][j][i].  The FP32
-//                 products never leave TMEM.
+//                 product stores C'_l mod p in [0, p) as 16 bits [l][j][i] (work
+//                 items: a tile with all moduli, or one (tile, modulus) pair when
+//                 mod_split); with FL > 0 the CRT of the previous tile is spread over
+//                 the epilogues (crt_common.cuh).  The FP32 products never leave TMEM.
 //   MODE_BOUND    C-bar' = A-bar B-bar; the epilogue keeps only the row and
 //                 column maxima (atomicMax on non-negative float bits).
 //   MODE_RAW      diagnostic: writes the FP32 accumulator.
