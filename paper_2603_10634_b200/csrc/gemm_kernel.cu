@@ -33,6 +33,7 @@
 //                 column maxima (atomicMax on non-negative float bits).
 //   MODE_RAW      diagnostic: writes the FP32 accumulator.
 #include <cstdint>
+#include <mutex>
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
 #include "oz2_internal.h"
@@ -520,18 +521,26 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     }
 }
 
+constexpr int kMaxDevices = 64;
+
 template <int MODE, int CG, int FL, int MC>
 static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& gp,
                               int num_sms, cudaStream_t st) {
-    static bool attr_set = false;
     using Cfg = GemmCfg<CG>;
     constexpr int CS = CG * MC;
     const int num_tiles = gp.m_tiles * (gp.n_tiles / MC);
     if (num_tiles == 0) return cudaSuccess;
     const int num_items = (MODE == MODE_RESIDUE || MODE == MODE_RESIDUE_I8) && gp.mod_split
                               ? num_tiles * gp.num_moduli : num_tiles;
-    static int max_clusters = 0;               // co-resident clusters of this configuration
-    if (!attr_set) {
+    // kernel attributes and the co-resident cluster count, once per device (attributes are
+    // per device; several host threads may launch concurrently)
+    static std::mutex mu;
+    static int max_clusters_dev[kMaxDevices] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(mu);
+    int& max_clusters = max_clusters_dev[dev];
+    if (max_clusters == 0) {
         cudaError_t err = cudaFuncSetAttribute(gemm_kernel<MODE, CG, FL, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
         if (err != cudaSuccess) return err;
         if (CS > 1) {
@@ -556,7 +565,6 @@ static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, cons
         } else {
             max_clusters = num_sms;
         }
-        attr_set = true;
     }
     // persistent grid: never more units than can be resident at once (the progress
     // throttle assumes every unit runs concurrently)
