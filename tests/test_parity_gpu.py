@@ -495,3 +495,52 @@ def test_degenerate_shapes(dev, m, k, n, sch):
     for l in range(N):
         assert np.array_equal(res["residues"][l], ref.residues[l]), l
     assert np.array_equal(res["C"], ref.C)
+
+
+def test_concurrent_host_threads(dev):
+    """The library state (stream, workspace, scheme, plans) is per host thread: two threads
+    running different schemes on their own streams at the same time get the bits of the
+    sequential calls."""
+    import threading
+    import torch
+    m, k, n = 700, 900, 600
+    A = torch.from_numpy(np.asfortranarray(gen_host(m, k, "phi", phi=1.0, seed=81))).cuda()
+    B = torch.from_numpy(np.asfortranarray(gen_host(k, n, "phi", phi=1.0, seed=82))).cuda()
+    Ad, Bd = A.t().contiguous().t(), B.t().contiguous().t()
+
+    def call(scheme, N, out):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            dev.oz2_set_stream(s.cuda_stream)
+            assert dev.oz2_set_scheme(scheme) == 0
+            for _ in range(3):
+                rc = dev.oz2_dgemm("N", "N", m, n, k, 1.0, Ad.data_ptr(), m, Bd.data_ptr(), k, 0.0,
+                                   out.data_ptr(), m, N)
+                assert rc == 0
+            s.synchronize()
+            dev.oz2_set_scheme("fp8")
+            dev.oz2_finalize()
+
+    jobs = [("fp8", 13), ("int8", 15), ("karatsuba", 14)]
+    seq = [torch.empty((n, m), dtype=torch.float64, device="cuda").t() for _ in jobs]
+    par = [torch.empty((n, m), dtype=torch.float64, device="cuda").t() for _ in jobs]
+    for (sch, N), o in zip(jobs, seq):
+        call(sch, N, o)
+    errors = []
+
+    def guarded(*a):
+        try:
+            call(*a)
+        except BaseException as e:      # surfaced below: a thread's assert must fail the test
+            errors.append(e)
+
+    threads = [threading.Thread(target=guarded, args=(sch, N, o)) for (sch, N), o in zip(jobs, par)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    torch.cuda.synchronize()
+    dev.oz2_set_stream(torch.cuda.current_stream().cuda_stream)
+    assert not errors, errors
+    for a, b in zip(seq, par):
+        assert torch.equal(a, b)
