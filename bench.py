@@ -248,6 +248,24 @@ def run_oz2(args, rank, world, local_rank):
                 # pair tiles re-read the panels of other tile rows/columns
                 "compulsory_bytes_per_launch": int(P.oz2_plan_query(N, k).num_planes * (m + n) * k
                                                    + 2 * N * m * n)}
+    # the HBM-bound conversion phases (north_star: achieved GB/s vs the HBM roofline):
+    # compulsory bytes / median phase time, against the measured copy bandwidth
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    nplanes = P.oz2_plan_query(N, k).num_planes
+    elems = (m + n) * k
+    hbm_bytes = {
+        "prescale": elems * (8 + 8 + (0 if args.mode == "fast" else 1)),   # rowmax read, cast read (+ write)
+        "digits": elems * (8 + nplanes),                                  # read X, write the digit planes
+    }
+    hbm_phases = {}
+    for ph, b in hbm_bytes.items():
+        t = phases.get(ph, 0.0)
+        if t > 0:
+            gbs = b / (t * 1e-3) / 1e9
+            hbm_phases[ph] = {"bytes": int(b), "gbs": round(gbs, 1), "frac_of_measured_hbm": round(gbs / hbm_peak, 3)}
+    hbm_phases["peak_gbs"] = hbm_peak
+    hbm_phases["note"] = ("phase times are CUDA events around both operands' kernels inside the step, "
+                          "at the power-capped clock; per-kernel ncu figures: profiles/round1_ncu_prep_16384.md")
     # rowmax x2, cast x2, [bound GEMM], exps, digits x2, residue GEMM, [k_crt unless fused]
     tiles = ((m + 255) // 256) * ((n + 255) // 256)
     mod_split = tiles < 8 * (torch.cuda.get_device_properties(dev).multi_processor_count // 2)
@@ -272,6 +290,7 @@ def run_oz2(args, rank, world, local_rank):
                                    if world > 1 else "single GPU")},
         "gpu_launches": launches_per_step * args.steps,
         "phases_ms": {k_: round(v, 3) for k_, v in phases.items()},
+        "hbm_phases": hbm_phases,
         "roofline": roofline,
         "clocks": clocks,
     }
