@@ -398,6 +398,13 @@ def run_oz2(args, rank, world, local_rank):
         msN = e0.elapsed_time(e1) / 3
         sweep[str(NN)] = {"tflops": round(flops_rank / (msN * 1e-3) / 1e12, 3), **errs(C[I][:, J].cpu().numpy())}
     acc["moduli_sweep"] = sweep
+    if args.scheme == "fp8" and args.mode == "accurate" and args.size == 16384 and "12" in sweep:
+        # the paper's own B200 figure is for accurate mode with N = 12;
+        # the headline uses N = 13 because N = 12 is less accurate than cuBLAS at k = 16384,
+        # so vs_baseline stays null and the like-for-like ratio is reported here
+        extras["paper_context"] = {"paper_tflops": 64.0, "paper_config": "B200, accurate, N=12, 16384^3 (P:709)",
+                                   "this_run_same_config_tflops": sweep["12"]["tflops"],
+                                   "ratio_same_config": round(sweep["12"]["tflops"] / 64.0, 3)}
     # the other scaling mode on the same inputs (fast N=13 ~ accurate N=12)
     other = "fast" if args.mode == "accurate" else "accurate"
     P.oz2_set_mode(other)
