@@ -197,3 +197,50 @@ def test_config5_rank_shard_fast_equals_unsharded(dev):
     full = _run_fast_light(dev, m * 2, k, n, 13, 1.0, 43, I, J)
     assert np.array_equal(shard["C"], full["C"])
     _check_light(full, 13, len(I), len(J))
+
+
+def test_karatsuba_16384_fast_sampled(dev):
+    """The Karatsuba-only family at the bench size in fast mode (exponents decided in exact
+    integers, R15): sampled C bit-exact against oracle.scheme with family="karatsuba"."""
+    N = 13
+    I, J = [7, 9001, 16383], [2, 15000]
+    dev.oz2_set_scheme("karatsuba")
+    try:
+        out = _run_fast_light(dev, 16384, 16384, 16384, N, 1.0, 51, I, J)
+    finally:
+        dev.oz2_set_scheme("fp8")
+    Ar, Bc = out["A_rows"], out["B_cols"]
+    plan, _, _ = scheme.plan_constants(N, "karatsuba")
+    eA, cA = scheme.prescale_rows(Ar)
+    eB, cB = scheme.prescale_rows(Bc.T.copy())
+    emu = scheme.fast_exponents(eA, cA, plan, [False] * len(I))
+    enu = scheme.fast_exponents(eB, cB, plan, [False] * len(J))
+    _, Cref = scheme.entries(Ar, Bc, N, list(range(len(I))), list(range(len(J))), emu, enu, family="karatsuba")
+    assert np.array_equal(out["C"], Cref)
+    ex = exact.exact_entries(Ar, Bc, range(len(I)), range(len(J)))
+    assert np.linalg.norm(out["C"] - ex) / np.linalg.norm(ex) < 2e-15
+
+
+def test_int8_config4_fast_sampled(dev):
+    """The INT8 scheme at config 4's shape (m = n = 4096, k = 65536 = its exactness limit),
+    fast mode: sampled C bit-exact against oracle.int8's definition (exponents from the
+    integer sums of squares of the U8 bounds, R16)."""
+    from oracle import int8
+    N = 15
+    I, J = [0, 2049, 4095], [5, 3000]
+    dev.oz2_set_scheme("int8")
+    try:
+        out = _run_fast_light(dev, 4096, 65536, 4096, N, 1.0, 53, I, J)
+    finally:
+        dev.oz2_set_scheme("fp8")
+    Ar, Bc = out["A_rows"], out["B_cols"]
+    pl = int8.plan(N)
+    eA, bA = int8.prescale_rows(Ar)
+    eB, bB = int8.prescale_rows(Bc.T.copy())
+    emu = int8.exponents(eA, [int(sum(int(v) ** 2 for v in r)) for r in bA], pl, [False] * len(I))
+    enu = int8.exponents(eB, [int(sum(int(v) ** 2 for v in r)) for r in bB], pl, [False] * len(J))
+    Aint = scheme.to_integral(Ar, emu)
+    BintT = scheme.to_integral(Bc.T.copy(), enu)
+    res = [scheme.modprod_direct(scheme.residues(Aint, p), scheme.residues(BintT, p), p) for p in pl.moduli]
+    Cref = scheme.inverse_scale(scheme.crt_combine(res, pl), emu, enu)
+    assert np.array_equal(out["C"], Cref)
