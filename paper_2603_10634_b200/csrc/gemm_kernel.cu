@@ -619,7 +619,7 @@ cudaError_t launch_gemm(int mode, int cg, int fused_limbs, const CUtensorMap& ta
                         const GemmParams& gp, int num_sms, cudaStream_t st) {
     cudaError_t err;
     if (cg == 4 && mode < MODE_RESIDUE_I8) err = launch_cg<2, 2>(mode, fused_limbs, ta, tb, gp, num_sms, st);
-    else if (cg == 4) err = launch_cg<2, 1>(mode, fused_limbs, ta, tb, gp, num_sms, st);
+    else if (cg == 4) return cudaErrorInvalidValue;       // no multicast variant of the kind::i8 kernels
     else if (cg == 2) err = launch_cg<2, 1>(mode, fused_limbs, ta, tb, gp, num_sms, st);
     else err = launch_cg<1, 1>(mode, fused_limbs, ta, tb, gp, num_sms, st);
     if (err != cudaSuccess) return err;

@@ -506,11 +506,11 @@ static int sync_lead() {   // progress throttle of the residue GEMM (OZ2_SYNC_LE
     return v < 0 ? 0 : v;
 }
 // 1: 128x256 CTA tiles; 2: 256x256 CTA-pair tiles; 4: two pairs per cluster sharing A by
-// TMA multicast (needs an even number of 256-column tiles, else 2)   (OZ2_CG)
-static int cta_group(int64_t n_pad) {
+// TMA multicast (FP8 kinds only; needs an even number of 256-column tiles, else 2) (OZ2_CG)
+static int cta_group(int64_t n_pad, bool i8) {
     const int v = env_int("OZ2_CG", 2);
     if (v == 1) return 1;
-    if (v == 4 && (n_pad / BN) % 2 == 0) return 4;
+    if (v == 4 && !i8 && (n_pad / BN) % 2 == 0) return 4;   // the kind::i8 kernels have no multicast variant
     return 2;
 }
 static int a_box_rows(int cg) { return cg == 4 ? BM / 2 : BM; }
@@ -616,7 +616,7 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
         // ---- step 2: bound GEMM C-bar' = A-bar B-bar, row/column maxima
         phase_mark(1);
         if (!fast) {
-            const int cg = cta_group(L.n_pad);
+            const int cg = cta_group(L.n_pad, i8);
             CUtensorMap ta, tb;
             if (!make_map(&ta, abar, L.k_pad, L.m_pad, L.k_pad, BK, a_box_rows(cg))) return OZ2_ERR_CUDA;
             if (!make_map(&tb, bbar, L.k_pad, L.n_pad, L.k_pad, BK, b_box_rows(cg))) return OZ2_ERR_CUDA;
@@ -692,7 +692,7 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
                 phase_mark(4);
             }
             // ---- step 5: 3N exact FP8 GEMMs with the modular epilogue
-            const int cg = cta_group(nbj_pad);
+            const int cg = cta_group(nbj_pad, i8);
             CUtensorMap ta, tb;
             if (!make_map(&ta, digA, L.k_pad, static_cast<uint64_t>(pl->M) * mbi_pad, L.k_pad, BK, a_box_rows(cg))) return OZ2_ERR_CUDA;
             if (!make_map(&tb, digB, L.k_pad, static_cast<uint64_t>(pl->M) * nbj_pad, L.k_pad, BK, b_box_rows(cg))) return OZ2_ERR_CUDA;
@@ -1031,7 +1031,7 @@ static int gemm_raw(int mode, const uint8_t* a, const uint8_t* b, float* C32, in
     if (e) return e;
     if (k == 0) { OZ2_CK(cudaMemsetAsync(C32, 0, 4ull * m * n, g_ts.stream)); return OZ2_SUCCESS; }
     if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15u) return OZ2_ERR_NOT_SUPPORTED;
-    const int cg = cta_group(((n + BN - 1) / BN) * BN);
+    const int cg = cta_group(((n + BN - 1) / BN) * BN, mode == MODE_RAW_I8);
     CUtensorMap ta, tb;
     if (!make_map(&ta, a, k, m, k, BK, a_box_rows(cg))) return OZ2_ERR_CUDA;
     if (!make_map(&tb, b, k, n, k, BK, b_box_rows(cg))) return OZ2_ERR_CUDA;

@@ -544,3 +544,45 @@ def test_concurrent_host_threads(dev):
     assert not errors, errors
     for a, b in zip(seq, par):
         assert torch.equal(a, b)
+
+
+_CG_SNIPPET = r"""
+import hashlib, sys
+import numpy as np, torch
+sys.path.insert(0, ".")
+import paper_2603_10634_b200 as P
+from synth import gen_device
+sch = sys.argv[1]
+m, n, k = 700, 1024, 3000
+A = gen_device(m, k, "phi", phi=1.0, seed=91)
+B = gen_device(k, n, "phi", phi=1.0, seed=92)
+C = torch.empty((n, m), dtype=torch.float64, device="cuda").t()
+P.oz2_set_stream(torch.cuda.current_stream().cuda_stream)
+assert P.oz2_set_scheme(sch) == 0
+for split in ("0", "1"):
+    import os
+    os.environ["OZ2_MOD_SPLIT"] = split
+    assert P.oz2_dgemm("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0, C.data_ptr(), m, 13) == 0
+    torch.cuda.synchronize()
+    print(split, hashlib.sha256(C.cpu().numpy().tobytes()).hexdigest())
+"""
+
+
+@pytest.mark.parametrize("sch", ["fp8", "int8", "karatsuba"])
+def test_gemm_variants_identical(dev, sch):
+    """OZ2_CG = 1 (128x256 CTAs), 2 (CTA pairs, default), 4 (two pairs multicasting A; FP8
+    kinds only, INT8 falls back to pairs) give identical C under both work-item schedules.
+    Each variant runs in a subprocess with a timeout, so a pipeline hang fails the test."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for cg in ["1", "2", "4"]:
+        env = dict(os.environ, OZ2_CG=cg)
+        r = subprocess.run([sys.executable, "-c", _CG_SNIPPET, sch], cwd=root, env=env,
+                           capture_output=True, text=True, timeout=240)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[cg] = r.stdout.split()
+    assert outs["1"] == outs["2"] == outs["4"]
+    assert outs["2"][1] == outs["2"][3]            # split and tile-major agree
