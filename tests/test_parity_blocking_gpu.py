@@ -124,3 +124,19 @@ def test_debug_outputs_force_unblocked(dev):
         dev.oz2_set_blocking(0, 0)
     ref = scheme.dgemm(A, B, 12, e_mu=out["e_mu"].tolist(), e_nu=out["e_nu"].tolist())
     assert np.array_equal(out["C"], ref.C)
+
+
+@pytest.mark.parametrize("sch", ["int8", "karatsuba"])
+@pytest.mark.parametrize("mode", ["accurate", "fast"])
+@pytest.mark.parametrize("mb,nb", [(256, 512), (512, 256)])
+def test_blocked_other_schemes(dev, sch, mode, mb, nb):
+    """The INT8 and Karatsuba-only schemes through m/n blocks: C and exponents identical to
+    the unblocked call of the same scheme (which the other files pin to the oracle)."""
+    m, k, n = 700, 900, 800
+    A = gen_host(m, k, "phi", phi=1.0, seed=95)
+    B = gen_host(k, n, "phi", phi=1.0, seed=96)
+    out, got = _run_blocked(dev, A, B, 14, mb, nb, scheme=sch, mode=mode)
+    assert got == (mb, nb)
+    full = run(A, B, 14, scheme=sch, mode=mode)
+    assert np.array_equal(out["e_mu"], full["e_mu"]) and np.array_equal(out["e_nu"], full["e_nu"])
+    assert np.array_equal(out["C"], full["C"])
