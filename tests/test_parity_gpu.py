@@ -392,15 +392,26 @@ def test_workspace_and_timing_api(dev):
     assert np.array_equal(C2.cpu().numpy(), ref)
 
 
-def test_k_beyond_exactness_window(dev):
+_LONGK_REF = {}
+
+
+@pytest.mark.parametrize("fam", ["hybrid", "karatsuba"])
+@pytest.mark.parametrize("sched", ["split", "tile_fused"])
+def test_k_beyond_exactness_window(dev, fam, sched, monkeypatch):
     """k > 2^16 (NEXT-2): products run in 2^16-long K segments reduced mod p; residues and C
-    stay bit-exact against the oracle, which needs no segmentation (exact integers)."""
+    stay bit-exact against the oracle, which needs no segmentation (exact integers) -- for
+    both FP8 families and both work-item schedules (tile-major with the fused CRT)."""
     from gpu_helpers import run
-    m, k, n, N = 16, 65536 + 300, 24, 12
+    m, k, n, N = 16, 65536 + 300, 24, 12 if fam == "hybrid" else 13
+    if sched == "tile_fused":
+        monkeypatch.setenv("OZ2_MOD_SPLIT", "0")
+        monkeypatch.setenv("OZ2_FUSED_CRT", "1")
     A = gen_host(m, k, "phi", phi=1.0, seed=61)
     B = gen_host(k, n, "phi", phi=1.0, seed=62)
-    ref = scheme.dgemm(A, B, N)
-    res = run(A, B, N, e_mu_in=ref.e_mu, e_nu_in=ref.e_nu)
+    if fam not in _LONGK_REF:
+        _LONGK_REF[fam] = scheme.dgemm(A, B, N, family=fam)
+    ref = _LONGK_REF[fam]
+    res = run(A, B, N, e_mu_in=ref.e_mu, e_nu_in=ref.e_nu, scheme="fp8" if fam == "hybrid" else "karatsuba")
     for l in range(N):
         assert np.array_equal(res["residues"][l], ref.residues[l]), l
     assert np.array_equal(res["C"], ref.C)
