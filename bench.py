@@ -267,11 +267,18 @@ def run_oz2(args, rank, world, local_rank):
     hbm_phases["note"] = ("phase times are CUDA events around both operands' kernels inside the step, "
                           "at the power-capped clock; per-kernel ncu figures: profiles/round1_ncu_prep_16384.md")
     # rowmax x2, cast x2, [bound GEMM], exps, digits x2, residue GEMM, [k_crt unless fused]
+    # the library's work-item rule (oz2_api.cu): all split below 8 tiles per CTA pair, else
+    # tile-major, or hybrid (split tail wave, separate CRT) when the last wave is ragged
     tiles = ((m + 255) // 256) * ((n + 255) // 256)
-    mod_split = tiles < 8 * (torch.cuda.get_device_properties(dev).multi_processor_count // 2)
+    units = torch.cuda.get_device_properties(dev).multi_processor_count // 2
+    waves = -(-tiles // units)
+    ms_env = int(os.environ.get("OZ2_MOD_SPLIT", "-1"))
+    ragged = tiles % units != 0 and (waves * units - tiles) > 0.005 * waves * units
     fenv = int(os.environ.get("OZ2_FUSED_CRT", "-1"))
-    fused = (P.oz2_plan_query(N, k).num_limbs <= 6 and k >= 8192 and not mod_split
-             and (fenv > 0 or (fenv < 0 and k >= (49152 if args.scheme == "int8" else 16384))))
+    fusable = (P.oz2_plan_query(N, k).num_limbs <= 6 and k >= 8192
+               and (fenv > 0 or (fenv < 0 and k >= (49152 if args.scheme == "int8" else 16384))))
+    mod_split = (ms_env == 1 or ms_env == 2) or (ms_env < 0 and (tiles < 8 * units or (ragged and not fusable)))
+    fused = fusable and not mod_split
     launches_per_step = 8 + (args.mode == "accurate") + (not fused)
 
     out = {

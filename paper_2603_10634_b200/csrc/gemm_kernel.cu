@@ -214,10 +214,18 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     // for grids with few tiles -- one (tile, modulus) pair, modulus-major over the tiles so
     // that concurrently running units share that modulus' operand panels; the residue of
     // every modulus is independent, only the (then separate) CRT needs them all
-    const int mod_split = (MODE == MODE_RESIDUE) ? P.mod_split : 0;
-    const int num_items = mod_split ? num_tiles * P.num_moduli : num_tiles;
-    const int mods_per_item = (MODE == MODE_RESIDUE) ? (mod_split ? 1 : P.num_moduli) : 0;
-    const int prods = (MODE == MODE_RESIDUE) ? NP * mods_per_item * nseg : 1;
+    // P.tail_head: tiles [0, head) are tile-major items, tiles [head, num_tiles) are split
+    // into (tile, modulus) items (mod_split: head = 0; the hybrid schedule: head = the full
+    // waves, so the last partial wave is spread over all units)
+    const int head = (MODE == MODE_RESIDUE) ? min(P.tail_head, num_tiles) : num_tiles;
+    const int tail = num_tiles - head;
+    const int NMOD = (MODE == MODE_RESIDUE) ? P.num_moduli : 1;
+    const int num_items = head + tail * NMOD;
+    // item -> (tile, first modulus, moduli count)
+    auto item_tile = [&](int it) { return it < head ? it : head + (it - head) % tail; };
+    auto item_l0 = [&](int it) { return it < head ? 0 : (it - head) / tail; };
+    auto item_nmods = [&](int it) { return it < head ? NMOD : 1; };
+    auto item_prods = [&](int it) { return (MODE == MODE_RESIDUE) ? NP * item_nmods(it) * nseg : 1; };
     const int unit = blockIdx.x / CS;            // tile-processing unit (cluster)
     const int units = gridDim.x / CS;
 
@@ -233,8 +241,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             const uint32_t full0 = smem_u32(&full[0]) & 0xFEFFFFFFu;   // pair leader's barrier (TMA operand)
             const uint32_t full_leader = (CS > 1) ? mapa_shared(smem_u32(&full[0]), crank & ~(CG - 1u)) : 0u;
             for (int it = unit; it < num_items; it += units) {
-                const int tile = mod_split ? it % num_tiles : it;
-                const int l0 = mod_split ? it / num_tiles : 0;
+                const int tile = item_tile(it);
+                const int l0 = item_l0(it);
+                const int prods = item_prods(it);
                 int tm, tn;
                 tile_coords<16 / CG>(tile, P.m_tiles, n_super, tm, tn);
                 tn = tn * MC + static_cast<int>(pairi);
@@ -297,7 +306,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             }
             if (P.sync_lead > 0 && crank == 0) {
                 // finished: count as having started every product so nobody waits on us
-                const long long gmax = static_cast<long long>((num_items + units - 1) / units) * prods * chunks_per_prod;
+                // upper bound of any unit's chunk count (round-robin: <= ceil(head / units)
+                // whole-tile items and <= ceil(tail items / units) single-modulus items)
+                const long long gmax = (static_cast<long long>((head + units - 1) / units) * (MODE == MODE_RESIDUE ? NP * NMOD * nseg : 1)
+                                        + static_cast<long long>((tail * NMOD + units - 1) / units) * NP * nseg)
+                                       * chunks_per_prod;
                 if (gmax > g) atomicAdd(P.progress, static_cast<unsigned long long>(gmax - g));
             }
         }
@@ -308,6 +321,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                                           : make_idesc_e4m3_f32(Cfg::TILE_M, BN);
             uint32_t stage = 0, phase = 0, g = 0;
             for (int it = unit; it < num_items; it += units) {
+                const int prods = item_prods(it);
                 for (int pr = 0; pr < prods; ++pr, ++g) {
                     const uint32_t slot = g & 1u, use = g >> 1;
                     mbar_wait(&tempty[slot], (use & 1u) ^ 1u);
@@ -382,8 +396,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         };
         uint32_t g = 0;
         for (int it = unit; it < num_items; it += units) {
-            const int tile = mod_split ? it % num_tiles : it;
-            const int l0 = mod_split ? it / num_tiles : 0;
+            const int tile = item_tile(it);
+            const int l0 = item_l0(it);
+            const int mods_per_item = item_nmods(it);
             int tm, tn;
             tile_coords<16 / CG>(tile, P.m_tiles, n_super, tm, tn);
             tn = tn * MC + static_cast<int>(pairi);
@@ -530,8 +545,9 @@ static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, cons
     constexpr int CS = CG * MC;
     const int num_tiles = gp.m_tiles * (gp.n_tiles / MC);
     if (num_tiles == 0) return cudaSuccess;
-    const int num_items = (MODE == MODE_RESIDUE || MODE == MODE_RESIDUE_I8) && gp.mod_split
-                              ? num_tiles * gp.num_moduli : num_tiles;
+    const bool res_mode = MODE == MODE_RESIDUE || MODE == MODE_RESIDUE_I8;
+    const int head = res_mode ? (gp.tail_head < num_tiles ? gp.tail_head : num_tiles) : num_tiles;
+    const int num_items = head + (num_tiles - head) * (res_mode ? gp.num_moduli : 1);
     // kernel attributes and the co-resident cluster count, once per device (attributes are
     // per device; several host threads may launch concurrently)
     static std::mutex mu;

@@ -1,6 +1,7 @@
 // oz2_api.cu -- the C ABI (include/oz2.h): argument checking, the host planner
 // (moduli, CRT constants, P', delta, f_k), workspace carving, TMA descriptors and the
 // launch sequence of the FP8 Ozaki-II pipeline.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -704,13 +705,24 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             gp.m_tiles = static_cast<int>(mbi_pad / tile_m(cg)); gp.n_tiles = static_cast<int>(nbj_pad / BN);
             gp.rows_per_plane_a = static_cast<int>(mbi_pad); gp.rows_per_plane_b = static_cast<int>(nbj_pad);
             gp.num_moduli = N;
-            {   // few tiles (< 8 per persistent unit): one work item per (tile, modulus)
-                const int64_t tiles = static_cast<int64_t>(gp.m_tiles) * gp.n_tiles;
-                const int64_t units = g_ts.num_sms / (cg == 1 ? 1 : 2);
-                const int ms = env_int("OZ2_MOD_SPLIT", -1);
-                gp.mod_split = (ms >= 0) ? (ms > 0 ? 1 : 0) : (tiles < 8 * units ? 1 : 0);
+            {   // work items (OZ2_MOD_SPLIT: -1 auto, 0 tile-major, 1 all (tile, modulus),
+                // 2 hybrid): few tiles (< 8 per persistent unit) -> all split; otherwise
+                // tile-major, with the last partial wave split over all units (hybrid) when
+                // it would leave more than 0.5 % of the unit-time idle
+                const int64_t tiles = static_cast<int64_t>(gp.m_tiles) * gp.n_tiles / (cg == 4 ? 2 : 1);
+                const int64_t units = std::max<int64_t>(1, g_ts.num_sms / (cg == 1 ? 1 : cg == 4 ? 4 : 2));
+                const int64_t full = tiles / units * units;
+                const int64_t waves = (tiles + units - 1) / units;
+                const bool ragged = full < tiles && static_cast<double>(waves * units - tiles) > 0.005 * waves * units;
+                int ms = env_int("OZ2_MOD_SPLIT", -1);
+                // hybrid only where the CRT runs separately anyway: giving up the fused CRT
+                // for the tail costs more than the tail (A/B: FP8 16384^3 -1.5 %, 8192^3 +3.4 %)
+                if (ms < 0) ms = tiles < 8 * units ? 1 : (ragged && !fused ? 2 : 0);
+                gp.tail_head = static_cast<int>(ms == 1 ? 0 : ms == 2 ? full : tiles);
             }
-            const int fused_blk = gp.mod_split ? 0 : fused;      // the CRT needs every modulus of a tile
+            // the fused CRT needs every modulus of a tile in one item
+            const int n_tiles_blk = gp.m_tiles * gp.n_tiles / (cg == 4 ? 2 : 1);
+            const int fused_blk = gp.tail_head < n_tiles_blk ? 0 : fused;
             gp.residues = res;
             gp.sync_lead = sync_lead();
             gp.sync_chunk = sync_chunk;

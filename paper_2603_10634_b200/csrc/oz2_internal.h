@@ -67,7 +67,8 @@ struct GemmParams {
     int rows_per_plane_a;        // m_pad
     int rows_per_plane_b;        // n_pad
     int num_moduli;
-    int mod_split;               // residue mode: one work item per (tile, modulus) (no fused CRT)
+    int tail_head;               // residue mode: tiles [0, head) tile-major, the rest as
+                                 // (tile, modulus) items (no fused CRT unless head = all tiles)
     int16_t* residues;           // [N][n][m]
     uint32_t* rmax;              // [m] float bits (bound)
     uint32_t* smax;              // [n]

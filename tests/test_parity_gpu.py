@@ -252,6 +252,10 @@ def test_work_item_schedules_agree_many_tiles(dev, sch, monkeypatch):
     monkeypatch.setenv("OZ2_MOD_SPLIT", "0")
     outs.append(run(A, B, N, scheme=sch))
     assert np.array_equal(outs[0]["C"], outs[2]["C"])
+    monkeypatch.setenv("OZ2_MOD_SPLIT", "2")        # hybrid: full waves tile-major, tail split
+    outs.append(run(A, B, N, scheme=sch))
+    assert np.array_equal(outs[0]["residues"], outs[3]["residues"])
+    assert np.array_equal(outs[0]["C"], outs[3]["C"])
     assert np.array_equal(outs[0]["e_mu"], outs[1]["e_mu"])
     assert np.array_equal(outs[0]["residues"], outs[1]["residues"])
     assert np.array_equal(outs[0]["C"], outs[1]["C"])
@@ -564,13 +568,13 @@ sys.path.insert(0, ".")
 import paper_2603_10634_b200 as P
 from synth import gen_device
 sch = sys.argv[1]
-m, n, k = 700, 1024, 3000
+m, n, k = 2560, 2560, 1024          # 100 CTA-pair tiles: hybrid = 74 tile-major + a split tail
 A = gen_device(m, k, "phi", phi=1.0, seed=91)
 B = gen_device(k, n, "phi", phi=1.0, seed=92)
 C = torch.empty((n, m), dtype=torch.float64, device="cuda").t()
 P.oz2_set_stream(torch.cuda.current_stream().cuda_stream)
 assert P.oz2_set_scheme(sch) == 0
-for split in ("0", "1"):
+for split in ("0", "1", "2"):
     import os
     os.environ["OZ2_MOD_SPLIT"] = split
     assert P.oz2_dgemm("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0, C.data_ptr(), m, 13) == 0
@@ -596,4 +600,4 @@ def test_gemm_variants_identical(dev, sch):
         assert r.returncode == 0, r.stderr[-2000:]
         outs[cg] = r.stdout.split()
     assert outs["1"] == outs["2"] == outs["4"]
-    assert outs["2"][1] == outs["2"][3]            # split and tile-major agree
+    assert outs["2"][1] == outs["2"][3] == outs["2"][5]   # tile-major, split and hybrid agree
