@@ -601,3 +601,19 @@ def test_gemm_variants_identical(dev, sch):
         outs[cg] = r.stdout.split()
     assert outs["1"] == outs["2"] == outs["4"]
     assert outs["2"][1] == outs["2"][3] == outs["2"][5]   # tile-major, split and hybrid agree
+
+
+@pytest.mark.parametrize("ea,eb", [(-600, -400), (500, 500), (-1030, 1000)])
+def test_extreme_exponent_ranges(dev, ea, eb):
+    """Inputs far from 1 (rows of A scaled by 2^ea, columns of B by 2^eb, including
+    subnormal A entries for ea = -1030): the power-of-two pre/post scaling stays exact, so
+    exponents, residues and C match the oracle bit for bit (results stay normal binary64)."""
+    from gpu_helpers import run
+    m, k, n = 40, 300, 30
+    A = gen_host(m, k, "phi", phi=1.0, seed=97) * 2.0 ** ea
+    B = gen_host(k, n, "phi", phi=1.0, seed=98) * 2.0 ** eb
+    ref = scheme.dgemm(A, B, 13)
+    res = run(A, B, 13)
+    mask = _compare(res, ref, A, B, 13)
+    assert mask.all()
+    assert np.all(np.isfinite(res["C"]))
