@@ -215,6 +215,23 @@ def run_oz2(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total = t.item()
+    bcast = None
+    if world > 1:
+        # the one collective of the path (north_star): B broadcast from rank 0, timed alone
+        # on the device (max over ranks), for the scaling analysis
+        torch.cuda.synchronize()
+        dist.barrier()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record()
+        for _ in range(3):
+            dist.broadcast(Bt, src=0)
+        b1.record()
+        torch.cuda.synchronize()
+        tb = torch.tensor([b0.elapsed_time(b1) / 3], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tb, op=dist.ReduceOp.MAX)
+        bms = tb.item()
+        bcast = {"ms": round(bms, 3), "bytes": 8 * k * n, "algbw_gbs": round(8 * k * n / (bms * 1e-3) / 1e9, 1),
+                 "share_of_step": round(bms / (ms_total / args.steps), 4), "backend": dist.get_backend()}
     ms_per_step = ms_total / args.steps
     flops_rank = 2.0 * m * n * k
     value = world * flops_rank * args.steps / (ms_total * 1e-3) / 1e12
@@ -300,6 +317,7 @@ def run_oz2(args, rank, world, local_rank):
         "hbm_phases": hbm_phases,
         "roofline": roofline,
         "clocks": clocks,
+        **({"broadcast_B": bcast} if bcast else {}),
     }
     # ---- e2e on every rank: pinned HOST buffers through the same C ABI; B goes host ->
     # rank 0 -> broadcast inside the step, A's row block and C's row block host <-> each rank
