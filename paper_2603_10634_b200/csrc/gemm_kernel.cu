@@ -233,6 +233,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         // ------------------------------------------------------------ TMA producer
         if (elect_one()) {
             uint32_t stage = 0, phase = 0;
+            const uint64_t hint_a = P.hint_a ? P.hint_a : kEvictNormal, hint_b = P.hint_b ? P.hint_b : kEvictNormal;
             long long g = 0;                         // throttle chunks started by this unit
             bool throttle_on = true;
             const long long nunits = units;
@@ -283,22 +284,22 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         mbar_wait(&empty[stage], phase ^ 1);
                         if (CG == 1) {
                             mbar_arrive_expect_tx(&full[stage], Cfg::A_STAGE + Cfg::B_STAGE);
-                            tma_load_2d(&tmA, &full[stage], sA + stage * Cfg::A_STAGE, kb * BK, a_row, kEvictNormal);
-                            tma_load_2d(&tmB, &full[stage], sB + stage * Cfg::B_STAGE, kb * BK, b_row, kEvictNormal);
+                            tma_load_2d(&tmA, &full[stage], sA + stage * Cfg::A_STAGE, kb * BK, a_row, hint_a);
+                            tma_load_2d(&tmB, &full[stage], sB + stage * Cfg::B_STAGE, kb * BK, b_row, hint_b);
                         } else {
                             const uint32_t lb = full0 + stage * 8u;
                             if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (Cfg::A_STAGE + Cfg::B_STAGE));
                             else mbar_arrive_cluster(full_leader + stage * 8u);
                             if (MC == 1) {
-                                tma_load_2d_cg2(&tmA, lb, sA + stage * Cfg::A_STAGE, kb * BK, a_row, kEvictNormal);
+                                tma_load_2d_cg2(&tmA, lb, sA + stage * Cfg::A_STAGE, kb * BK, a_row, hint_a);
                             } else {
                                 // this CTA's half of the A tile, multicast to the CTA with the same
                                 // rank in the other pair (which loads the other half for both)
                                 const uint16_t amask = static_cast<uint16_t>((1u << rank) | (1u << (rank + CG)));
                                 tma_load_2d_cg2_mc(&tmA, lb, sA + stage * Cfg::A_STAGE + pairi * (Cfg::A_STAGE / 2),
-                                                   kb * BK, a_row, amask, kEvictNormal);
+                                                   kb * BK, a_row, amask, hint_a);
                             }
-                            tma_load_2d_cg2(&tmB, lb, sB + stage * Cfg::B_STAGE, kb * BK, b_row, kEvictNormal);
+                            tma_load_2d_cg2(&tmB, lb, sB + stage * Cfg::B_STAGE, kb * BK, b_row, hint_b);
                         }
                         if (++stage == NS) { stage = 0; phase ^= 1; }
                     }

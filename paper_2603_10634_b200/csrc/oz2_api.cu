@@ -726,6 +726,13 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             gp.residues = res;
             gp.sync_lead = sync_lead();
             gp.sync_chunk = sync_chunk;
+            {   // OZ2_TMA_HINT_A / _B: 0 evict-normal (default), 1 evict-last, 2 evict-first
+                auto hint = [](int v) -> unsigned long long {
+                    return v == 1 ? 0x14F0000000000000ull : v == 2 ? 0x12F0000000000000ull : 0x1000000000000000ull;
+                };
+                gp.hint_a = hint(env_int("OZ2_TMA_HINT_A", 0));
+                gp.hint_b = hint(env_int("OZ2_TMA_HINT_B", 0));
+            }
             if (gp.sync_lead > 0) {
                 gp.progress = reinterpret_cast<unsigned long long*>(maxbits);   // dead after step 3
                 OZ2_CK(cudaMemsetAsync(gp.progress, 0, 8, st));

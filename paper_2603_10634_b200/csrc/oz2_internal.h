@@ -81,6 +81,7 @@ struct GemmParams {
     double* C;
     int64_t ldc;
     CrtParams crt;
+    unsigned long long hint_a, hint_b;   // L2 cache policies of the operand TMA loads
     int sync_lead;               // 0 = off; else max chunks ahead of the chip-wide average
     int sync_chunk;              // k-blocks per throttle chunk (0 = one chunk per product)
     ModEpi mod[kMaxModuli];
