@@ -289,9 +289,9 @@ def run_oz2(args, rank, world, local_rank):
     tiles = ((m + 255) // 256) * ((n + 255) // 256)
     units = torch.cuda.get_device_properties(dev).multi_processor_count // 2
     waves = -(-tiles // units)
-    ms_env = int(os.environ.get("OZ2_MOD_SPLIT", "-1"))
+    ms_env = P.oz2_get_tuning("mod_split")
     ragged = tiles % units != 0 and (waves * units - tiles) > 0.005 * waves * units
-    fenv = int(os.environ.get("OZ2_FUSED_CRT", "-1"))
+    fenv = P.oz2_get_tuning("fused_crt")
     fusable = (P.oz2_plan_query(N, k).num_limbs <= 6 and k >= 8192
                and (fenv > 0 or (fenv < 0 and k >= (49152 if args.scheme == "int8" else 16384))))
     mod_split = (ms_env == 1 or ms_env == 2) or (ms_env < 0 and (tiles < 8 * units or (ragged and not fusable)))

@@ -121,7 +121,15 @@ typedef struct oz2_options {
     /* inputs */
     const int32_t* e_mu_in; /* [m]  if non-NULL together with e_nu_in: use these scaling */
     const int32_t* e_nu_in; /* [n]  exponents and skip steps 1-3             */
-    int32_t reserved[8];    /* must be zero                                               */
+    /* per-call settings (override the thread's oz2_set_mode / oz2_set_scheme /
+     * oz2_set_timing for this call only) */
+    float*  timing_ms;      /* HOST [7] or NULL: this call's phase times in ms, layout of
+                               oz2_get_timing; the call then synchronises its stream      */
+    int32_t set_mode;       /* nonzero: run this call in `mode`                           */
+    int32_t mode;           /* OZ2_MODE_ACCURATE / OZ2_MODE_FAST                          */
+    int32_t set_scheme;     /* nonzero: run this call with `scheme`                       */
+    int32_t scheme;         /* OZ2_SCHEME_*                                               */
+    int32_t reserved[4];    /* must be zero                                               */
 } oz2_options;
 
 int oz2_dgemm_ex(char transa, char transb, int64_t m, int64_t n, int64_t k,
@@ -206,8 +214,57 @@ int oz2_get_status(int32_t* status);
 int oz2_set_timing(int enable);
 int oz2_get_timing(float* ms_out, int n);
 
-/* Frees library-owned buffers and cached plans of this host thread. */
+/* Frees library-owned buffers and cached plans of this host thread (on every device it
+ * used).  A thread that exits without calling it has them freed by its thread-local
+ * destructor. */
 int oz2_finalize(void);
+
+/* ---- tuning knobs (per host thread; defaults are the measured best) ------------
+ *
+ * Every setting gives bit-identical results; they only change the kernel schedule.
+ * Read at each call (no environment variables are consulted by the library).
+ *
+ *   OZ2_TUNE_CTA_GROUP   2    residue/bound GEMM tile: 1 = 128x256 single CTA, 2 =
+ *                             256x256 CTA pair (tcgen05 cta_group::2), 4 = two pairs
+ *                             sharing A by TMA multicast (FP8 kinds; INT8 uses 2)
+ *   OZ2_TUNE_SYNC_LEAD   1    progress throttle: chunks a pair may lead the chip-wide
+ *                             average (0 = off)
+ *   OZ2_TUNE_SYNC_CHUNK  8    k-blocks per throttle chunk (power of two, 1..512)
+ *   OZ2_TUNE_L2_PROMO    3    L2 promotion of TMA misses: 0 none, 1 64 B, 2 128 B, 3 256 B
+ *   OZ2_TUNE_MAX_UNITS   0    cap on persistent CTA pairs (0 = all; power-wall study)
+ *   OZ2_TUNE_TMA_HINT_A  0    L2 policy of A's operand loads: 0 normal, 1 evict-last,
+ *   OZ2_TUNE_TMA_HINT_B  0      2 evict-first (same for B)
+ *   OZ2_TUNE_MOD_SPLIT  -1    residue-GEMM work items: -1 auto, 0 tile-major, 1 (tile,
+ *                             modulus), 2 hybrid (tail wave split)
+ *   OZ2_TUNE_FUSED_CRT  -1    CRT in the GEMM epilogue: -1 auto, 0 never, 1 whenever
+ *                             the limbs <= 6 and k >= 8192
+ *   OZ2_TUNE_SQ_ORDER    1    square-modulus product order: 1 = A1B2, A2B2, A2B1 (L2
+ *                             reuse), 0 = the order of eq. 3matmult-notKaratsuba
+ *   OZ2_TUNE_CRT_GENERIC 0    1 = the generic standalone CRT kernel (A/B reference)
+ *   OZ2_TUNE_HOST_BLOCKS 4    host-pointer calls with pinned C: column blocks of C whose
+ *                             device-to-host copies overlap the GEMMs (1 = off)
+ *   OZ2_TUNE_KCAT        1    square moduli: accumulate A1B2 + A2B1 in one TMEM
+ *                             accumulator (K-concatenated) when k <= 2^15
+ *
+ * oz2_set_tuning returns -1 for an unknown knob, -2 for a value out of range;
+ * oz2_get_tuning writes the current value. */
+#define OZ2_TUNE_CTA_GROUP    0
+#define OZ2_TUNE_SYNC_LEAD    1
+#define OZ2_TUNE_SYNC_CHUNK   2
+#define OZ2_TUNE_L2_PROMO     3
+#define OZ2_TUNE_MAX_UNITS    4
+#define OZ2_TUNE_TMA_HINT_A   5
+#define OZ2_TUNE_TMA_HINT_B   6
+#define OZ2_TUNE_MOD_SPLIT    7
+#define OZ2_TUNE_FUSED_CRT    8
+#define OZ2_TUNE_SQ_ORDER     9
+#define OZ2_TUNE_CRT_GENERIC 10
+#define OZ2_TUNE_HOST_BLOCKS 11
+#define OZ2_TUNE_KCAT        12
+#define OZ2_TUNE_COUNT       13
+int oz2_set_tuning(int knob, int value);
+int oz2_get_tuning(int knob, int* value);
+void oz2_reset_tuning(void);
 
 /* ---- host-only queries (no device needed) -------------------------------------- */
 

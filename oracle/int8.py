@@ -124,3 +124,37 @@ def dgemm(A: np.ndarray, B: np.ndarray, N: int, alpha: float = 1.0, beta: float 
     r.extra["Aint"] = Aint
     r.extra["BintT"] = BintT
     return r
+
+
+def prescale_rows_fast(X: np.ndarray):
+    """Vectorised prescale_rows (same definition; pinned equal in tests): ldexp by the
+    row exponent is exact for normal results, and a nonzero entry whose scaled value
+    underflows still gets the upper bound 1."""
+    X = np.asarray(X, dtype=np.float64)
+    rows, k = X.shape
+    ax = np.abs(X)
+    mx = ax.max(axis=1) if k else np.zeros(rows)
+    e_prime = np.zeros(rows, dtype=np.int64)
+    nz = mx > 0
+    _, ex = np.frexp(mx[nz])
+    e_prime[nz] = 6 - (ex - 1)
+    y = np.ceil(np.ldexp(ax, np.broadcast_to(e_prime[:, None], ax.shape)))
+    y = np.where((ax > 0) & (y == 0), 1.0, y)
+    return e_prime.tolist(), y.astype(np.int64)
+
+
+def row_exponents(X: np.ndarray, rows, Y_T: np.ndarray, N: int, mode: str = "accurate"):
+    """e' and log2 mu for selected rows r of X against the full other operand Y_T
+    (accurate mode: R_r = max_j (A-bar B-bar)_rj, exact; fast: S_r = sum_h abar_rh^2)."""
+    pl = plan(N)
+    rows = list(rows)
+    e1, xb = prescale_rows_fast(np.ascontiguousarray(X[rows]))
+    if mode == "fast":
+        U = [int(sum(int(v) ** 2 for v in r)) for r in xb]
+    else:
+        _, yb = prescale_rows_fast(Y_T)
+        assert X.shape[1] * 2 ** 14 < 2 ** 53
+        prod = xb.astype(np.float64) @ yb.astype(np.float64).T      # exact integers
+        U = [int(v) for v in np.rint(prod.max(axis=1))] if prod.size else [0] * len(rows)
+    z = [not np.any(X[r]) for r in rows]
+    return e1, exponents(e1, U, pl, z)

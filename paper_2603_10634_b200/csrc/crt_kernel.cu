@@ -106,12 +106,11 @@ cudaError_t launch_res_symmetric(int16_t* out, const int16_t* in, int64_t per, c
 
 cudaError_t launch_crt(int limbs, const int16_t* res, int64_t m, int64_t n, const CrtParams& cp,
                        const int32_t* e_mu, const int32_t* e_nu, double alpha, double beta,
-                       double* C, int64_t ldc, cudaStream_t st) {
+                       double* C, int64_t ldc, bool generic, cudaStream_t st) {
     if (m == 0 || n == 0) return cudaSuccess;
     // ~2048 blocks in total, each looping over many columns (amortises the staging of
     // the CRT constants in shared memory)
-    const char* gen = std::getenv("OZ2_CRT_GENERIC");              // A/B knob: 1 = generic kernel
-    if (m % 2 == 0 && !(gen && gen[0] == '1')) {
+    if (m % 2 == 0 && !generic) {          // generic: OZ2_TUNE_CRT_GENERIC (A/B reference)
         const int64_t gx2 = (m / 2 + 255) / 256;
         int64_t gy2 = 2048 / gx2;
         gy2 = gy2 < 1 ? 1 : (gy2 > n ? n : gy2);

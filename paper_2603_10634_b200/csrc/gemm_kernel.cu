@@ -588,11 +588,8 @@ static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, cons
     // throttle assumes every unit runs concurrently)
     int max_units = num_sms / CS;
     if (max_clusters < max_units) max_units = max_clusters;
-    {   // OZ2_MAX_UNITS: experiment knob, caps the persistent units (power-wall study)
-        const char* mu_env = std::getenv("OZ2_MAX_UNITS");
-        const int cap = mu_env ? std::atoi(mu_env) : 0;
-        if (cap > 0 && cap < max_units) max_units = cap;
-    }
+    // OZ2_TUNE_MAX_UNITS: experiment knob, caps the persistent units (power-wall study)
+    if (gp.max_units > 0 && gp.max_units < max_units) max_units = gp.max_units;
     const int units = num_items < max_units ? num_items : max_units;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(units * CS);

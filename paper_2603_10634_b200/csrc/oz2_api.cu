@@ -131,9 +131,7 @@ struct Plan {
     std::vector<Big> w;
 };
 
-static int env_int(const char* name, int dflt);
-
-static Plan build_plan(int N, int family) {
+static Plan build_plan(int N, int family, int sq_order) {
     Plan pl;
     pl.N = N;
     pl.family = family;
@@ -269,7 +267,7 @@ static Plan build_plan(int N, int family) {
             plane += 1;
         } else if (md.square) {
             // C'_l = mod(s A1 B2 + s A2 B1 + A2 B2, p)  (eq. 3matmult-notKaratsuba)
-            if (env_int("OZ2_SQ_ORDER", 1) == 1) {
+            if (sq_order == 1) {
                 // A1 B2, A2 B2, A2 B1: consecutive products share B2, then A2, so their
                 // operand panels are still in L2 (residue-GEMM DRAM reads 187 -> 178 GB at
                 // 16384^3, N = 13); OZ2_SQ_ORDER=0 restores the order of the equation
@@ -308,69 +306,127 @@ static float f_k_of(int64_t k) {   // reading R5: RU32(1/(1 - k 2^-23))
 // =================================================================================
 // per-thread runtime state
 
-struct ThreadState {
-    cudaStream_t stream = nullptr;
-    cudaStream_t copy_stream = nullptr;   // host-pointer calls: D2H of finished C blocks
-    cudaEvent_t copy_ev = nullptr;
-    void* user_ws = nullptr;
-    size_t user_ws_bytes = 0;
+// Resources tied to one device (a host thread that switches devices with cudaSetDevice
+// gets a separate set per device; nothing of device A is ever used on device B).
+struct DevState {
+    int device = -1;
+    int num_sms = 0;
     void* own_ws = nullptr;
     size_t own_ws_bytes = 0;
     void* staging = nullptr;
     size_t staging_bytes = 0;
+    cudaStream_t copy_stream = nullptr;   // host-pointer calls: D2H of finished C blocks
+    cudaEvent_t copy_ev = nullptr;
     int32_t* d_status = nullptr;
-    int device = -1;
-    int num_sms = 0;
+    cudaEvent_t ev[8] = {};               // phase timers
+    std::map<int, std::unique_ptr<Plan>> plans;   // device copies of the plan tables
+    void release() {
+        int prev = -1;
+        if (cudaGetDevice(&prev) != cudaSuccess) { cudaGetLastError(); return; }   // runtime gone
+        if (prev != device) cudaSetDevice(device);
+        cudaDeviceSynchronize();
+        if (own_ws) cudaFree(own_ws);
+        if (staging) cudaFree(staging);
+        if (d_status) cudaFree(d_status);
+        if (copy_stream) cudaStreamDestroy(copy_stream);
+        if (copy_ev) cudaEventDestroy(copy_ev);
+        for (auto& e : ev) if (e) cudaEventDestroy(e);
+        for (auto& kv : plans) if (kv.second->d_pow2tab) cudaFree(kv.second->d_pow2tab);
+        plans.clear();
+        own_ws = staging = nullptr; own_ws_bytes = staging_bytes = 0;
+        d_status = nullptr; copy_stream = nullptr; copy_ev = nullptr;
+        for (auto& e : ev) e = nullptr;
+        if (prev != device) cudaSetDevice(prev);
+        cudaGetLastError();
+    }
+};
+
+static const int kTuneDefault[OZ2_TUNE_COUNT] = {
+    2,    // CTA_GROUP
+    1,    // SYNC_LEAD
+    8,    // SYNC_CHUNK
+    3,    // L2_PROMO
+    0,    // MAX_UNITS
+    0,    // TMA_HINT_A
+    0,    // TMA_HINT_B
+    -1,   // MOD_SPLIT
+    -1,   // FUSED_CRT
+    1,    // SQ_ORDER
+    0,    // CRT_GENERIC
+    4,    // HOST_BLOCKS
+    1,    // KCAT
+};
+
+struct ThreadState {
+    cudaStream_t stream = nullptr;
+    void* user_ws = nullptr;
+    size_t user_ws_bytes = 0;
     int mode = OZ2_MODE_ACCURATE;
-    int scheme = OZ2_SCHEME_FP8;          // FAMILY_HYBRID_FP8 / FAMILY_INT8
+    int scheme = OZ2_SCHEME_FP8;          // FAMILY_HYBRID_FP8 / FAMILY_INT8 / FAMILY_KARATSUBA_FP8
     int64_t block_m = 0, block_n = 0;     // forced m/n blocking (0: automatic)
     int64_t last_mb = 0, last_nb = 0;     // blocking used by the last call
-    std::map<int, std::unique_ptr<Plan>> plans;
     bool timing = false;
     bool timed_last = false;
-    cudaEvent_t ev[8] = {};
-    ~ThreadState() {}
+    int tune[OZ2_TUNE_COUNT];
+    std::map<int, std::unique_ptr<DevState>> devs;
+    DevState* cur = nullptr;              // state of the current device (ensure_device)
+    ThreadState() { std::memcpy(tune, kTuneDefault, sizeof(tune)); }
+    ~ThreadState() { release_all(); }
+    void release_all() {
+        for (auto& kv : devs) kv.second->release();
+        devs.clear();
+        cur = nullptr;
+    }
 };
 static thread_local ThreadState g_ts;
+static inline DevState& D() { return *g_ts.cur; }
+static inline int tune(int knob) { return g_ts.tune[knob]; }
 
 static std::mutex g_plan_mutex;
 static std::map<int, std::unique_ptr<Plan>> g_host_plans;   // host-only queries
 
-static int plan_key(int N, int family) { return N + 64 * family; }
+static int plan_key(int N, int family, int sq_order) { return N + 64 * family + 1024 * sq_order; }
 
 static const Plan& host_plan(int N) {   // for the calling thread's scheme
     const int fam = g_ts.scheme;
+    const int sq = tune(OZ2_TUNE_SQ_ORDER);
     std::lock_guard<std::mutex> lk(g_plan_mutex);
-    auto it = g_host_plans.find(plan_key(N, fam));
+    auto it = g_host_plans.find(plan_key(N, fam, sq));
     if (it == g_host_plans.end())
-        it = g_host_plans.emplace(plan_key(N, fam), std::make_unique<Plan>(build_plan(N, fam))).first;
+        it = g_host_plans.emplace(plan_key(N, fam, sq), std::make_unique<Plan>(build_plan(N, fam, sq))).first;
     return *it->second;
 }
 
 static int ensure_device() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return OZ2_ERR_CUDA;
-    if (g_ts.device != dev) {
-        int major = 0;
-        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return OZ2_ERR_CUDA;
-        if (major != 10) return OZ2_ERR_NOT_SUPPORTED;
-        if (cudaDeviceGetAttribute(&g_ts.num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return OZ2_ERR_CUDA;
-        g_ts.device = dev;
-        g_ts.plans.clear();
-        g_ts.d_status = nullptr;
+    if (!g_ts.cur || g_ts.cur->device != dev) {
+        auto it = g_ts.devs.find(dev);
+        if (it == g_ts.devs.end()) {
+            int major = 0, sms = 0;
+            if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return OZ2_ERR_CUDA;
+            if (major != 10) return OZ2_ERR_NOT_SUPPORTED;
+            if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return OZ2_ERR_CUDA;
+            auto ds = std::make_unique<DevState>();
+            ds->device = dev;
+            ds->num_sms = sms;
+            it = g_ts.devs.emplace(dev, std::move(ds)).first;
+        }
+        g_ts.cur = it->second.get();
     }
-    if (!g_ts.d_status) {
-        if (cudaMalloc(&g_ts.d_status, sizeof(int32_t)) != cudaSuccess) return OZ2_ERR_ALLOC;
-        if (cudaMemset(g_ts.d_status, 0, sizeof(int32_t)) != cudaSuccess) return OZ2_ERR_CUDA;
+    if (!D().d_status) {
+        if (cudaMalloc(&D().d_status, sizeof(int32_t)) != cudaSuccess) return OZ2_ERR_ALLOC;
+        if (cudaMemset(D().d_status, 0, sizeof(int32_t)) != cudaSuccess) return OZ2_ERR_CUDA;
     }
     return OZ2_SUCCESS;
 }
 
 static Plan* device_plan(int N, int* err) {
-    const int key = plan_key(N, g_ts.scheme);
-    auto it = g_ts.plans.find(key);
-    if (it != g_ts.plans.end()) return it->second.get();
-    auto pl = std::make_unique<Plan>(build_plan(N, g_ts.scheme));
+    const int sq = tune(OZ2_TUNE_SQ_ORDER);
+    const int key = plan_key(N, g_ts.scheme, sq);
+    auto it = D().plans.find(key);
+    if (it != D().plans.end()) return it->second.get();
+    auto pl = std::make_unique<Plan>(build_plan(N, g_ts.scheme, sq));
     const size_t bytes = pl->pow2tab.size() * sizeof(uint16_t);
     if (cudaMalloc(&pl->d_pow2tab, bytes) != cudaSuccess) { *err = OZ2_ERR_ALLOC; return nullptr; }
     if (cudaMemcpy(pl->d_pow2tab, pl->pow2tab.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
@@ -379,7 +435,7 @@ static Plan* device_plan(int N, int* err) {
     }
     pl->dig.pow2tab = pl->d_pow2tab;
     Plan* raw = pl.get();
-    g_ts.plans.emplace(key, std::move(pl));
+    D().plans.emplace(key, std::move(pl));
     return raw;
 }
 
@@ -477,11 +533,6 @@ static PFN_encodeTiled_t encode_fn() {
     return fn;
 }
 
-// tuning knobs (read per call; defaults are the measured best)
-static int env_int(const char* name, int dflt) {
-    const char* e = std::getenv(name);
-    return e ? std::atoi(e) : dflt;
-}
 // 2D byte tensor [outer][inner] with row pitch `pitch` bytes, box inner x outer, 128B swizzle
 static bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                      uint64_t pitch, uint32_t box_inner, uint32_t box_outer) {
@@ -491,8 +542,8 @@ static bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_
     cuuint64_t strides[1] = {pitch};
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t es[2] = {1, 1};
-    // L2 promotion of TMA misses (OZ2_L2PROMO: 0 none, 1 64B, 2 128B, 3 256B)
-    const int promo = env_int("OZ2_L2PROMO", 3);
+    // L2 promotion of TMA misses (OZ2_TUNE_L2_PROMO: 0 none, 1 64B, 2 128B, 3 256B)
+    const int promo = tune(OZ2_TUNE_L2_PROMO);
     const CUtensorMapL2promotion pr = promo == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
                                     : promo == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
                                     : promo == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
@@ -502,14 +553,15 @@ static bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static int sync_lead() {   // progress throttle of the residue GEMM (OZ2_SYNC_LEAD)
-    const int v = env_int("OZ2_SYNC_LEAD", 1);
+static int sync_lead() {   // progress throttle of the residue GEMM (OZ2_TUNE_SYNC_LEAD)
+    const int v = tune(OZ2_TUNE_SYNC_LEAD);
     return v < 0 ? 0 : v;
 }
 // 1: 128x256 CTA tiles; 2: 256x256 CTA-pair tiles; 4: two pairs per cluster sharing A by
-// TMA multicast (FP8 kinds only; needs an even number of 256-column tiles, else 2) (OZ2_CG)
+// TMA multicast (FP8 kinds only; needs an even number of 256-column tiles, else 2)
+// (OZ2_TUNE_CTA_GROUP)
 static int cta_group(int64_t n_pad, bool i8) {
-    const int v = env_int("OZ2_CG", 2);
+    const int v = tune(OZ2_TUNE_CTA_GROUP);
     if (v == 1) return 1;
     if (v == 4 && !i8 && (n_pad / BN) % 2 == 0) return 4;   // the kind::i8 kernels have no multicast variant
     return 2;
@@ -520,8 +572,18 @@ static int tile_m(int cg) { return cg == 1 ? BM : 2 * BM; }
 
 static void phase_mark(int i) {
     if (!g_ts.timing) return;
-    if (!g_ts.ev[i]) cudaEventCreate(&g_ts.ev[i]);
-    cudaEventRecord(g_ts.ev[i], g_ts.stream);
+    if (!D().ev[i]) cudaEventCreate(&D().ev[i]);
+    cudaEventRecord(D().ev[i], g_ts.stream);
+}
+
+static int read_timing(float* ms_out, int n) {   // phase times of the last timed call
+    if (cudaEventSynchronize(D().ev[6]) != cudaSuccess) return OZ2_ERR_CUDA;
+    float v[7];
+    for (int i = 0; i < 6; ++i)
+        if (cudaEventElapsedTime(&v[i], D().ev[i], D().ev[i + 1]) != cudaSuccess) return OZ2_ERR_CUDA;
+    if (cudaEventElapsedTime(&v[6], D().ev[0], D().ev[6]) != cudaSuccess) return OZ2_ERR_CUDA;
+    for (int i = 0; i < n && i < 7; ++i) ms_out[i] = v[i];
+    return OZ2_SUCCESS;
 }
 
 #define OZ2_CK(x)                                   \
@@ -569,12 +631,12 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
         ws = static_cast<uint8_t*>(g_ts.user_ws);
     } else {
         L = make_layout(m, n, k, N, pl->M, mb, nb);
-        if (g_ts.own_ws_bytes < L.total) {
-            if (g_ts.own_ws) { cudaStreamSynchronize(st); cudaFree(g_ts.own_ws); g_ts.own_ws = nullptr; g_ts.own_ws_bytes = 0; }
-            if (cudaMalloc(&g_ts.own_ws, L.total) != cudaSuccess) return OZ2_ERR_ALLOC;
-            g_ts.own_ws_bytes = L.total;
+        if (D().own_ws_bytes < L.total) {
+            if (D().own_ws) { cudaStreamSynchronize(st); cudaFree(D().own_ws); D().own_ws = nullptr; D().own_ws_bytes = 0; }
+            if (cudaMalloc(&D().own_ws, L.total) != cudaSuccess) return OZ2_ERR_ALLOC;
+            D().own_ws_bytes = L.total;
         }
-        ws = static_cast<uint8_t*>(g_ts.own_ws);
+        ws = static_cast<uint8_t*>(D().own_ws);
     }
     g_ts.last_mb = L.mb;
     g_ts.last_nb = L.nb;
@@ -596,7 +658,7 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
     const bool imported = opt && opt->e_mu_in && opt->e_nu_in;
     g_ts.timed_last = false;
     phase_mark(0);
-    OZ2_CK(cudaMemsetAsync(g_ts.d_status, 0, sizeof(int32_t), st));
+    OZ2_CK(cudaMemsetAsync(D().d_status, 0, sizeof(int32_t), st));
     if (!imported) {
         // ---- step 1: prescale (eq. def:mu'nu')
         OZ2_CK(cudaMemsetAsync(maxbits, 0, 8 * static_cast<size_t>(m + n), st));
@@ -604,9 +666,9 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
         OZ2_CK(launch_rowmax(A, m, k, lda, a_kmajor, maxbits, st));
         OZ2_CK(launch_rowmax(B, n, k, ldb, b_kmajor, maxbits + m, st));
         if (fast) OZ2_CK(cudaMemsetAsync(sumsq, 0, 8 * static_cast<size_t>(m + n), st));
-        OZ2_CK(launch_cast(A, m, k, lda, a_kmajor, maxbits, eprime, abar, L.m_pad, L.k_pad, g_ts.d_status,
+        OZ2_CK(launch_cast(A, m, k, lda, a_kmajor, maxbits, eprime, abar, L.m_pad, L.k_pad, D().d_status,
                            fast ? sumsq : nullptr, i8, st));
-        OZ2_CK(launch_cast(B, n, k, ldb, b_kmajor, maxbits + m, eprime + m, bbar, L.n_pad, L.k_pad, g_ts.d_status,
+        OZ2_CK(launch_cast(B, n, k, ldb, b_kmajor, maxbits + m, eprime + m, bbar, L.n_pad, L.k_pad, D().d_status,
                            fast ? sumsq + m : nullptr, i8, st));
         if (opt && opt->e_prime_a) OZ2_CK(cudaMemcpyAsync(opt->e_prime_a, eprime, 4 * m, cudaMemcpyDeviceToDevice, st));
         if (opt && opt->e_prime_b) OZ2_CK(cudaMemcpyAsync(opt->e_prime_b, eprime + m, 4 * n, cudaMemcpyDeviceToDevice, st));
@@ -628,7 +690,7 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             gp.m_tiles = static_cast<int>(L.m_pad / tile_m(cg)); gp.n_tiles = static_cast<int>(L.n_pad / BN);
             gp.rows_per_plane_a = static_cast<int>(L.m_pad); gp.rows_per_plane_b = static_cast<int>(L.n_pad);
             gp.rmax = rsmax; gp.smax = rsmax + m;
-            OZ2_CK(launch_gemm(i8 ? MODE_BOUND_I8 : MODE_BOUND, cg, 0, ta, tb, gp, g_ts.num_sms, st));
+            OZ2_CK(launch_gemm(i8 ? MODE_BOUND_I8 : MODE_BOUND, cg, 0, ta, tb, gp, D().num_sms, st));
         }
         if (opt && opt->rmax && !fast) OZ2_CK(cudaMemcpyAsync(opt->rmax, rsmax, 4 * m, cudaMemcpyDeviceToDevice, st));
         if (opt && opt->smax && !fast) OZ2_CK(cudaMemcpyAsync(opt->smax, rsmax + m, 4 * n, cudaMemcpyDeviceToDevice, st));
@@ -657,13 +719,13 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
     // enough to hide the CRT steps spread over it: measured (profiles/round1_fused_crt_ab.md)
     // FP8 fused wins from k = 16384 on (+1-2 %) and loses 20 % at k = 8192; INT8 (one
     // product per modulus, so 3x the CRT work per product) loses 23 % at k = 16384.
-    // OZ2_FUSED_CRT: -1 auto (default), 0 never, 1 whenever L <= 6 and k >= 8192.
-    const int fuse_env = env_int("OZ2_FUSED_CRT", -1);
+    // OZ2_TUNE_FUSED_CRT: -1 auto (default), 0 never, 1 whenever L <= 6 and k >= 8192.
+    const int fuse_env = tune(OZ2_TUNE_FUSED_CRT);
     const bool fuse_auto = i8 ? k >= 49152 : k >= 16384;
     const int fused = (pl->L <= 6 && k >= 8192 && (fuse_env > 0 || (fuse_env < 0 && fuse_auto))) ? pl->L : 0;
     int sync_chunk = 1;
     {   // chunks must tile the 512-block K segments: a power of two in [1, 512]
-        const int kc = env_int("OZ2_SYNC_CHUNK", 8);
+        const int kc = tune(OZ2_TUNE_SYNC_CHUNK);
         while (sync_chunk * 2 <= kc && sync_chunk * 2 <= 512) sync_chunk *= 2;
     }
     // ---- steps 4-6 on blocks of C (one block when unblocked)
@@ -705,16 +767,16 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             gp.m_tiles = static_cast<int>(mbi_pad / tile_m(cg)); gp.n_tiles = static_cast<int>(nbj_pad / BN);
             gp.rows_per_plane_a = static_cast<int>(mbi_pad); gp.rows_per_plane_b = static_cast<int>(nbj_pad);
             gp.num_moduli = N;
-            {   // work items (OZ2_MOD_SPLIT: -1 auto, 0 tile-major, 1 all (tile, modulus),
+            {   // work items (OZ2_TUNE_MOD_SPLIT: -1 auto, 0 tile-major, 1 all (tile, modulus),
                 // 2 hybrid): few tiles (< 8 per persistent unit) -> all split; otherwise
                 // tile-major, with the last partial wave split over all units (hybrid) when
                 // it would leave more than 0.5 % of the unit-time idle
                 const int64_t tiles = static_cast<int64_t>(gp.m_tiles) * gp.n_tiles / (cg == 4 ? 2 : 1);
-                const int64_t units = std::max<int64_t>(1, g_ts.num_sms / (cg == 1 ? 1 : cg == 4 ? 4 : 2));
+                const int64_t units = std::max<int64_t>(1, D().num_sms / (cg == 1 ? 1 : cg == 4 ? 4 : 2));
                 const int64_t full = tiles / units * units;
                 const int64_t waves = (tiles + units - 1) / units;
                 const bool ragged = full < tiles && static_cast<double>(waves * units - tiles) > 0.005 * waves * units;
-                int ms = env_int("OZ2_MOD_SPLIT", -1);
+                int ms = tune(OZ2_TUNE_MOD_SPLIT);
                 // hybrid only where the CRT runs separately anyway: giving up the fused CRT
                 // for the tail costs more than the tail (A/B: FP8 16384^3 -1.5 %, 8192^3 +3.4 %)
                 if (ms < 0) ms = tiles < 8 * units ? 1 : (ragged && !fused ? 2 : 0);
@@ -726,12 +788,13 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             gp.residues = res;
             gp.sync_lead = sync_lead();
             gp.sync_chunk = sync_chunk;
-            {   // OZ2_TMA_HINT_A / _B: 0 evict-normal (default), 1 evict-last, 2 evict-first
+            gp.max_units = tune(OZ2_TUNE_MAX_UNITS);
+            {   // OZ2_TUNE_TMA_HINT_A / _B: 0 evict-normal (default), 1 evict-last, 2 evict-first
                 auto hint = [](int v) -> unsigned long long {
                     return v == 1 ? 0x14F0000000000000ull : v == 2 ? 0x12F0000000000000ull : 0x1000000000000000ull;
                 };
-                gp.hint_a = hint(env_int("OZ2_TMA_HINT_A", 0));
-                gp.hint_b = hint(env_int("OZ2_TMA_HINT_B", 0));
+                gp.hint_a = hint(tune(OZ2_TUNE_TMA_HINT_A));
+                gp.hint_b = hint(tune(OZ2_TUNE_TMA_HINT_B));
             }
             if (gp.sync_lead > 0) {
                 gp.progress = reinterpret_cast<unsigned long long*>(maxbits);   // dead after step 3
@@ -744,7 +807,7 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
                 gp.alpha = alpha; gp.beta = beta;
                 gp.C = Cij; gp.ldc = ldc;
             }
-            OZ2_CK(launch_gemm(i8 ? MODE_RESIDUE_I8 : MODE_RESIDUE, cg, fused_blk, ta, tb, gp, g_ts.num_sms, st));
+            OZ2_CK(launch_gemm(i8 ? MODE_RESIDUE_I8 : MODE_RESIDUE, cg, fused_blk, ta, tb, gp, D().num_sms, st));
             if (!L.blocked) {
                 if (opt && opt->residues)   // stored as u_l in [0, p_l): symmetric C'_l for the caller
                     OZ2_CK(launch_res_symmetric(opt->residues, res, m * n, pl->crt, st));
@@ -752,7 +815,8 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             }
             // ---- step 6: CRT + inverse scaling (eqs. CRT_finalreduction, inversescaling)
             if (!fused_blk)
-                OZ2_CK(launch_crt(pl->L, res, mbi, nbj, pl->crt, e_mu + i0, e_nu + j0, alpha, beta, Cij, ldc, st));
+                OZ2_CK(launch_crt(pl->L, res, mbi, nbj, pl->crt, e_mu + i0, e_nu + j0, alpha, beta, Cij, ldc,
+                                  tune(OZ2_TUNE_CRT_GENERIC) != 0, st));
         }
         if (hook && hook->done) {
             const int hr = hook->done(hook->ctx, j0, nbj);
@@ -771,14 +835,51 @@ static bool is_device_ptr(const void* p) {
     return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
+static bool is_pinned_host(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return at.type == cudaMemoryTypeHost;
+}
+
 static bool trans_ok(char t) {
     return t == 'N' || t == 'n' || t == 'T' || t == 't' || t == 'C' || t == 'c';
 }
 static bool is_n(char t) { return t == 'N' || t == 'n'; }
 
+static int dgemm_call(char transa, char transb, int64_t m, int64_t n, int64_t k, double alpha,
+                      const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+                      int64_t ldc, int N, const oz2_options* opt);
+
+// Per-call settings of oz2_options (mode, scheme, timing) applied for the duration of one
+// call and restored afterwards (the thread's settings are the defaults).
 int dgemm_impl(char transa, char transb, int64_t m, int64_t n, int64_t k, double alpha,
                const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
                int64_t ldc, int N, const oz2_options* opt) {
+    if (opt) {
+        for (int i = 0; i < 4; ++i) if (opt->reserved[i]) return -15;
+        if (opt->set_mode && opt->mode != OZ2_MODE_ACCURATE && opt->mode != OZ2_MODE_FAST) return -15;
+        if (opt->set_scheme && opt->scheme != OZ2_SCHEME_FP8 && opt->scheme != OZ2_SCHEME_INT8 &&
+            opt->scheme != OZ2_SCHEME_FP8_KARATSUBA) return -15;
+    }
+    const int mode0 = g_ts.mode, scheme0 = g_ts.scheme;
+    const bool timing0 = g_ts.timing;
+    if (opt && opt->set_mode) g_ts.mode = opt->mode;
+    if (opt && opt->set_scheme) g_ts.scheme = opt->scheme;
+    if (opt && opt->timing_ms) g_ts.timing = true;
+    int rc = dgemm_call(transa, transb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, N, opt);
+    if (rc == OZ2_SUCCESS && opt && opt->timing_ms) {
+        if (g_ts.timed_last) rc = read_timing(opt->timing_ms, 7);
+        else for (int i = 0; i < 7; ++i) opt->timing_ms[i] = 0.0f;   // quick return: nothing ran
+    }
+    g_ts.mode = mode0;
+    g_ts.scheme = scheme0;
+    g_ts.timing = timing0;
+    return rc;
+}
+
+static int dgemm_call(char transa, char transb, int64_t m, int64_t n, int64_t k, double alpha,
+                      const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+                      int64_t ldc, int N, const oz2_options* opt) {
     // BLAS argument checks (xerbla order)
     if (!trans_ok(transa)) return -1;
     if (!trans_ok(transb)) return -2;
@@ -791,13 +892,13 @@ int dgemm_impl(char transa, char transb, int64_t m, int64_t n, int64_t k, double
     if (ldb < (rowsB > 1 ? rowsB : 1)) return -10;
     if (ldc < (m > 1 ? m : 1)) return -13;
     if (N < 2 || N > kMaxModuli) return -14;
-    if (opt) for (int i = 0; i < 8; ++i) if (opt->reserved[i]) return -15;
+    g_ts.timed_last = false;
     if (m == 0 || n == 0) return OZ2_SUCCESS;
     int e = ensure_device();
     if (e) return e;
     if (k > kMaxKTotal) return OZ2_ERR_NOT_SUPPORTED;      // f_k = 1/(1 - k 2^-23) needs k << 2^23
     if (g_ts.scheme == OZ2_SCHEME_INT8 && k > kMaxK) return OZ2_ERR_NOT_SUPPORTED;   // exact S32 bound (R16)
-    if (m > (1ll << 30) || n > (1ll << 30)) return OZ2_ERR_NOT_SUPPORTED;
+    if (m > kMaxRows || n > kMaxRows) return OZ2_ERR_NOT_SUPPORTED;   // conversion-kernel grids
     cudaStream_t st = g_ts.stream;
     const bool quick = (alpha == 0.0 || k == 0);
     const bool dev = is_device_ptr(C);
@@ -812,14 +913,14 @@ int dgemm_impl(char transa, char transb, int64_t m, int64_t n, int64_t k, double
     const size_t bA = align_up(8ull * rowsA * colsA, 256), bB = align_up(8ull * rowsB * colsB, 256);
     const size_t bC = align_up(8ull * m * n, 256);
     const size_t need = bA + bB + bC;
-    if (g_ts.staging_bytes < need) {
-        if (g_ts.staging) { cudaStreamSynchronize(st); cudaFree(g_ts.staging); g_ts.staging = nullptr; g_ts.staging_bytes = 0; }
-        if (cudaMalloc(&g_ts.staging, need) != cudaSuccess) return OZ2_ERR_ALLOC;
-        g_ts.staging_bytes = need;
+    if (D().staging_bytes < need) {
+        if (D().staging) { cudaStreamSynchronize(st); cudaFree(D().staging); D().staging = nullptr; D().staging_bytes = 0; }
+        if (cudaMalloc(&D().staging, need) != cudaSuccess) return OZ2_ERR_ALLOC;
+        D().staging_bytes = need;
     }
-    double* dA = static_cast<double*>(g_ts.staging);
-    double* dB = reinterpret_cast<double*>(static_cast<uint8_t*>(g_ts.staging) + bA);
-    double* dC = reinterpret_cast<double*>(static_cast<uint8_t*>(g_ts.staging) + bA + bB);
+    double* dA = static_cast<double*>(D().staging);
+    double* dB = reinterpret_cast<double*>(static_cast<uint8_t*>(D().staging) + bA);
+    double* dC = reinterpret_cast<double*>(static_cast<uint8_t*>(D().staging) + bA + bB);
     if (!quick) {
         OZ2_CK(cudaMemcpy2DAsync(dA, 8 * rowsA, A, 8 * lda, 8 * rowsA, colsA, cudaMemcpyHostToDevice, st));
         OZ2_CK(cudaMemcpy2DAsync(dB, 8 * rowsB, B, 8 * ldb, 8 * rowsB, colsB, cudaMemcpyHostToDevice, st));
@@ -835,27 +936,29 @@ int dgemm_impl(char transa, char transb, int64_t m, int64_t n, int64_t k, double
     }
     // C goes back in column blocks: block j's device-to-host copy (on a second stream)
     // overlaps the GEMMs of blocks j+1.. (OZ2_HOST_BLOCKS blocks, default 4; 1 = off)
-    if (!g_ts.copy_stream) {
-        OZ2_CK(cudaStreamCreateWithFlags(&g_ts.copy_stream, cudaStreamNonBlocking));
-        OZ2_CK(cudaEventCreateWithFlags(&g_ts.copy_ev, cudaEventDisableTiming));
+    if (!D().copy_stream) {
+        OZ2_CK(cudaStreamCreateWithFlags(&D().copy_stream, cudaStreamNonBlocking));
+        OZ2_CK(cudaEventCreateWithFlags(&D().copy_ev, cudaEventDisableTiming));
     }
     struct Ctx { double* C; int64_t ldc; const double* dC; int64_t m; } ctx{C, ldc, dC, m};
     BlockHook hook{};
-    const int nblk = env_int("OZ2_HOST_BLOCKS", 4);
-    if (nblk > 1 && n >= 2 * PAD_N * nblk) hook.nb = round_up((n + nblk - 1) / nblk, PAD_N);
+    // (a copy into pageable memory is synchronous with the host, which would serialise
+    // the blocks: only pinned C is copied in blocks)
+    const int nblk = tune(OZ2_TUNE_HOST_BLOCKS);
+    if (nblk > 1 && n >= 2 * PAD_N * nblk && is_pinned_host(C)) hook.nb = round_up((n + nblk - 1) / nblk, PAD_N);
     hook.ctx = &ctx;
     hook.done = [](void* c, int64_t j0, int64_t nbj) -> int {
         const Ctx& x = *static_cast<const Ctx*>(c);
-        if (cudaEventRecord(g_ts.copy_ev, g_ts.stream) != cudaSuccess) return OZ2_ERR_CUDA;
-        if (cudaStreamWaitEvent(g_ts.copy_stream, g_ts.copy_ev, 0) != cudaSuccess) return OZ2_ERR_CUDA;
+        if (cudaEventRecord(D().copy_ev, g_ts.stream) != cudaSuccess) return OZ2_ERR_CUDA;
+        if (cudaStreamWaitEvent(D().copy_stream, D().copy_ev, 0) != cudaSuccess) return OZ2_ERR_CUDA;
         if (cudaMemcpy2DAsync(x.C + j0 * x.ldc, 8 * x.ldc, x.dC + j0 * x.m, 8 * x.m, 8 * x.m, nbj,
-                              cudaMemcpyDeviceToHost, g_ts.copy_stream) != cudaSuccess)
+                              cudaMemcpyDeviceToHost, D().copy_stream) != cudaSuccess)
             return OZ2_ERR_CUDA;
         return OZ2_SUCCESS;
     };
     rc = run_device(!is_n(transa), is_n(transb), m, n, k, alpha, dA, rowsA, dB, rowsB, beta, dC, m, N, opt, &hook);
     const cudaError_t e1 = cudaStreamSynchronize(st);
-    const cudaError_t e2 = cudaStreamSynchronize(g_ts.copy_stream);
+    const cudaError_t e2 = cudaStreamSynchronize(D().copy_stream);
     if (rc) return rc;
     if (e1 != cudaSuccess || e2 != cudaSuccess) return OZ2_ERR_CUDA;
     return OZ2_SUCCESS;
@@ -959,8 +1062,8 @@ int oz2_get_status(int32_t* status) {
     if (e) return e;
     int32_t h = 0;
     OZ2_CK(cudaStreamSynchronize(g_ts.stream));
-    OZ2_CK(cudaMemcpy(&h, g_ts.d_status, sizeof(h), cudaMemcpyDeviceToHost));
-    OZ2_CK(cudaMemset(g_ts.d_status, 0, sizeof(int32_t)));
+    OZ2_CK(cudaMemcpy(&h, D().d_status, sizeof(h), cudaMemcpyDeviceToHost));
+    OZ2_CK(cudaMemset(D().d_status, 0, sizeof(int32_t)));
     *status = h ? OZ2_ERR_NONFINITE : OZ2_SUCCESS;
     return OZ2_SUCCESS;
 }
@@ -972,32 +1075,49 @@ int oz2_set_timing(int enable) {
 
 int oz2_get_timing(float* ms_out, int n) {
     if (!ms_out) return -1;
-    if (!g_ts.timed_last) return OZ2_ERR_NOT_SUPPORTED;
-    if (cudaEventSynchronize(g_ts.ev[6]) != cudaSuccess) return OZ2_ERR_CUDA;
-    float v[7];
-    for (int i = 0; i < 6; ++i)
-        if (cudaEventElapsedTime(&v[i], g_ts.ev[i], g_ts.ev[i + 1]) != cudaSuccess) return OZ2_ERR_CUDA;
-    if (cudaEventElapsedTime(&v[6], g_ts.ev[0], g_ts.ev[6]) != cudaSuccess) return OZ2_ERR_CUDA;
-    for (int i = 0; i < n && i < 7; ++i) ms_out[i] = v[i];
-    return OZ2_SUCCESS;
+    if (!g_ts.timed_last || !g_ts.cur) return OZ2_ERR_NOT_SUPPORTED;
+    return read_timing(ms_out, n);
 }
+
 
 int oz2_finalize(void) {
     if (g_ts.stream) cudaStreamSynchronize(g_ts.stream);
-    if (g_ts.own_ws) cudaFree(g_ts.own_ws);
-    if (g_ts.staging) cudaFree(g_ts.staging);
-    if (g_ts.d_status) cudaFree(g_ts.d_status);
-    if (g_ts.copy_stream) { cudaStreamSynchronize(g_ts.copy_stream); cudaStreamDestroy(g_ts.copy_stream); }
-    if (g_ts.copy_ev) cudaEventDestroy(g_ts.copy_ev);
-    g_ts.copy_stream = nullptr; g_ts.copy_ev = nullptr;
-    for (auto& kv : g_ts.plans) if (kv.second->d_pow2tab) cudaFree(kv.second->d_pow2tab);
-    g_ts.plans.clear();
-    g_ts.own_ws = nullptr; g_ts.own_ws_bytes = 0;
-    g_ts.staging = nullptr; g_ts.staging_bytes = 0;
-    g_ts.d_status = nullptr;
-    g_ts.device = -1;
+    g_ts.release_all();
     return OZ2_SUCCESS;
 }
+
+int oz2_set_tuning(int knob, int value) {
+    if (knob < 0 || knob >= OZ2_TUNE_COUNT) return -1;
+    bool ok = true;
+    switch (knob) {
+        case OZ2_TUNE_CTA_GROUP: ok = value == 1 || value == 2 || value == 4; break;
+        case OZ2_TUNE_SYNC_LEAD: ok = value >= 0 && value <= 1 << 20; break;
+        case OZ2_TUNE_SYNC_CHUNK: ok = value >= 1 && value <= 512; break;
+        case OZ2_TUNE_L2_PROMO: ok = value >= 0 && value <= 3; break;
+        case OZ2_TUNE_MAX_UNITS: ok = value >= 0; break;
+        case OZ2_TUNE_TMA_HINT_A:
+        case OZ2_TUNE_TMA_HINT_B: ok = value >= 0 && value <= 2; break;
+        case OZ2_TUNE_MOD_SPLIT: ok = value >= -1 && value <= 2; break;
+        case OZ2_TUNE_FUSED_CRT: ok = value >= -1 && value <= 1; break;
+        case OZ2_TUNE_SQ_ORDER:
+        case OZ2_TUNE_CRT_GENERIC:
+        case OZ2_TUNE_KCAT: ok = value == 0 || value == 1; break;
+        case OZ2_TUNE_HOST_BLOCKS: ok = value >= 1 && value <= 64; break;
+        default: break;
+    }
+    if (!ok) return -2;
+    g_ts.tune[knob] = value;
+    return OZ2_SUCCESS;
+}
+
+int oz2_get_tuning(int knob, int* value) {
+    if (knob < 0 || knob >= OZ2_TUNE_COUNT) return -1;
+    if (!value) return -2;
+    *value = g_ts.tune[knob];
+    return OZ2_SUCCESS;
+}
+
+void oz2_reset_tuning(void) { std::memcpy(g_ts.tune, kTuneDefault, sizeof(g_ts.tune)); }
 
 int oz2_moduli(int num_moduli, int32_t* p_out) {
     if (num_moduli < 2 || num_moduli > kMaxModuli) return -1;
@@ -1060,7 +1180,7 @@ static int gemm_raw(int mode, const uint8_t* a, const uint8_t* b, float* C32, in
     gp.num_k_blocks = static_cast<int>((k + BK - 1) / BK);
     gp.m_tiles = static_cast<int>((m + tile_m(cg) - 1) / tile_m(cg)); gp.n_tiles = static_cast<int>((n + BN - 1) / BN);
     gp.c32 = C32;
-    OZ2_CK(launch_gemm(mode, cg, 0, ta, tb, gp, g_ts.num_sms, g_ts.stream));
+    OZ2_CK(launch_gemm(mode, cg, 0, ta, tb, gp, D().num_sms, g_ts.stream));
     return OZ2_SUCCESS;
 }
 

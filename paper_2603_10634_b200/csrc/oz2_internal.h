@@ -15,6 +15,8 @@ constexpr int kMaxLimbs = 12;
 constexpr int kPow2Tab = 1024;   // 2^E mod p for E in [0, 1024)
 constexpr int kMaxK = 65536;     // exactness window of one FP32 accumulation
 constexpr int64_t kMaxKTotal = int64_t(1) << 22;   // longer k runs in 2^16 segments (NEXT-2)
+// rows of op(A) / columns of op(B): the conversion kernels put 32-row tiles in gridDim.y
+constexpr int64_t kMaxRows = int64_t(65535) * 32;
 
 // ---- GEMM (tcgen05) ------------------------------------------------------------
 constexpr int BM = 128;          // rows of A per CTA tile (TMEM lanes)
@@ -84,6 +86,7 @@ struct GemmParams {
     unsigned long long hint_a, hint_b;   // L2 cache policies of the operand TMA loads
     int sync_lead;               // 0 = off; else max chunks ahead of the chip-wide average
     int sync_chunk;              // k-blocks per throttle chunk (0 = one chunk per product)
+    int max_units;               // host only: cap on persistent units (0 = all)
     ModEpi mod[kMaxModuli];
 };
 
@@ -148,7 +151,7 @@ cudaError_t launch_res_symmetric(int16_t* out, const int16_t* in, int64_t per, c
                                  cudaStream_t st);
 cudaError_t launch_crt(int limbs, const int16_t* res, int64_t m, int64_t n, const CrtParams& cp,
                        const int32_t* e_mu, const int32_t* e_nu, double alpha, double beta,
-                       double* C, int64_t ldc, cudaStream_t st);
+                       double* C, int64_t ldc, bool generic, cudaStream_t st);
 cudaError_t launch_scale(double* C, int64_t m, int64_t n, int64_t ldc, double beta, cudaStream_t st);
 
 }  // namespace oz2

@@ -25,6 +25,13 @@ OZ2_MODE_ACCURATE = 0
 OZ2_MODE_FAST = 1
 _MODES = {"accurate": OZ2_MODE_ACCURATE, "fast": OZ2_MODE_FAST}
 
+# tuning knobs (include/oz2.h OZ2_TUNE_*): schedule only, results are bit-identical
+TUNE = {
+    "cta_group": 0, "sync_lead": 1, "sync_chunk": 2, "l2_promo": 3, "max_units": 4,
+    "tma_hint_a": 5, "tma_hint_b": 6, "mod_split": 7, "fused_crt": 8, "sq_order": 9,
+    "crt_generic": 10, "host_blocks": 11, "kcat": 12,
+}
+
 _c_int64 = ctypes.c_int64
 _vp = ctypes.c_void_p
 
@@ -35,7 +42,10 @@ class oz2_options(ctypes.Structure):
         ("rmax", _vp), ("smax", _vp), ("e_mu", _vp), ("e_nu", _vp),
         ("digits_a", _vp), ("digits_b", _vp), ("residues", _vp),
         ("e_mu_in", _vp), ("e_nu_in", _vp),
-        ("reserved", ctypes.c_int32 * 8),
+        ("timing_ms", _vp),
+        ("set_mode", ctypes.c_int32), ("mode", ctypes.c_int32),
+        ("set_scheme", ctypes.c_int32), ("scheme", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 4),
     ]
 
 
@@ -76,6 +86,9 @@ SIGNATURES = [
     ("oz2_set_timing", ctypes.c_int, [ctypes.c_int]),
     ("oz2_get_timing", ctypes.c_int, [ctypes.POINTER(ctypes.c_float), ctypes.c_int]),
     ("oz2_finalize", ctypes.c_int, []),
+    ("oz2_set_tuning", ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
+    ("oz2_get_tuning", ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
+    ("oz2_reset_tuning", None, []),
     ("oz2_moduli", ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int32)]),
     ("oz2_plan_query", ctypes.c_int, [ctypes.c_int, _c_int64, ctypes.POINTER(oz2_plan_info)]),
     ("oz2_version", ctypes.c_char_p, []),
@@ -201,6 +214,41 @@ def oz2_finalize():
     return lib().oz2_finalize()
 
 
+def oz2_set_tuning(knob, value):
+    """knob: OZ2_TUNE_* number or its lower-case name in TUNE."""
+    return lib().oz2_set_tuning(TUNE.get(knob, knob), int(value))
+
+
+def oz2_get_tuning(knob):
+    v = ctypes.c_int(0)
+    _check(lib().oz2_get_tuning(TUNE.get(knob, knob), ctypes.byref(v)), "oz2_get_tuning")
+    return v.value
+
+
+def oz2_reset_tuning():
+    lib().oz2_reset_tuning()
+
+
+class tuning:
+    """Context manager: ``with tuning(cta_group=1, mod_split=0): ...`` sets knobs of the
+    calling thread and restores the previous values on exit."""
+
+    def __init__(self, **knobs):
+        self.knobs = knobs
+        self.prev = {}
+
+    def __enter__(self):
+        for k, v in self.knobs.items():
+            self.prev[k] = oz2_get_tuning(k)
+            _check(oz2_set_tuning(k, v), f"oz2_set_tuning({k}={v})")
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.prev.items():
+            oz2_set_tuning(k, v)
+        return False
+
+
 def oz2_moduli(num_moduli):
     out = (ctypes.c_int32 * num_moduli)()
     _check(lib().oz2_moduli(num_moduli, out), "oz2_moduli")
@@ -231,15 +279,25 @@ _ws = {}
 
 
 def _bind_stream_and_workspace(torch, device, nbytes):
-    """Point the library at torch's current stream and a torch-owned workspace."""
+    """Point the library at torch's current stream and a torch-owned workspace.
+
+    The library's calls are asynchronous on that stream and its state is per host thread,
+    so the cached scratch buffer is keyed by (thread, device, stream): two threads, or two
+    streams of one thread, never share one.  record_stream keeps the caching allocator
+    from handing the buffer out again while the stream's kernels may still use it."""
+    import threading
     stream = torch.cuda.current_stream(device)
     oz2_set_stream(stream.cuda_stream)
-    key = (device.index if device.index is not None else torch.cuda.current_device())
+    dev = device.index if device.index is not None else torch.cuda.current_device()
+    key = (threading.get_ident(), dev, stream.cuda_stream)
     buf = _ws.get(key)
     if buf is None or buf.numel() < nbytes:
+        if buf is not None:
+            buf.record_stream(stream)
         _ws[key] = None
         buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
         _ws[key] = buf
+    buf.record_stream(stream)
     oz2_set_workspace(buf.data_ptr(), buf.numel())
 
 
@@ -256,24 +314,12 @@ def _colmajor(X):
 
 
 def dgemm(A, B, alpha=1.0, beta=0.0, C=None, num_moduli=13, mode=None, scheme=None):
-    """C <- alpha A @ B + beta C on torch float64 CUDA tensors via oz2_dgemm.
+    """C <- alpha A @ B + beta C on torch float64 CUDA tensors via oz2_dgemm_ex.
 
-    Any 2-D strided layout is accepted; the result is column-major (Fortran order).
-    ``mode`` ("accurate" / "fast") and ``scheme`` ("fp8" / "int8" / "karatsuba") apply to this call
-    only; None keeps the thread's setting."""
-    prev_mode, prev_scheme = oz2_get_mode(), oz2_get_scheme()
-    if mode is not None:
-        _check(oz2_set_mode(mode), "oz2_set_mode")
-    if scheme is not None:
-        _check(oz2_set_scheme(scheme), "oz2_set_scheme")
-    try:
-        return _dgemm(A, B, alpha, beta, C, num_moduli)
-    finally:
-        oz2_set_mode(prev_mode)
-        oz2_set_scheme(prev_scheme)
-
-
-def _dgemm(A, B, alpha, beta, C, num_moduli):
+    Any 2-D strided layout is accepted for A, B and C; a new C is column-major (Fortran
+    order).  ``mode`` ("accurate" / "fast") and ``scheme`` ("fp8" / "int8" / "karatsuba")
+    apply to this call only (oz2_options.set_mode / set_scheme); None keeps the thread's
+    setting."""
     import torch
     assert A.dtype == torch.float64 and B.dtype == torch.float64
     m, k = A.shape
@@ -282,21 +328,34 @@ def _dgemm(A, B, alpha, beta, C, num_moduli):
     if C is None:
         C = torch.empty((n, m), dtype=torch.float64, device=A.device).t()
         beta = 0.0
+    assert C.shape == (m, n) and C.dtype == torch.float64
+    opt = oz2_options()
+    if mode is not None:
+        opt.set_mode, opt.mode = 1, _MODES.get(mode, mode)
+    if scheme is not None:
+        opt.set_scheme, opt.scheme = 1, _SCHEMES.get(scheme, scheme)
     A_, ta, lda = _colmajor(A)
     B_, tb, ldb = _colmajor(B)
-    if C.stride(0) == 1:
-        C_, ldc = C, max(1, C.stride(1))
+    s0, s1 = C.stride()
+    if s0 == 1 and s1 >= max(1, m):
         ws = oz2_workspace_size(ta, tb, m, n, k, num_moduli)
         _bind_stream_and_workspace(torch, A.device, ws)
-        _check(oz2_dgemm(ta, tb, m, n, k, alpha, A_.data_ptr(), lda, B_.data_ptr(), ldb, beta,
-                         C_.data_ptr(), ldc, num_moduli), "oz2_dgemm")
+        _check(oz2_dgemm_ex(ta, tb, m, n, k, alpha, A_.data_ptr(), lda, B_.data_ptr(), ldb, beta,
+                            C.data_ptr(), s1, num_moduli, opt), "oz2_dgemm_ex")
         return C
-    # row-major C: compute C^T = B^T A^T into the column-major view of C^T
-    Ct = C.t()
-    tb2 = "T" if tb == "N" else "N"
-    ta2 = "T" if ta == "N" else "N"
-    ws = oz2_workspace_size(tb2, ta2, n, m, k, num_moduli)
-    _bind_stream_and_workspace(torch, A.device, ws)
-    _check(oz2_dgemm(tb2, ta2, n, m, k, alpha, B_.data_ptr(), ldb, A_.data_ptr(), lda, beta,
-                     Ct.data_ptr(), max(1, Ct.stride(1)), num_moduli), "oz2_dgemm")
+    if s1 == 1 and s0 >= max(1, n):
+        # row-major C: compute C^T = B^T A^T into the column-major view of C^T
+        tb2 = "T" if tb == "N" else "N"
+        ta2 = "T" if ta == "N" else "N"
+        ws = oz2_workspace_size(tb2, ta2, n, m, k, num_moduli)
+        _bind_stream_and_workspace(torch, A.device, ws)
+        _check(oz2_dgemm_ex(tb2, ta2, n, m, k, alpha, B_.data_ptr(), ldb, A_.data_ptr(), lda, beta,
+                            C.data_ptr(), s0, num_moduli, opt), "oz2_dgemm_ex")
+        return C
+    # any other view (e.g. C[:, ::2]): compute into a column-major temporary, copy back
+    T = torch.empty((n, m), dtype=torch.float64, device=C.device).t()
+    if beta != 0.0:
+        T.copy_(C)
+    dgemm(A, B, alpha=alpha, beta=beta, C=T, num_moduli=num_moduli, mode=mode, scheme=scheme)
+    C.copy_(T)
     return C

@@ -29,3 +29,20 @@ def facts():
 @pytest.fixture(scope="session")
 def spec():
     return load_golden("spec_examples.json")
+
+
+@pytest.fixture
+def knobs():
+    """knobs(cta_group=1, mod_split=0, ...) sets the library's tuning knobs for the calling
+    thread (OZ2_TUNE_*, schedule only); each knob gets its previous value back after the
+    test."""
+    import paper_2603_10634_b200 as P
+    prev = {}
+
+    def set_(**kw):
+        for k, v in kw.items():
+            prev.setdefault(k, P.oz2_get_tuning(k))
+            assert P.oz2_set_tuning(k, int(v)) == 0, (k, v)
+    yield set_
+    for k, v in prev.items():
+        P.oz2_set_tuning(k, v)

@@ -69,10 +69,9 @@ def test_blocked_layouts_alpha_beta(dev, ta, tb):
     assert np.array_equal(out["C_pad"], full["C_pad"])       # rows beyond m untouched
 
 
-def test_blocked_fused_crt_path(dev, monkeypatch):
-    """k >= 8192 with OZ2_FUSED_CRT=1 takes the CRT-in-epilogue path; blocks of 512 x 768."""
-    monkeypatch.setenv("OZ2_FUSED_CRT", "1")
-    monkeypatch.setenv("OZ2_MOD_SPLIT", "0")
+def test_blocked_fused_crt_path(dev, knobs):
+    """k >= 8192 with the fused CRT forced takes the CRT-in-epilogue path; blocks of 512 x 768."""
+    knobs(fused_crt=1, mod_split=0)
     m, k, n = 1100, 8192, 1300
     A = gen_host(m, k, "phi", phi=0.5, seed=46, order="F")
     B = gen_host(k, n, "phi", phi=0.5, seed=47, order="F")
@@ -122,8 +121,10 @@ def test_debug_outputs_force_unblocked(dev):
         assert dev.oz2_get_blocking() == (300, 280)
     finally:
         dev.oz2_set_blocking(0, 0)
-    ref = scheme.dgemm(A, B, 12, e_mu=out["e_mu"].tolist(), e_nu=out["e_nu"].tolist())
-    assert np.array_equal(out["C"], ref.C)
+    from sampled import check_sampled
+    check_sampled(A, B, 12, list(range(300)), list(range(280)),
+                  {"e_mu": out["e_mu"], "e_nu": out["e_nu"], "C": out["C"],
+                   "res": out["residues"]}, accuracy=False)
 
 
 @pytest.mark.parametrize("sch", ["int8", "karatsuba"])
@@ -131,7 +132,7 @@ def test_debug_outputs_force_unblocked(dev):
 @pytest.mark.parametrize("mb,nb", [(256, 512), (512, 256)])
 def test_blocked_other_schemes(dev, sch, mode, mb, nb):
     """The INT8 and Karatsuba-only schemes through m/n blocks: C and exponents identical to
-    the unblocked call of the same scheme (which the other files pin to the oracle)."""
+    the unblocked call of the same scheme, and the oracle's on one sampled entry per tile."""
     m, k, n = 700, 900, 800
     A = gen_host(m, k, "phi", phi=1.0, seed=95)
     B = gen_host(k, n, "phi", phi=1.0, seed=96)
@@ -140,3 +141,8 @@ def test_blocked_other_schemes(dev, sch, mode, mb, nb):
     full = run(A, B, 14, scheme=sch, mode=mode)
     assert np.array_equal(out["e_mu"], full["e_mu"]) and np.array_equal(out["e_nu"], full["e_nu"])
     assert np.array_equal(out["C"], full["C"])
+    from sampled import check_sampled, col_cover, tile_cover
+    I, J = tile_cover(m), col_cover(n)
+    check_sampled(A, B, 14, I, J, {"e_mu": out["e_mu"], "e_nu": out["e_nu"],
+                                   "C": out["C"][np.ix_(I, J)]},
+                  family="int8" if sch == "int8" else "karatsuba", mode=mode, accuracy=False)

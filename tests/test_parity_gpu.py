@@ -23,22 +23,18 @@ from synth import gen_host
 
 @pytest.fixture(scope="module", params=["cg1", "cg2", "cg4"])
 def dev(request):
-    """The library with each GEMM variant (OZ2_CG selects it per call): 128x256
+    """The library with each GEMM variant (OZ2_TUNE_CTA_GROUP, read per call): 128x256
     single-CTA tiles, 256x256 CTA-pair (tcgen05 cta_group::2) tiles, and clusters of two
     pairs sharing A by TMA multicast."""
-    import os
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import paper_2603_10634_b200 as P
     P.lib()
-    old = os.environ.get("OZ2_CG")
-    os.environ["OZ2_CG"] = request.param[2:]
+    P.oz2_reset_tuning()
+    assert P.oz2_set_tuning("cta_group", int(request.param[2:])) == 0
     yield P
-    if old is None:
-        os.environ.pop("OZ2_CG", None)
-    else:
-        os.environ["OZ2_CG"] = old
+    P.oz2_reset_tuning()
 
 
 _LUT = np.array([fp8.encode_int(v) for v in range(-16, 17)], dtype=np.uint8)
@@ -106,7 +102,28 @@ def test_fp8_bound_rounding_within_R5(dev):
 
 # ------------------------------------------------------------------ full pipeline parity
 
-def _compare(res, ref, A, B, N):
+def _certified_pairs(Aint, BintT, P, rows, cols):
+    """Condition 2 sum_h |a'_ih||b'_hj| < P for every (i, j) with i in rows
+    or j in cols, exactly in Python integers."""
+    absA = np.abs(Aint.astype(object))
+    absB = np.abs(BintT.astype(object))
+    for i in rows:
+        s = absB.dot(absA[i])                       # over all j
+        assert all(2 * int(v) < P for v in s), ("row", i)
+    for j in cols:
+        s = absA.dot(absB[j])                       # over all i
+        assert all(2 * int(v) < P for v in s), ("col", j)
+
+
+def _compare(res, ref, A, B, N, family=None):
+    """Stage-by-stage parity (bars in the module docstring).  Rows / columns whose GPU
+    exponent differs from the oracle's own (the R6 rounding window) are not skipped: the
+    oracle is re-run with the GPU's exponents (reading R13: given the exponents, the
+    residues and C are unique), the certified condition is checked exactly
+    for every pair they touch, and then EVERY residue and EVERY entry of C must be
+    bit-exact.  Returns the mask of entries whose row and column exponents agreed."""
+    if family is None:
+        family = "karatsuba" if ref.plan.moduli[0] == 513 else "hybrid"
     m, n = A.shape[0], B.shape[1]
     assert res["e_prime_a"].tolist() == ref.e_prime_A
     assert res["e_prime_b"].tolist() == ref.e_prime_B
@@ -125,28 +142,32 @@ def _compare(res, ref, A, B, N):
         assert g <= exact_max * (1 + 2.0 ** -23) and g >= exact_max * (1 - k * 2.0 ** -23)
     rows_ok = [res["e_mu"][i] == ref.e_mu[i] for i in range(m)]
     cols_ok = [res["e_nu"][j] == ref.e_nu[j] for j in range(n)]
-    # exponents may differ only where the oracle's own FP32 model rounds differently
+    # exponents may differ only where the tensor core's FP32 rounding of C-bar' moves the
+    # floor of eq. mu-computation: the GPU's offset must lie between the offsets of the
+    # exact maximum and of its k 2^-23 underestimate
+    Pp, dlt = ref.Pp, ref.delta
     for i in range(m):
         if not rows_ok[i]:
-            Pp, dlt = ref.Pp, ref.delta
             lo = scheme.scaling_offset(Fraction(float(Cx[i].max())) * (1 - Fraction(k, 2 ** 23)), k, Pp, dlt)
             hi = scheme.scaling_offset(Fraction(float(Cx[i].max())), k, Pp, dlt)
             assert hi <= res["e_mu"][i] - ref.e_prime_A[i] <= lo
     for j in range(n):
         if not cols_ok[j]:
-            Pp, dlt = ref.Pp, ref.delta
             lo = scheme.scaling_offset(Fraction(float(Cx[:, j].max())) * (1 - Fraction(k, 2 ** 23)), k, Pp, dlt)
             hi = scheme.scaling_offset(Fraction(float(Cx[:, j].max())), k, Pp, dlt)
             assert hi <= res["e_nu"][j] - ref.e_prime_B[j] <= lo
     assert sum(rows_ok) >= m - 1 and sum(cols_ok) >= n - 1
+    if all(rows_ok) and all(cols_ok):
+        ref2 = ref
+    else:
+        ref2 = scheme.dgemm(A, B, N, e_mu=[int(v) for v in res["e_mu"]],
+                            e_nu=[int(v) for v in res["e_nu"]], family=family)
+        _certified_pairs(ref2.extra["Aint"], ref2.extra["BintT"], ref2.plan.P,
+                         [i for i in range(m) if not rows_ok[i]],
+                         [j for j in range(n) if not cols_ok[j]])
     for l in range(N):
-        for i in range(m):
-            if not rows_ok[i]:
-                continue
-            want = ref.residues[l][i]
-            got = res["residues"][l][i]
-            mask = np.array(cols_ok)
-            assert np.array_equal(got[mask], want[mask]), (l, i)
+        assert np.array_equal(res["residues"][l], ref2.residues[l]), l
+    assert np.array_equal(res["C"], ref2.C)
     mask = np.outer(rows_ok, cols_ok)
     assert np.array_equal(res["C"][mask], ref.C[mask])
     return mask
@@ -211,15 +232,14 @@ _SCHED_REF = {}
 
 @pytest.mark.parametrize("split", ["0", "1"])
 @pytest.mark.parametrize("sch", ["fp8", "int8"])
-def test_work_item_schedules(dev, split, sch, monkeypatch):
+def test_work_item_schedules(dev, split, sch, knobs):
     """Both residue-GEMM schedules -- tile-major (every modulus of a tile in one work item,
     CRT fused into the epilogue for k >= 8192) and modulus-split (one (tile, modulus) item,
     separate CRT; automatic for grids with few tiles) -- give the oracle's residues and C
     bit for bit (imported exponents), with alpha/beta and k >= 8192."""
     from gpu_helpers import run
     from oracle import int8
-    monkeypatch.setenv("OZ2_MOD_SPLIT", split)
-    monkeypatch.setenv("OZ2_FUSED_CRT", "1")        # tile-major then fuses (k >= 8192)
+    knobs(mod_split=split, fused_crt=1)             # tile-major then fuses (k >= 8192)
     m, k, n, N = 16, 8200, 24, 13
     A = gen_host(m, k, "phi", phi=1.0, seed=51)
     B = gen_host(k, n, "phi", phi=1.0, seed=52)
@@ -236,29 +256,35 @@ def test_work_item_schedules(dev, split, sch, monkeypatch):
 
 
 @pytest.mark.parametrize("sch", ["fp8", "int8", "karatsuba"])
-def test_work_item_schedules_agree_many_tiles(dev, sch, monkeypatch):
+def test_work_item_schedules_agree_many_tiles(dev, sch, knobs):
     """Tile-major (fused CRT) and modulus-split schedules on a grid of 4 x 5 CTA-pair tiles
-    with ragged edges: identical residues and C (both are exact)."""
+    with ragged edges: identical residues and C (both are exact), and the oracle's on one
+    sampled entry per tile (exponents, residues and C, tests/sampled.py)."""
     from gpu_helpers import run
     m, k, n, N = 1000, 8192, 1100, 14
     A = gen_host(m, k, "phi", phi=2.0, seed=53)
     B = gen_host(k, n, "phi", phi=2.0, seed=54)
     outs = []
-    monkeypatch.setenv("OZ2_FUSED_CRT", "1")        # tile-major then fuses (k >= 8192)
     for split in ["0", "1"]:
-        monkeypatch.setenv("OZ2_MOD_SPLIT", split)
+        knobs(fused_crt=1, mod_split=split)        # tile-major then fuses (k >= 8192)
         outs.append(run(A, B, N, scheme=sch))
-    monkeypatch.setenv("OZ2_FUSED_CRT", "0")        # tile-major with the separate CRT
-    monkeypatch.setenv("OZ2_MOD_SPLIT", "0")
+    knobs(fused_crt=0, mod_split=0)                # tile-major with the separate CRT
     outs.append(run(A, B, N, scheme=sch))
     assert np.array_equal(outs[0]["C"], outs[2]["C"])
-    monkeypatch.setenv("OZ2_MOD_SPLIT", "2")        # hybrid: full waves tile-major, tail split
+    knobs(mod_split=2)                             # hybrid: full waves tile-major, tail split
     outs.append(run(A, B, N, scheme=sch))
     assert np.array_equal(outs[0]["residues"], outs[3]["residues"])
     assert np.array_equal(outs[0]["C"], outs[3]["C"])
     assert np.array_equal(outs[0]["e_mu"], outs[1]["e_mu"])
     assert np.array_equal(outs[0]["residues"], outs[1]["residues"])
     assert np.array_equal(outs[0]["C"], outs[1]["C"])
+    from sampled import check_sampled, col_cover, tile_cover
+    I, J = tile_cover(m), col_cover(n)
+    o = outs[0]
+    gpu = {"e_mu": o["e_mu"], "e_nu": o["e_nu"], "C": o["C"][np.ix_(I, J)],
+           "res": np.array([R[np.ix_(I, J)] for R in o["residues"]])}
+    fam = {"fp8": "hybrid", "int8": "int8", "karatsuba": "karatsuba"}[sch]
+    check_sampled(A, B, N, I, J, gpu, family=fam, accuracy=False)
 
 
 def test_alpha_beta_and_quick_returns(dev):
@@ -320,12 +346,12 @@ def test_host_pointer_path(dev):
 
 
 @pytest.mark.parametrize("blocks", ["1", "4", "3"])
-def test_host_pointer_column_blocks(dev, blocks, monkeypatch):
+def test_host_pointer_column_blocks(dev, blocks, knobs):
     """Host buffers with C returned in column blocks (each block's device-to-host copy
-    overlaps the next block's GEMMs; OZ2_HOST_BLOCKS): bit-identical to the device-pointer
+    overlaps the next block's GEMMs; OZ2_TUNE_HOST_BLOCKS): bit-identical to the device-pointer
     call, including a ragged last block, ldc padding, beta != 0 and transposed A."""
     from gpu_helpers import run
-    monkeypatch.setenv("OZ2_HOST_BLOCKS", blocks)
+    knobs(host_blocks=blocks)
     m, k, n = 300, 260, 2600
     A = gen_host(m, k, "phi", phi=1.0, seed=21)
     B = gen_host(k, n, "phi", phi=1.0, seed=22)
@@ -401,15 +427,14 @@ _LONGK_REF = {}
 
 @pytest.mark.parametrize("fam", ["hybrid", "karatsuba"])
 @pytest.mark.parametrize("sched", ["split", "tile_fused"])
-def test_k_beyond_exactness_window(dev, fam, sched, monkeypatch):
+def test_k_beyond_exactness_window(dev, fam, sched, knobs):
     """k > 2^16 (NEXT-2): products run in 2^16-long K segments reduced mod p; residues and C
     stay bit-exact against the oracle, which needs no segmentation (exact integers) -- for
     both FP8 families and both work-item schedules (tile-major with the fused CRT)."""
     from gpu_helpers import run
     m, k, n, N = 16, 65536 + 300, 24, 12 if fam == "hybrid" else 13
     if sched == "tile_fused":
-        monkeypatch.setenv("OZ2_MOD_SPLIT", "0")
-        monkeypatch.setenv("OZ2_FUSED_CRT", "1")
+        knobs(mod_split=0, fused_crt=1)
     A = gen_host(m, k, "phi", phi=1.0, seed=61)
     B = gen_host(k, n, "phi", phi=1.0, seed=62)
     if fam not in _LONGK_REF:
@@ -574,9 +599,9 @@ B = gen_device(k, n, "phi", phi=1.0, seed=92)
 C = torch.empty((n, m), dtype=torch.float64, device="cuda").t()
 P.oz2_set_stream(torch.cuda.current_stream().cuda_stream)
 assert P.oz2_set_scheme(sch) == 0
+assert P.oz2_set_tuning("cta_group", int(sys.argv[2])) == 0
 for split in ("0", "1", "2"):
-    import os
-    os.environ["OZ2_MOD_SPLIT"] = split
+    assert P.oz2_set_tuning("mod_split", int(split)) == 0
     assert P.oz2_dgemm("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0, C.data_ptr(), m, 13) == 0
     torch.cuda.synchronize()
     print(split, hashlib.sha256(C.cpu().numpy().tobytes()).hexdigest())
@@ -585,22 +610,48 @@ for split in ("0", "1", "2"):
 
 @pytest.mark.parametrize("sch", ["fp8", "int8", "karatsuba"])
 def test_gemm_variants_identical(dev, sch):
-    """OZ2_CG = 1 (128x256 CTAs), 2 (CTA pairs, default), 4 (two pairs multicasting A; FP8
-    kinds only, INT8 falls back to pairs) give identical C under both work-item schedules.
-    Each variant runs in a subprocess with a timeout, so a pipeline hang fails the test."""
+    """CTA group 1 (128x256 CTAs), 2 (CTA pairs, default), 4 (two pairs multicasting A; FP8
+    kinds only, INT8 falls back to pairs) give identical C under all three work-item
+    schedules, and that C is the oracle's on one sampled entry per 256 x 256 tile.  Each
+    variant runs in a subprocess with a timeout, so a pipeline hang fails the test."""
+    import hashlib
     import os
     import subprocess
     import sys
+    import torch
+    from sampled import check_sampled, col_cover, tile_cover
+    from synth import gen_device
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = {}
     for cg in ["1", "2", "4"]:
-        env = dict(os.environ, OZ2_CG=cg)
-        r = subprocess.run([sys.executable, "-c", _CG_SNIPPET, sch], cwd=root, env=env,
+        r = subprocess.run([sys.executable, "-c", _CG_SNIPPET, sch, cg], cwd=root,
                            capture_output=True, text=True, timeout=240)
         assert r.returncode == 0, r.stderr[-2000:]
         outs[cg] = r.stdout.split()
     assert outs["1"] == outs["2"] == outs["4"]
     assert outs["2"][1] == outs["2"][3] == outs["2"][5]   # tile-major, split and hybrid agree
+    # the same problem in-process (default kernels) with exponent outputs -> the oracle
+    m, n, k = 2560, 2560, 1024
+    A = gen_device(m, k, "phi", phi=1.0, seed=91)
+    B = gen_device(k, n, "phi", phi=1.0, seed=92)
+    C = torch.empty((n, m), dtype=torch.float64, device="cuda").t()
+    e_mu = torch.zeros(m, dtype=torch.int32, device="cuda")
+    e_nu = torch.zeros(n, dtype=torch.int32, device="cuda")
+    opt = dev.oz2_options()
+    opt.e_mu, opt.e_nu = e_mu.data_ptr(), e_nu.data_ptr()
+    opt.set_scheme, opt.scheme = 1, {"fp8": 0, "int8": 1, "karatsuba": 2}[sch]
+    dev.oz2_set_stream(torch.cuda.current_stream().cuda_stream)
+    dev.oz2_set_workspace(None, 0)
+    assert dev.oz2_dgemm_ex("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0,
+                            C.data_ptr(), m, 13, opt) == 0
+    torch.cuda.synchronize()
+    Ch = C.cpu().numpy()
+    assert hashlib.sha256(Ch.tobytes()).hexdigest() == outs["2"][1]
+    I, J = tile_cover(m), col_cover(n)
+    fam = {"fp8": "hybrid", "int8": "int8", "karatsuba": "karatsuba"}[sch]
+    check_sampled(A.cpu().numpy(), B.cpu().numpy(), 13, I, J,
+                  {"e_mu": e_mu.cpu().numpy(), "e_nu": e_nu.cpu().numpy(), "C": Ch[np.ix_(I, J)]},
+                  family=fam, accuracy=False)
 
 
 @pytest.mark.parametrize("ea,eb", [(-600, -400), (500, 500), (-1030, 1000)])

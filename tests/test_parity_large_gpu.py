@@ -12,6 +12,7 @@ pytestmark = pytest.mark.gpu
 
 from oracle import exact, scheme
 from synth import gen_device
+from sampled import check_sampled, col_cover, tile_cover
 
 
 @pytest.fixture(scope="module")
@@ -51,8 +52,8 @@ def _run_sampled(P, m, k, n, N, phi, seed, I, J, mode="accurate"):
     res3 = res.view(N, n, m)
     out = {
         "C": C[It][:, Jt].cpu().numpy(),
-        "e_mu": e_mu[It].cpu().numpy(),
-        "e_nu": e_nu[Jt].cpu().numpy(),
+        "e_mu": e_mu.cpu().numpy(),
+        "e_nu": e_nu.cpu().numpy(),
         "res": res3[:, Jt][:, :, It].permute(0, 2, 1).cpu().numpy(),     # [l][a][b]
         "A_rows": A[It].cpu().numpy(),
         "B_cols": B[:, Jt].cpu().numpy(),
@@ -74,41 +75,36 @@ def _fast_exps(X, rows, N):
     return scheme.fast_exponents(e_prime, codes, plan, zero)
 
 
-def _check(out, N, I, J, ref_exps=None, mode="accurate"):
-    A, B = out["A"], out["B"]
-    k = A.shape[1]
-    if mode == "fast":
-        emu, enu = _fast_exps(A, I, N), _fast_exps(B.T, J, N)
-    elif ref_exps is None:
-        _, emu, _ = scheme.row_exponents(A, I, B.T, N)
-        _, enu, _ = scheme.row_exponents(B.T, J, A, N)
-    else:
-        emu, enu = ref_exps
-    assert np.array_equal(out["e_mu"], emu) and np.array_equal(out["e_nu"], enu)
-    res, Cref = scheme.entries(A, B, N, I, J, list(emu), list(enu))
-    assert np.array_equal(out["res"], res)
-    assert np.array_equal(out["C"], Cref)
-    ex = exact.exact_entries(A, B, I, J)
-    bound = exact.apriori_bound(A[I], B[:, J], list(emu), list(enu))
-    assert np.all(np.abs(out["C"] - ex) <= 2 * bound + np.abs(ex) * 2.0 ** -52)
-    return float(np.linalg.norm(out["C"] - ex) / np.linalg.norm(ex))
+def _check(out, N, I, J, mode="accurate"):
+    return check_sampled(out["A"], out["B"], N, I, J, out, mode=mode)
 
 
 @pytest.mark.parametrize("phi", [0.0, 4.0])
 def test_config2_8192_moduli_sweep(dev, phi):
-    """BASELINE config 2: m=n=k=8192, N in 12..20, accuracy vs exact falls with N."""
+    """BASELINE config 2: m=n=k=8192, N in 12..20, accuracy vs exact falls with N.  At
+    N = 13 the sample covers every 256 x 256 tile (the hybrid schedule: 13 full waves
+    tile-major, the ragged last wave split into (tile, modulus) items, separate CRT)."""
     m = n = k = 8192
-    I, J = [0, 4097, 8191], [1, 5000, 8190]
     errs = []
-    for N in [12, 16, 20]:
+    for N in [12, 13, 16, 20]:
+        if N == 13:
+            I, J = tile_cover(m), col_cover(n)
+        else:
+            I, J = [0, 4097, 8191], [1, 5000, 8190]
         out = _run_sampled(dev, m, k, n, N, phi, 11, I, J)
-        errs.append(_check(out, N, I, J))
+        e = _check(out, N, I, J)
+        if N != 13:
+            errs.append(e)
     assert errs[1] <= errs[0] and errs[2] <= max(errs[1], 2e-17)
 
 
 def test_config3_16384_bench_workload(dev):
-    """BASELINE config 3 as bench.py runs it: m=n=k=16384, phi=1, N=13."""
-    I, J = [3, 9000, 16383], [0, 12345]
+    """BASELINE config 3 as bench.py runs it (m=n=k=16384, phi=1, N=13, default kernels:
+    CTA pairs, tile-major persistent schedule with the CRT fused and deferred into the
+    next tile's epilogues): 64 x 64 sampled entries, one per output tile -- every tile,
+    both CTAs of each pair, all four TMEM lane quadrants, both epilogue column halves."""
+    I, J = tile_cover(16384), col_cover(16384)
+    assert len(I) == len(J) == 64
     out = _run_sampled(dev, 16384, 16384, 16384, 13, 1.0, 21, I, J)
     err = _check(out, 13, I, J)
     assert err < 1e-15
@@ -116,8 +112,9 @@ def test_config3_16384_bench_workload(dev):
 
 @pytest.mark.parametrize("N,phi", [(12, 0.0), (13, 1.0)])
 def test_config4_large_k_65536(dev, N, phi):
-    """BASELINE config 4: m=n=4096, k=65536 -- the FP32 exactness limit k = 2^16."""
-    I, J = [0, 2048, 4095], [7, 4000]
+    """BASELINE config 4: m=n=4096, k=65536 -- the FP32 exactness limit k = 2^16; every
+    tile sampled."""
+    I, J = tile_cover(4096), col_cover(4096)
     out = _run_sampled(dev, 4096, 65536, 4096, N, phi, 31, I, J)
     _check(out, N, I, J)
 
@@ -126,7 +123,7 @@ def test_config4_large_k_65536(dev, N, phi):
 def test_config3_16384_fast_mode(dev, N):
     """Fast mode (R15) at the bench workload: exponents, residues and C bit-exact on the
     sampled entries; fast mode with N = 13 stays within the FP64-level band."""
-    I, J = [3, 9000, 16383], [0, 12345]
+    I, J = tile_cover(16384)[::4], col_cover(16384)[1::4]
     out = _run_sampled(dev, 16384, 16384, 16384, N, 1.0, 21, I, J, mode="fast")
     err = _check(out, N, I, J, mode="fast")
     assert err < 1e-14

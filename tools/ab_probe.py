@@ -1,9 +1,8 @@
-"""A/B an environment knob of liboz2 in ONE process, alternating settings call by call
-(so clock / power drift hits both arms alike).
+"""A/B a tuning knob of liboz2 (oz2_set_tuning, names in paper_2603_10634_b200.TUNE) in ONE
+process, alternating settings call by call (so clock / power drift hits both arms alike).
 
-    python tools/ab_probe.py SIZE N VAR VAL_A VAL_B [rounds] [k] [scheme]
+    python tools/ab_probe.py SIZE N KNOB VAL_A VAL_B [rounds] [k] [scheme]
 """
-import os
 import statistics
 import sys
 import torch
@@ -27,7 +26,7 @@ P.oz2_set_timing(True)
 res = {v: [] for v in vals}
 for r in range(rounds + 1):
     for v in (vals if r % 2 == 0 else vals[::-1]):
-        os.environ[var] = v
+        assert P.oz2_set_tuning(var, int(v)) == 0
         assert P.oz2_dgemm("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0, C.data_ptr(), m, N) == 0
         t = P.oz2_get_timing()
         if r > 0:
