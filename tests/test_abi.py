@@ -174,3 +174,32 @@ def test_int8_scheme_plan_matches_oracle(oz2mod):
         oz2mod.oz2_set_scheme("fp8")
     w_fp8 = oz2mod.oz2_workspace_size("N", "N", 4096, 4096, 4096, 14)
     assert w8 < w_fp8
+
+
+def test_tuning_knobs_host_only(oz2mod):
+    """oz2_set_tuning validates knob and range, oz2_get_tuning reads back, reset restores
+    the defaults (include/oz2.h OZ2_TUNE_*); no environment variable is consulted."""
+    P = oz2mod
+    P.oz2_reset_tuning()
+    defaults = {k: P.oz2_get_tuning(k) for k in P.TUNE}
+    assert defaults["cta_group"] == 2 and defaults["mod_split"] == -1 and defaults["sq_order"] == 1
+    assert P.oz2_set_tuning("cta_group", 3) == -2
+    assert P.oz2_set_tuning(99, 1) == -1
+    assert P.oz2_set_tuning("sync_chunk", 0) == -2
+    assert P.oz2_set_tuning("cta_group", 1) == 0 and P.oz2_get_tuning("cta_group") == 1
+    with P.tuning(mod_split=2, fused_crt=0):
+        assert P.oz2_get_tuning("mod_split") == 2 and P.oz2_get_tuning("fused_crt") == 0
+    assert P.oz2_get_tuning("mod_split") == -1
+    P.oz2_reset_tuning()
+    assert {k: P.oz2_get_tuning(k) for k in P.TUNE} == defaults
+    src = open(os.path.join(ROOT, "paper_2603_10634_b200", "csrc", "oz2_api.cu")).read()
+    for f in ["oz2_api.cu", "gemm_kernel.cu", "crt_kernel.cu", "prep_kernels.cu"]:
+        src = open(os.path.join(ROOT, "paper_2603_10634_b200", "csrc", f)).read()
+        assert "getenv" not in src, f
+
+
+def test_options_struct_layout(oz2mod):
+    """The ctypes mirror of oz2_options has the C layout: 13 pointers, timing_ms, four
+    int32 settings and four reserved int32 (x86-64: 14 * 8 + 8 * 4 = 144 bytes)."""
+    import ctypes
+    assert ctypes.sizeof(oz2mod.oz2_options) == 14 * 8 + 8 * 4

@@ -345,11 +345,13 @@ def test_host_pointer_path(dev):
     assert np.array_equal(C, run(A, B, 13)["C"])
 
 
-@pytest.mark.parametrize("blocks", ["1", "4", "3"])
-def test_host_pointer_column_blocks(dev, blocks, knobs):
+@pytest.mark.parametrize("blocks,pinned", [("1", True), ("4", True), ("3", True), ("4", False)])
+def test_host_pointer_column_blocks(dev, blocks, pinned, knobs):
     """Host buffers with C returned in column blocks (each block's device-to-host copy
-    overlaps the next block's GEMMs; OZ2_TUNE_HOST_BLOCKS): bit-identical to the device-pointer
-    call, including a ragged last block, ldc padding, beta != 0 and transposed A."""
+    overlaps the next block's GEMMs; OZ2_TUNE_HOST_BLOCKS, pinned C only -- pageable C is
+    copied in one piece): bit-identical to the device-pointer call, including a ragged
+    last block, ldc padding, beta != 0 and transposed A."""
+    import torch
     from gpu_helpers import run
     knobs(host_blocks=blocks)
     m, k, n = 300, 260, 2600
@@ -359,7 +361,10 @@ def test_host_pointer_column_blocks(dev, blocks, knobs):
     At = np.asfortranarray(A.T)                       # op(A) = A with transa = 'T'
     Bh = np.asfortranarray(B)
     ldc = m + 5
-    Ch = np.asfortranarray(np.zeros((ldc, n)))
+    if pinned:
+        Ch = torch.zeros((n, ldc), dtype=torch.float64, pin_memory=True).numpy().T
+    else:
+        Ch = np.asfortranarray(np.zeros((ldc, n)))
     Ch[:m] = C0
     rc = dev.oz2_dgemm("T", "N", m, n, k, 0.5, At.ctypes.data, k, Bh.ctypes.data, k, -1.5,
                        Ch.ctypes.data, ldc, 13)
@@ -367,6 +372,72 @@ def test_host_pointer_column_blocks(dev, blocks, knobs):
     ref = run(A, B, 13, alpha=0.5, beta=-1.5, C0=C0)["C"]
     assert np.array_equal(Ch[:m], ref)
     assert np.all(Ch[m:] == 0.0)
+
+
+def test_per_call_options(dev):
+    """oz2_options.set_mode / set_scheme apply to one call only and equal the thread-level
+    setting; timing_ms receives the phase times (total = sum of the phases)."""
+    import ctypes
+    import torch
+    m, k, n = 300, 400, 260
+    A = torch.from_numpy(gen_host(m, k, "phi", phi=1.0, seed=15)).cuda()
+    B = torch.from_numpy(gen_host(k, n, "phi", phi=1.0, seed=16)).cuda()
+    A = A.t().contiguous().t()
+    B = B.t().contiguous().t()
+    outs = {}
+    for mode, sch in [("fast", "fp8"), ("accurate", "int8"), ("fast", "karatsuba")]:
+        C1 = torch.zeros((n, m), dtype=torch.float64, device="cuda").t()
+        C2 = torch.zeros((n, m), dtype=torch.float64, device="cuda").t()
+        opt = dev.oz2_options()
+        opt.set_mode, opt.mode = 1, {"accurate": 0, "fast": 1}[mode]
+        opt.set_scheme, opt.scheme = 1, {"fp8": 0, "int8": 1, "karatsuba": 2}[sch]
+        ms = (ctypes.c_float * 7)()
+        opt.timing_ms = ctypes.addressof(ms)
+        dev.oz2_set_stream(torch.cuda.current_stream().cuda_stream)
+        dev.oz2_set_workspace(None, 0)
+        assert dev.oz2_dgemm_ex("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0,
+                                C1.data_ptr(), m, 14, opt) == 0
+        assert dev.oz2_get_mode() == 0 and dev.oz2_get_scheme() == 0     # thread settings untouched
+        assert ms[6] > 0 and abs(sum(ms[:6]) - ms[6]) < 0.05 * ms[6] + 0.05
+        dev.oz2_set_mode(mode)
+        dev.oz2_set_scheme(sch)
+        try:
+            assert dev.oz2_dgemm("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0,
+                                 C2.data_ptr(), m, 14) == 0
+        finally:
+            dev.oz2_set_mode("accurate")
+            dev.oz2_set_scheme("fp8")
+        torch.cuda.synchronize()
+        assert torch.equal(C1, C2)
+        outs[(mode, sch)] = C1
+    assert not torch.equal(outs[("fast", "fp8")], outs[("fast", "karatsuba")])
+    bad = dev.oz2_options()
+    bad.set_mode, bad.mode = 1, 7
+    C = torch.zeros((n, m), dtype=torch.float64, device="cuda").t()
+    assert dev.oz2_dgemm_ex("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0,
+                            C.data_ptr(), m, 14, bad) == -15
+
+
+def test_torch_wrapper_strided_C(dev):
+    """dgemm() into a non-contiguous view (every other column of a larger matrix): the
+    other columns stay untouched and the view gets the same C as a dense call."""
+    import torch
+    A = torch.from_numpy(gen_host(70, 90, "phi", phi=1.0, seed=17)).cuda()
+    B = torch.from_numpy(gen_host(90, 40, "phi", phi=1.0, seed=18)).cuda()
+    big = torch.full((70, 80), 7.0, dtype=torch.float64, device="cuda")
+    view = big[:, ::2]
+    dev.dgemm(A, B, C=view, num_moduli=13)
+    ref = dev.dgemm(A, B, num_moduli=13)
+    assert torch.equal(view, ref)
+    assert torch.all(big[:, 1::2] == 7.0)
+    C0 = torch.from_numpy(gen_host(70, 40, "uniform", seed=19)).cuda()
+    big2 = torch.zeros((80, 70), dtype=torch.float64, device="cuda").t()[:, :40]   # col-major, ld 70
+    big2.copy_(C0)
+    dev.dgemm(A, B, alpha=2.0, beta=-1.0, C=big2, num_moduli=13)
+    big3 = torch.zeros((40, 140), dtype=torch.float64, device="cuda").t()[::2]      # stride (2, 140)
+    big3.copy_(C0)
+    dev.dgemm(A, B, alpha=2.0, beta=-1.0, C=big3, num_moduli=13)
+    assert torch.equal(big2, big3)
 
 
 def test_torch_wrapper_layouts(dev):
