@@ -17,7 +17,10 @@ Printed JSON line (rank 0): the contract keys plus
                 (MEASURED_PEAKS.json x the nominal fp8/bf16 ratio 4.5/2.25)
   e2e           the same metric through oz2_dgemm with pinned HOST buffers (H2D of A, B
                 and D2H of C inside the timed region)
-  cpu_baseline  the oracle (oracle/, pure Python + numpy) on a bounded sub-block
+  cpu_baseline  the oracle (oracle/, pure Python + numpy) on bounded sub-blocks, one per
+                host core in parallel (cpu_baseline_1core: the same on one core)
+  vendor_fp8    cuBLASLt FP8 (torch._scaled_mm) burst / sustained on the same box: the
+                vendor ceiling for the residue GEMMs (roofline.frac_vs_vendor_fp8_sustained)
   cublas        native torch.matmul float64 (cuBLAS DGEMM) on the same inputs
   accuracy      normwise / max relative error of oz2 and of cuBLAS against the exact
                 product on sampled entries, and the moduli sweep (N = 12..16)
@@ -54,6 +57,14 @@ def parse():
     ap.add_argument("--mode", default="accurate", choices=["accurate", "fast"],
                     help="scaling mode (fast: Cauchy-Schwarz bound, no bound GEMM; DESIGN.md R15)")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e/cuBLAS/accuracy/sweep/cpu legs")
+    ap.add_argument("--m-total", type=int, default=0,
+                    help="strong scaling: total rows of A/C split over the ranks (BASELINE config 5: "
+                         "--size 32768 --m-total 32768); 0 = weak scaling, --size rows per rank")
+    ap.add_argument("--panels", type=int, default=0,
+                    help="N > 1: broadcast B in this many column panels overlapped with the per-panel "
+                         "calls (0 = 4 when N > 1)")
+    ap.add_argument("--tune", action="append", default=[], metavar="KNOB=VALUE",
+                    help="liboz2 tuning knob (paper_2603_10634_b200.TUNE), repeatable")
     return ap.parse_args()
 
 
@@ -146,6 +157,62 @@ def two_prod_exact_dot(a, b):
     return math.fsum(np.concatenate([p, e]).tolist())
 
 
+def vendor_fp8_ceiling(torch, local_rank, size=16384, sustain_s=4.0):
+    """cuBLASLt FP8 (torch._scaled_mm, E4M3 x E4M3 -> FP32 accumulate, bf16 out) on the same
+    box: burst (best of 10) and sustained (back to back for `sustain_s` seconds, clocks
+    sampled), the vendor's ceiling for the residue GEMMs (P:652 uses cuBLASLt, P:711 quotes
+    ~3 PFLOP/s).  Operands hold random integers in [-16, 16] -- the value class of the digit
+    planes -- and, for the burst figure, random normal E4M3 values too."""
+    out = {"kernel": "torch._scaled_mm (cuBLASLt) e4m3 x e4m3, fp32 accumulate, bf16 out",
+           "shape": f"{size}^3"}
+    try:
+        g = torch.Generator(device="cuda")
+        g.manual_seed(5)
+        one = torch.ones((), dtype=torch.float32, device="cuda")
+        data = {
+            "digits": (torch.randint(-16, 17, (size, size), generator=g, device="cuda").to(torch.float8_e4m3fn),
+                       torch.randint(-16, 17, (size, size), generator=g, device="cuda").to(torch.float8_e4m3fn)),
+            "normal": (torch.randn((size, size), generator=g, device="cuda").to(torch.float8_e4m3fn),
+                       torch.randn((size, size), generator=g, device="cuda").to(torch.float8_e4m3fn)),
+        }
+        flops = 2.0 * size ** 3
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for name, (a, b) in data.items():
+            f = lambda: torch._scaled_mm(a, b.t(), scale_a=one, scale_b=one, out_dtype=torch.bfloat16)
+            for _ in range(3):
+                f()
+            best = float("inf")
+            for _ in range(10):
+                e0.record()
+                f()
+                e1.record()
+                torch.cuda.synchronize()
+                best = min(best, e0.elapsed_time(e1))
+            out[f"burst_tflops_{name}"] = round(flops / (best * 1e-3) / 1e12, 1)
+        a, b = data["digits"]
+        f = lambda: torch._scaled_mm(a, b.t(), scale_a=one, scale_b=one, out_dtype=torch.bfloat16)
+        sampler = ClockSampler(local_rank)
+        sampler.start()
+        time.sleep(0.2)
+        reps, t0 = 0, time.perf_counter()
+        e0.record()
+        while time.perf_counter() - t0 < sustain_s:
+            for _ in range(20):
+                f()
+            reps += 20
+            torch.cuda.synchronize()
+        e1.record()
+        torch.cuda.synchronize()
+        out["sustained_tflops_digits"] = round(flops * reps / (e0.elapsed_time(e1) * 1e-3) / 1e12, 1)
+        out["sustained_clocks"] = sampler.stop()
+        out["sustained_seconds"] = sustain_s
+        del data, a, b
+        torch.cuda.empty_cache()
+    except Exception as e:            # report, never fail the bench on the probe
+        out["error"] = repr(e)[:300]
+    return out
+
+
 # ---------------------------------------------------------------------------------- oz2 arm
 
 def run_oz2(args, rank, world, local_rank):
@@ -159,8 +226,18 @@ def run_oz2(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     n = k = args.size
-    m = args.size                                   # rows per rank (weak scaling)
+    if args.m_total:                                # strong scaling: rows of A/C split over ranks
+        from paper_2603_10634_b200.dist import row_block
+        r0, r1 = row_block(args.m_total, rank, world)
+        m = r1 - r0
+    else:
+        m = args.size                               # rows per rank (weak scaling)
     N = args.moduli
+    for kv in args.tune:
+        kn, v = kv.split("=")
+        if P.oz2_set_tuning(kn, int(v)) != 0:
+            raise ValueError(f"bad --tune {kv}")
+    panels = args.panels or (4 if world > 1 else 1)
     A = gen_device(m, k, "phi", phi=args.phi, seed=1000 + rank, device="cuda")
     B = gen_device(k, n, "phi", phi=args.phi, seed=7, device="cuda") if rank == 0 else \
         torch.empty((n, k), dtype=torch.float64, device="cuda").t()
@@ -177,10 +254,22 @@ def run_oz2(args, rank, world, local_rank):
         raise RuntimeError("oz2_set_mode / oz2_set_scheme failed")
 
     Bt = B.t()                                   # contiguous (n x k) storage of column-major B
+    from paper_2603_10634_b200.dist import dgemm_rowsharded
+
+    def panel_gemm(A_, B_, alpha, beta, C_, num_moduli):
+        # the C ABI on the column panel (B_ and C_ are column-major views, ld = k and m)
+        rc = P.oz2_dgemm("N", "N", m, B_.shape[1], k, alpha, A_.data_ptr(), m, B_.data_ptr(), k, beta,
+                         C_.data_ptr(), m, num_moduli)
+        if rc != 0:
+            raise RuntimeError(f"oz2_dgemm rc={rc}")
+        return C_
 
     def step():
         if world > 1:
-            dist.broadcast(Bt, src=0)
+            # B broadcast from rank 0 in column panels, panel p's call overlapping the
+            # transfer of panels p+1.. (paper_2603_10634_b200.dist)
+            dgemm_rowsharded(A, B, C_local=C, num_moduli=N, gemm_fn=panel_gemm, panels=panels)
+            return
         rc = P.oz2_dgemm("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0, C.data_ptr(), m, N)
         if rc != 0:
             raise RuntimeError(f"oz2_dgemm rc={rc}")
@@ -198,12 +287,16 @@ def run_oz2(args, rank, world, local_rank):
     torch.cuda.synchronize()
     sampler.start()
     time.sleep(0.3)
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     ev0.record()
-    for _ in range(args.steps):
+    step_ev[0].record()
+    for i in range(args.steps):
         step()
-        ph = P.oz2_get_timing()
-        for key, v in ph.items():
-            phase_acc.setdefault(key, []).append(v)
+        step_ev[i + 1].record()
+        if world == 1:               # phase timers of the single call (panelled steps: several calls)
+            ph = P.oz2_get_timing()
+            for key, v in ph.items():
+                phase_acc.setdefault(key, []).append(v)
     ev1.record()
     torch.cuda.synchronize()
     if world > 1:
@@ -233,8 +326,23 @@ def run_oz2(args, rank, world, local_rank):
         bcast = {"ms": round(bms, 3), "bytes": 8 * k * n, "algbw_gbs": round(8 * k * n / (bms * 1e-3) / 1e9, 1),
                  "share_of_step": round(bms / (ms_total / args.steps), 4), "backend": dist.get_backend()}
     ms_per_step = ms_total / args.steps
+    step_ms = [step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(args.steps)]
+    tm = torch.tensor([statistics.median(step_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    median_ms = tm.item()
     flops_rank = 2.0 * m * n * k
-    value = world * flops_rank * args.steps / (ms_total * 1e-3) / 1e12
+    total_flops = 2.0 * (args.m_total or world * m) * n * k
+    value = total_flops * args.steps / (ms_total * 1e-3) / 1e12
+    if world > 1:
+        # phase timers need a single call per step: one extra timed unpanelled call (rank-local)
+        P.oz2_set_timing(True)
+        for _ in range(2):
+            rc = P.oz2_dgemm("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0, C.data_ptr(), m, N)
+            assert rc == 0
+            for key, v in P.oz2_get_timing().items():
+                phase_acc.setdefault(key, []).append(v)
+        P.oz2_set_timing(False)
 
     phases = {key: statistics.median(v) for key, v in phase_acc.items()}
     peaks, peak_kind = measured_peaks()
@@ -296,22 +404,30 @@ def run_oz2(args, rank, world, local_rank):
                and (fenv > 0 or (fenv < 0 and k >= (49152 if args.scheme == "int8" else 16384))))
     mod_split = (ms_env == 1 or ms_env == 2) or (ms_env < 0 and (tiles < 8 * units or (ragged and not fusable)))
     fused = fusable and not mod_split
-    launches_per_step = 8 + (args.mode == "accurate") + (not fused)
+    launches_per_step = (8 + (args.mode == "accurate") + (not fused)) * (panels if world > 1 else 1)
 
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if args.m_total else "weak", "vs_baseline": None,
+        # the paper's protocol is the median over timed runs: per-step CUDA events
+        "median": {"ms_per_step": round(median_ms, 3),
+                   "value": round(total_flops / (median_ms * 1e-3) / 1e12, 3)},
         "dtype": "f64", "data": "synthetic (paper generator (rand-0.5)*exp(randn*phi), seeded, on device)",
-        "config": {"workload": (f"{'config3' if args.size == 16384 else 'custom'}: m=n=k={args.size} per GPU, "
+        "config": {"workload": (f"config5: m=n=k={args.size}, {args.m_total} rows split over {world} GPU(s)"
+                                f", phi={args.phi}, N={N}, {args.scheme} scheme, {args.mode} mode"
+                                if args.m_total else
+                                f"{'config3' if args.size == 16384 else 'custom'}: m=n=k={args.size} per GPU, "
                                f"phi={args.phi}, N={N} {dict(fp8='hybrid', int8='INT8', karatsuba='Karatsuba-only')[args.scheme]} moduli, "
                                f"{args.scheme} scheme, {args.mode} mode"),
                    "mode": args.mode, "scheme": args.scheme,
                    "m_per_gpu": m, "n": n, "k": k, "num_moduli": N, "phi": args.phi,
                    "l2": (f"no flush: A, B, C are {8 * m * k / 2**30:.2f}, {8 * k * n / 2**30:.2f}, "
                           f"{8 * m * n / 2**30:.2f} GiB (L2 is 126 MB)"),
-                   "parallelism": (f"row-sharded A/C over {world} GPU(s), B broadcast ({dist.get_backend()})"
-                                   if world > 1 else "single GPU")},
+                   "parallelism": (f"row-sharded A/C over {world} GPU(s), B broadcast in {panels} column "
+                                   f"panels overlapped with the per-panel calls ({dist.get_backend()})"
+                                   if world > 1 else "single GPU"),
+                   "tuning": {kn: P.oz2_get_tuning(kn) for kn in P.TUNE}},
         "gpu_launches": launches_per_step * args.steps,
         "phases_ms": {k_: round(v, 3) for k_, v in phases.items()},
         "hbm_phases": hbm_phases,
@@ -372,6 +488,12 @@ def run_oz2(args, rank, world, local_rank):
         return out, None
 
     extras = {}
+    # ---- the vendor FP8 ceiling on this box, under the same power cap
+    vend = vendor_fp8_ceiling(torch, local_rank)
+    extras["vendor_fp8"] = vend
+    if vend.get("sustained_tflops_digits"):
+        out["roofline"]["frac_vs_vendor_fp8_sustained"] = round(out["roofline"]["achieved"]
+                                                                 / vend["sustained_tflops_digits"], 4)
     # ---- cuBLAS DGEMM on the same inputs
     ref = torch.empty_like(C)
     for _ in range(2):
@@ -388,14 +510,14 @@ def run_oz2(args, rank, world, local_rank):
     extras["cublas"] = {"tflops": round(flops_rank / (cub_ms * 1e-3) / 1e12, 3), "ms": round(cub_ms, 3),
                         "speedup_oz2_vs_cublas": round(value / world / (flops_rank / (cub_ms * 1e-3) / 1e12), 3)}
 
-    # ---- accuracy against the exact product on sampled entries, and the N sweep
+    # ---- accuracy against the exact product on sampled entries (64 x 64 = 4096),
+    # and the N sweep
     rng = np.random.default_rng(0)
-    ns = 32
-    I = rng.choice(m, ns, replace=False)
-    J = rng.choice(n, ns, replace=False)
-    Ah = A[I, :].cpu().numpy()
-    Bh = B[:, J].cpu().numpy()
-    exact = np.array([[two_prod_exact_dot(Ah[a], Bh[:, b]) for b in range(len(J))] for a in range(len(I))])
+    ns = 64
+    I = np.sort(rng.choice(m, ns, replace=False))
+    J = np.sort(rng.choice(n, ns, replace=False))
+    It, Jt = torch.from_numpy(I).cuda(), torch.from_numpy(J).cuda()
+    exact = exact_block(A[It].cpu().numpy(), B[:, Jt].cpu().numpy())
 
     def errs(Cs):
         d = Cs - exact
@@ -404,9 +526,9 @@ def run_oz2(args, rank, world, local_rank):
 
     P.oz2_dgemm("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0, C.data_ptr(), m, N)
     torch.cuda.synchronize()
-    acc = {"sample": f"{ns} x {ns} entries, exact dot products (TwoProduct + fsum)",
-           f"oz2_N{N}": errs(C[I][:, J].cpu().numpy()),
-           "cublas": errs(ref[I][:, J].cpu().numpy())}
+    acc = {"sample": f"{ns} x {ns} entries, exact dot products (TwoProduct + fsum), phi={args.phi}",
+           f"oz2_N{N}": errs(C[It][:, Jt].cpu().numpy()),
+           "cublas": errs(ref[It][:, Jt].cpu().numpy())}
     sweep = {}
     for NN in [12, 13, 14, 16]:
         ws2 = P.oz2_workspace_size("N", "N", m, n, k, NN)
@@ -421,7 +543,7 @@ def run_oz2(args, rank, world, local_rank):
         e1.record()
         torch.cuda.synchronize()
         msN = e0.elapsed_time(e1) / 3
-        sweep[str(NN)] = {"tflops": round(flops_rank / (msN * 1e-3) / 1e12, 3), **errs(C[I][:, J].cpu().numpy())}
+        sweep[str(NN)] = {"tflops": round(flops_rank / (msN * 1e-3) / 1e12, 3), **errs(C[It][:, Jt].cpu().numpy())}
     acc["moduli_sweep"] = sweep
     if args.scheme == "fp8" and args.mode == "accurate" and args.size == 16384 and "12" in sweep:
         # the paper's own B200 figure is for accurate mode with N = 12;
@@ -446,7 +568,7 @@ def run_oz2(args, rank, world, local_rank):
         e1.record()
         torch.cuda.synchronize()
         msN = e0.elapsed_time(e1) / 3
-        osweep[str(NN)] = {"tflops": round(flops_rank / (msN * 1e-3) / 1e12, 3), **errs(C[I][:, J].cpu().numpy())}
+        osweep[str(NN)] = {"tflops": round(flops_rank / (msN * 1e-3) / 1e12, 3), **errs(C[It][:, Jt].cpu().numpy())}
     P.oz2_set_mode(args.mode)
     acc[f"{other}_mode_sweep"] = osweep
     # the other scheme (INT8 Ozaki-II baseline of P:151-202, or FP8), accurate mode
@@ -465,57 +587,136 @@ def run_oz2(args, rank, world, local_rank):
         e1.record()
         torch.cuda.synchronize()
         msN = e0.elapsed_time(e1) / 3
-        ssweep[str(NN)] = {"tflops": round(flops_rank / (msN * 1e-3) / 1e12, 3), **errs(C[I][:, J].cpu().numpy())}
+        ssweep[str(NN)] = {"tflops": round(flops_rank / (msN * 1e-3) / 1e12, 3), **errs(C[It][:, Jt].cpu().numpy())}
     P.oz2_set_scheme(args.scheme)
     acc[f"{oscheme}_scheme_sweep"] = ssweep
+    # phi sweep (BASELINE config 3: phi = 0.5, 1, 2, 4): oz2 at N = 12, 13, 14 and cuBLAS
+    # DGEMM, each against the exact product on 64 x 64 sampled entries
+    if args.scheme == "fp8" and args.mode == "accurate":
+        from synth import gen_device as _gd
+        psweep = {}
+        for ph_ in [0.5, 1.0, 2.0, 4.0]:
+            A.copy_(_gd(m, k, "phi", phi=ph_, seed=2000, device="cuda"))
+            B.copy_(_gd(k, n, "phi", phi=ph_, seed=2001, device="cuda"))
+            ex_ = exact_block(A[It].cpu().numpy(), B[:, Jt].cpu().numpy())
+            row = {}
+            torch.matmul(A, B, out=ref)
+            torch.cuda.synchronize()
+            d = ref[It][:, Jt].cpu().numpy() - ex_
+            row["cublas"] = {"normwise": float(np.linalg.norm(d) / np.linalg.norm(ex_)),
+                             "max_rel": float(np.max(np.abs(d) / np.abs(ex_)))}
+            for NN in [12, 13, 14]:
+                if P.oz2_workspace_size("N", "N", m, n, k, NN) > ws.numel():
+                    continue
+                assert P.oz2_dgemm("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0,
+                                   C.data_ptr(), m, NN) == 0
+                torch.cuda.synchronize()
+                d = C[It][:, Jt].cpu().numpy() - ex_
+                row[f"oz2_N{NN}"] = {"normwise": float(np.linalg.norm(d) / np.linalg.norm(ex_)),
+                                     "max_rel": float(np.max(np.abs(d) / np.abs(ex_)))}
+            psweep[str(ph_)] = row
+        acc["phi_sweep"] = psweep
     extras["accuracy"] = acc
 
     return out, extras
 
 
-def cpu_baseline(args, sample_rows=16, seed_off=0):
-    """The oracle as it stands, on a bounded sub-block of the same workload: the full
-    pipeline on an (s x k) x (k x s) block of the m=n=k problem (per-block scaling,
-    i.e. the paper's blocked call)."""
+def exact_block(Ah, Bh):
+    """RN64 of the exact dot products Ah[a] . Bh[:, b] for every (a, b): TwoProduct split of
+    each product (exact), then fsum (correctly rounded sum); accuracy probe only."""
     import numpy as np
+    c = 134217729.0
+    BT = np.ascontiguousarray(Bh.T)
+    bh = c * BT
+    bh = bh - (bh - BT)
+    bl = BT - bh
+    out = np.zeros((Ah.shape[0], BT.shape[0]))
+    for a in range(Ah.shape[0]):
+        x = Ah[a][None, :]
+        p = x * BT
+        ah = c * x
+        ah = ah - (ah - x)
+        al = x - ah
+        e = ((ah * bh - p) + ah * bl + al * bh) + al * bl
+        for b in range(BT.shape[0]):
+            out[a, b] = math.fsum(np.concatenate([p[b], e[b]]).tolist())
+    return out
+
+
+def _oracle_block(job):
+    """One sub-block of the workload through the full oracle pipeline on one core (worker
+    of cpu_baseline / the reference arm); returns its wall time."""
+    size, phi, moduli, sch, mode, s, seed = job
     from threadpoolctl import threadpool_limits
     from oracle import int8, scheme
     from synth import gen_host
-    s = sample_rows
-    k = args.size
-    A = gen_host(s, k, "phi", phi=args.phi, seed=50 + seed_off)
-    B = gen_host(k, s, "phi", phi=args.phi, seed=60 + seed_off)
+    A = gen_host(s, size, "phi", phi=phi, seed=50 + seed)
+    B = gen_host(size, s, "phi", phi=phi, seed=60 + seed)
     with threadpool_limits(limits=1):
         t0 = time.perf_counter()
-        if args.scheme == "int8":
-            int8.dgemm(A, B, args.moduli, mode=args.mode)
+        if sch == "int8":
+            int8.dgemm(A, B, moduli, mode=mode)
         else:
-            scheme.dgemm(A, B, args.moduli, mode=args.mode)
-        dt = time.perf_counter() - t0
-    return {"value": 2.0 * s * s * k / dt / 1e12, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{s} x {k} x {s} sub-block, N={args.moduli} (full oracle pipeline, exact ints/Fractions)",
+            scheme.dgemm(A, B, moduli, mode=mode, family="karatsuba" if sch == "karatsuba" else "hybrid")
+        return time.perf_counter() - t0
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(args, sample_rows=16, seed_off=0, cores=1, pool=None):
+    """The oracle as it stands, on bounded sub-blocks of the same workload: the full
+    pipeline on (s x k) x (k x s) blocks of the m=n=k problem (per-block scaling, i.e. the
+    paper's blocked call), one block per core, all cores at once.  value = the
+    blocks' FP64 flops / wall time."""
+    s, k = sample_rows, args.size
+    jobs = [(k, args.phi, args.moduli, args.scheme, args.mode, s, seed_off + c) for c in range(cores)]
+    t0 = time.perf_counter()
+    if cores == 1:
+        _oracle_block(jobs[0])
+    else:
+        list(pool.map(_oracle_block, jobs))
+    dt = time.perf_counter() - t0
+    return {"value": 2.0 * s * s * k * cores / dt / 1e12, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": (f"{cores} x ({s} x {k} x {s}) sub-blocks, one per core in parallel processes, "
+                       f"N={args.moduli} (full oracle pipeline, exact ints/Fractions)"),
             "seconds": round(dt, 3)}
+
+
+def oracle_pool(cores):
+    import concurrent.futures
+    import multiprocessing
+    return concurrent.futures.ProcessPoolExecutor(max_workers=cores,
+                                                  mp_context=multiprocessing.get_context("spawn"))
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    for w in range(args.warmup):
-        cpu_baseline(args, sample_rows=2, seed_off=w)
-    vals = []
-    t0 = time.perf_counter()
-    for s_ in range(args.steps):
-        vals.append(cpu_baseline(args, sample_rows=2, seed_off=100 + s_))
-    total = time.perf_counter() - t0
-    flops = sum(2.0 * 2 * 2 * args.size for _ in vals)
+    cores = min(host_cores(), 256)
+    s = 2
+    with oracle_pool(cores) as pool:
+        list(pool.map(_oracle_block, [(64, args.phi, args.moduli, args.scheme, args.mode, 1, c)
+                                      for c in range(cores)]))      # start the workers
+        for w in range(args.warmup):
+            cpu_baseline(args, sample_rows=s, seed_off=1000 * w, cores=cores, pool=pool)
+        t0 = time.perf_counter()
+        for st in range(args.steps):
+            cpu_baseline(args, sample_rows=s, seed_off=1000 * (100 + st), cores=cores, pool=pool)
+        total = time.perf_counter() - t0
+    flops = 2.0 * s * s * args.size * cores * args.steps
     value = flops / total / 1e12
+    sample = f"{cores} x ({s} x {args.size} x {s}) sub-blocks per step, one per core (full oracle pipeline)"
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": f"config3 sub-blocks: 2 x {args.size} x 2 per step, N={args.moduli}, phi={args.phi}"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"2 x {args.size} x 2 sub-block per step (full oracle pipeline)"},
+            "config": {"workload": f"config3 sub-blocks: {sample}, N={args.moduli}, phi={args.phi}"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -546,7 +747,14 @@ def main():
         if extras:
             out.update(extras)
         if world == 1 and not args.no_extras:
-            out["cpu_baseline"] = cpu_baseline(args)
+            cores = min(host_cores(), 256)
+            one = cpu_baseline(args)
+            with oracle_pool(cores) as pool:
+                list(pool.map(_oracle_block, [(64, args.phi, args.moduli, args.scheme, args.mode, 1, c)
+                                              for c in range(cores)]))   # start the workers
+                allc = cpu_baseline(args, seed_off=10, cores=cores, pool=pool)
+            out["cpu_baseline"] = allc
+            out["cpu_baseline_1core"] = one
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()

@@ -152,7 +152,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     // INT8 variants run the same pipeline on kind::i8 (S32 accumulators)
     constexpr bool I8 = MODE_ >= MODE_RESIDUE_I8;
     constexpr int MODE = I8 ? MODE_ - 3 : MODE_;
-    constexpr int NP = I8 ? 1 : 3;                    // products per modulus
+    // k-block passes per modulus: 3 (FP8: three products, or a K-concatenated pair + one)
+    // or 1 (INT8); the number of accumulator drains is P.mod[l].nprod
+    constexpr int NP = I8 ? 1 : 3;
     using Cfg = GemmCfg<CG>;
     constexpr int NS = Cfg::NSTAGE;
     extern __shared__ uint8_t smem_raw[];
@@ -226,7 +228,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     auto item_tile = [&](int it) { return it < head ? it : head + (it - head) % tail; };
     auto item_l0 = [&](int it) { return it < head ? 0 : (it - head) / tail; };
     auto item_nmods = [&](int it) { return it < head ? NMOD : 1; };
-    auto item_prods = [&](int it) { return (MODE == MODE_RESIDUE) ? NP * item_nmods(it) * nseg : 1; };
+    // products of modulus l (accumulator drains, each in nseg K segments)
+    auto nprod_of = [&](int l) { return (MODE == MODE_RESIDUE) ? P.mod[l].nprod : 1; };
+    auto nparts_of = [&](int l, int x) { return (MODE == MODE_RESIDUE && x == 0 && P.mod[l].a_plane2 >= 0) ? 2 : 1; };
     const int unit = blockIdx.x / CS;            // tile-processing unit (cluster)
     const int units = gridDim.x / CS;
 
@@ -245,20 +249,21 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             for (int it = unit; it < num_items; it += units) {
                 const int tile = item_tile(it);
                 const int l0 = item_l0(it);
-                const int prods = item_prods(it);
+                const int l1 = (MODE == MODE_RESIDUE) ? l0 + item_nmods(it) : l0 + 1;
                 int tm, tn;
                 tile_coords<16 / CG>(tile, P.m_tiles, n_super, tm, tn);
                 tn = tn * MC + static_cast<int>(pairi);
-                for (int pr = 0; pr < prods; ++pr) {
-                    int a_row = tm * Cfg::TILE_M + static_cast<int>(rank) * BM + (MC == 2 ? static_cast<int>(pairi) * (BM / 2) : 0);
-                    int b_row = tn * BN + static_cast<int>(rank) * Cfg::B_ROWS;
+                const int a_row0 = tm * Cfg::TILE_M + static_cast<int>(rank) * BM + (MC == 2 ? static_cast<int>(pairi) * (BM / 2) : 0);
+                const int b_row0 = tn * BN + static_cast<int>(rank) * Cfg::B_ROWS;
+                for (int l = l0; l < l1; ++l)
+                for (int x = 0; x < nprod_of(l); ++x)
+                for (int seg = 0; seg < nseg; ++seg)
+                for (int part = 0; part < nparts_of(l, x); ++part) {
+                    int a_row = a_row0, b_row = b_row0;
                     int kb0 = 0, kb1 = nkb;
                     if (MODE == MODE_RESIDUE) {
-                        const int lr = pr / (NP * nseg), rem = pr - lr * NP * nseg;
-                        const int l = l0 + lr;
-                        const int x = rem / nseg, seg = rem - x * nseg;
-                        a_row += P.mod[l].a_plane[x] * P.rows_per_plane_a;
-                        b_row += P.mod[l].b_plane[x] * P.rows_per_plane_b;
+                        a_row += (part ? P.mod[l].a_plane2 : P.mod[l].a_plane[x]) * P.rows_per_plane_a;
+                        b_row += (part ? P.mod[l].b_plane2 : P.mod[l].b_plane[x]) * P.rows_per_plane_b;
                         kb0 = seg * kseg;
                         kb1 = min(nkb, kb0 + kseg);
                     }
@@ -323,14 +328,18 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                                           : make_idesc_e4m3_f32(Cfg::TILE_M, BN);
             uint32_t stage = 0, phase = 0, g = 0;
             for (int it = unit; it < num_items; it += units) {
-                const int prods = item_prods(it);
-                for (int pr = 0; pr < prods; ++pr, ++g) {
+                const int l0 = item_l0(it);
+                const int l1 = (MODE == MODE_RESIDUE) ? l0 + item_nmods(it) : l0 + 1;
+                for (int l = l0; l < l1; ++l)
+                for (int x = 0; x < nprod_of(l); ++x)
+                for (int seg = 0; seg < nseg; ++seg, ++g) {
                     const uint32_t slot = g & 1u, use = g >> 1;
                     mbar_wait(&tempty[slot], (use & 1u) ^ 1u);
                     tc_fence_after();
                     const uint32_t d_tmem = tmem_base + slot * BN;
-                    const int seg = (MODE == MODE_RESIDUE) ? pr % nseg : 0;
                     const int kb0 = seg * kseg, kb1 = min(nkb, kb0 + kseg);
+                    const int nparts = nparts_of(l, x);
+                    for (int part = 0; part < nparts; ++part)
                     for (int kb = kb0; kb < kb1; ++kb) {
                         mbar_wait(&full[stage], phase);
                         tc_fence_after();
@@ -339,7 +348,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 #pragma unroll
                         for (int kk = 0; kk < BK / 32; ++kk) {
                             // advance 32 bytes of K inside the 128-byte swizzle atom
-                            const uint32_t acc = (kb > kb0 || kk > 0) ? 1u : 0u;
+                            const uint32_t acc = (part > 0 || kb > kb0 || kk > 0) ? 1u : 0u;
                             if (I8) {
                                 if (CG == 1) mma_i8(d_tmem, a0 + 2 * kk, b0 + 2 * kk, idesc, acc);
                                 else mma_i8_cg2(d_tmem, a0 + 2 * kk, b0 + 2 * kk, idesc, acc);
@@ -378,7 +387,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         // of an element were written by this same thread (program order).
         int64_t crt_row = -1, crt_col0 = 0;
         int crt_j = 128;
-        const int crt_per_prod = (MODE == MODE_RESIDUE) ? (128 + NP * P.num_moduli - 1) / (NP * P.num_moduli) + 1 : 0;
+        const int crt_per_prod = (MODE == MODE_RESIDUE) ? (128 + P.prods_per_tile * nseg - 1) / (P.prods_per_tile * nseg) + 1 : 0;
         auto crt_steps = [&](int ncols) {
             if (FL == 0 || crt_j >= 128) return;
             if (crt_row >= P.m) { crt_j = 128; return; }
@@ -414,12 +423,12 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     // (|.| <= p/2 + 1 <= 546), held exactly in binary16 pairs
                     __half2 part[64];
                     int16_t* out = P.residues + (static_cast<int64_t>(l) * P.n + col0) * P.m + row;
-#pragma unroll
-                    for (int x = 0; x < NP; ++x) {
+                    const int npl = nprod_of(l);
+                    for (int x = 0; x < npl; ++x) {
                       const float coef = P.mod[l].coef[x];
                       for (int seg = 0; seg < nseg; ++seg, ++g) {
                         const bool first = (x == 0) && (seg == 0);
-                        const bool last = (x == NP - 1) && (seg == nseg - 1);
+                        const bool last = (x == npl - 1) && (seg == nseg - 1);
                         const uint32_t slot = g & 1u, use = g >> 1;
                         mbar_wait(&tfull[slot], use & 1u);
                         tc_fence_after();

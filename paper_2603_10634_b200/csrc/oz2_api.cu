@@ -124,7 +124,8 @@ struct Plan {
     FastExpParams fast{};             // H = RD64((P-1)/2) for fast mode (R15)
     CrtParams crt{};
     DigitParams dig{};
-    GemmParams gemm_mod{};            // only .mod[] filled
+    GemmParams gemm_mod{};            // only .mod[] filled: 3 products per FP8 modulus
+    GemmParams gemm_mod_kcat{};       // square moduli with the K-concatenated cross product
     std::vector<uint16_t> pow2tab;    // [N][kPow2Tab]
     uint16_t* d_pow2tab = nullptr;    // device copy (per thread)
     Big P;
@@ -261,9 +262,12 @@ static Plan build_plan(int N, int family, int sq_order) {
             if (w >= (p + 1) / 2) w -= p;
             me.w16 = static_cast<float>(w);
         }
+        me.nprod = 3;
+        me.a_plane2 = me.b_plane2 = -1;
         if (i8) {
             // one exact INT8 GEMM per modulus: C'_l = mod(A'_l B'_l, p_l) (eq. CRTmatmul)
             me.coef[0] = 1.0f; me.a_plane[0] = plane; me.b_plane[0] = plane;
+            me.nprod = 1;
             plane += 1;
         } else if (md.square) {
             // C'_l = mod(s A1 B2 + s A2 B1 + A2 B2, p)  (eq. 3matmult-notKaratsuba)
@@ -279,6 +283,17 @@ static Plan build_plan(int N, int family, int sq_order) {
                 me.coef[1] = static_cast<float>(s); me.a_plane[1] = plane + 1; me.b_plane[1] = plane + 0;
                 me.coef[2] = 1.0f;                  me.a_plane[2] = plane + 1; me.b_plane[2] = plane + 1;
             }
+            {   // K-concatenated: s (A1 B2 + A2 B1) in ONE accumulator (|sum| <= 2 k 2^8 <=
+                // 2^24 for k <= 2^15, exact), then A2 B2 -- 2 drains instead of 3 (the M_N
+                // product buffers of P:609, 2 per square modulus)
+                ModEpi& mk = pl.gemm_mod_kcat.mod[l];
+                mk = me;
+                mk.nprod = 2;
+                mk.coef[0] = static_cast<float>(s); mk.a_plane[0] = plane + 0; mk.b_plane[0] = plane + 1;
+                mk.a_plane2 = plane + 1; mk.b_plane2 = plane + 0;
+                mk.coef[1] = 1.0f;                  mk.a_plane[1] = plane + 1; mk.b_plane[1] = plane + 1;
+                mk.coef[2] = 0.0f;                  mk.a_plane[2] = mk.b_plane[2] = -1;
+            }
             plane += 2;
         } else {
             // A'B' = 256 C1 + C2 + 16 (C3 - C1 - C2)  (eq. C'-Karatsuba)
@@ -287,6 +302,7 @@ static Plan build_plan(int N, int family, int sq_order) {
             me.coef[2] = 16.0f;  me.a_plane[2] = plane + 2; me.b_plane[2] = plane + 2;
             plane += 3;
         }
+        if (!md.square || i8) pl.gemm_mod_kcat.mod[l] = me;
     }
     pl.pow2tab.resize(static_cast<size_t>(N) * kPow2Tab);
     for (int l = 0; l < N; ++l) {
@@ -759,7 +775,12 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             CUtensorMap ta, tb;
             if (!make_map(&ta, digA, L.k_pad, static_cast<uint64_t>(pl->M) * mbi_pad, L.k_pad, BK, a_box_rows(cg))) return OZ2_ERR_CUDA;
             if (!make_map(&tb, digB, L.k_pad, static_cast<uint64_t>(pl->M) * nbj_pad, L.k_pad, BK, b_box_rows(cg))) return OZ2_ERR_CUDA;
-            GemmParams gp = pl->gemm_mod;
+            // square moduli: A1 B2 + A2 B1 K-concatenated in one accumulator when the sum
+            // stays in the FP32 exactness window (k <= 2^15; OZ2_TUNE_KCAT)
+            const bool kcat = tune(OZ2_TUNE_KCAT) != 0 && !i8 && pl->nsq > 0 && k <= kMaxK / 2;
+            GemmParams gp = kcat ? pl->gemm_mod_kcat : pl->gemm_mod;
+            gp.prods_per_tile = 0;
+            for (int l = 0; l < N; ++l) gp.prods_per_tile += gp.mod[l].nprod;
             gp.m = static_cast<int>(mbi); gp.n = static_cast<int>(nbj);
             gp.num_k_blocks = static_cast<int>(L.k_pad / BK);
             gp.kseg_blocks = kMaxK / BK;                                  // 2^16 per segment

@@ -58,6 +58,10 @@ struct ModEpi {          // per modulus, residue-GEMM epilogue (P:292-299, P:241
     float coef[3];       // square: (s, s, 1); non-square: (240, -15, 16); INT8: (1)
     int a_plane[3];      // digit-plane index of the A operand of product x
     int b_plane[3];
+    int nprod;           // products (accumulator drains) of this modulus: 3, 1 (INT8) or 2
+                         // (square, K-concatenated cross products)
+    int a_plane2;        // >= 0: product 0 has a second part a_plane2 x b_plane2 accumulated
+    int b_plane2;        // into the same TMEM accumulator (A1 B2 + A2 B1, k <= 2^15)
 };
 
 struct GemmParams {
@@ -86,6 +90,7 @@ struct GemmParams {
     unsigned long long hint_a, hint_b;   // L2 cache policies of the operand TMA loads
     int sync_lead;               // 0 = off; else max chunks ahead of the chip-wide average
     int sync_chunk;              // k-blocks per throttle chunk (0 = one chunk per product)
+    int prods_per_tile;          // residue mode: sum of mod[l].nprod (accumulator drains per tile)
     int max_units;               // host only: cap on persistent units (0 = all)
     ModEpi mod[kMaxModuli];
 };

@@ -1,13 +1,15 @@
-"""World-size-2 gloo test of the row-sharded driver on CPU: the partition, the broadcast
-of B, and per-shard results equal to the oracle on the same sub-problem (the per-shard
-compute is injected; on GPUs it is oz2_dgemm over NCCL)."""
+"""World-size-2 gloo tests of the row-sharded driver on CPU: the partition, the broadcast
+of B (whole, or in column panels overlapped with the per-panel calls), and per-shard /
+per-panel results equal to the oracle on the same sub-problem (the per-block compute is
+injected here; on GPUs it is oz2_dgemm over NCCL -- tests/test_dist_gpu.py runs the CUDA
+path under a 2-rank process group on one device)."""
 import os
 import socket
 
 import numpy as np
 import pytest
 
-from paper_2603_10634_b200.dist import row_block
+from paper_2603_10634_b200.dist import col_panels, row_block
 
 
 def test_row_block_partition():
@@ -21,6 +23,17 @@ def test_row_block_partition():
             assert max(sizes) - min(sizes) <= 1
 
 
+def test_col_panels():
+    assert col_panels(1000, 1) == [(0, 1000)]
+    assert col_panels(200, 4) == [(0, 200)]
+    for n in [257, 1000, 4096, 32768, 5000]:
+        for p in [2, 3, 4, 8]:
+            pans = col_panels(n, p)
+            assert pans[0][0] == 0 and pans[-1][1] == n and len(pans) <= p
+            assert all(b == c for (_, b), (c, _) in zip(pans, pans[1:]))
+            assert all((b - a) % 256 == 0 for a, b in pans[:-1])
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -29,7 +42,10 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out_q):
+M, K, NCOL, NMOD = 24, 40, 600, 12
+
+
+def _worker(rank, world, port, panels, out_q):
     import torch
     import torch.distributed as dist
     from oracle import scheme
@@ -39,25 +55,29 @@ def _worker(rank, world, port, out_q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    m, k, n, N = 24, 40, 10, 12
-    A = gen_host(m, k, "phi", phi=1.0, seed=3, order="C")
-    r0, r1 = row_block(m, rank, world)
+    A = gen_host(M, K, "phi", phi=1.0, seed=3, order="C")
+    r0, r1 = row_block(M, rank, world)
     A_local = torch.from_numpy(A[r0:r1].copy())
+    # column-major B (the layout the panelled broadcast needs)
     if rank == 0:
-        B = torch.from_numpy(gen_host(k, n, "phi", phi=1.0, seed=4, order="C"))
+        B = torch.from_numpy(np.ascontiguousarray(gen_host(K, NCOL, "phi", phi=1.0, seed=4).T)).t()
     else:
-        B = torch.zeros((k, n), dtype=torch.float64)     # filled by the broadcast
+        B = torch.zeros((NCOL, K), dtype=torch.float64).t()     # filled by the broadcast
+    calls = []
 
     def oracle_gemm(A_, B_, alpha, beta, C, num_moduli):
-        return torch.from_numpy(scheme.dgemm(A_.numpy(), B_.numpy(), num_moduli).C)
+        calls.append(B_.shape[1])
+        C.copy_(torch.from_numpy(scheme.dgemm(A_.numpy(), B_.numpy(), num_moduli).C))
+        return C
 
-    C_local = dgemm_rowsharded(A_local, B, num_moduli=N, gemm_fn=oracle_gemm)
-    out_q.put((rank, r0, r1, C_local.numpy(), B.numpy()))
+    C_local = dgemm_rowsharded(A_local, B, num_moduli=NMOD, gemm_fn=oracle_gemm, panels=panels)
+    out_q.put((rank, r0, r1, C_local.numpy().copy(), B.numpy().copy(), calls))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_rowsharded_gloo_world2():
+@pytest.mark.parametrize("panels", [1, 3])
+def test_rowsharded_gloo_world2(panels):
     import torch.multiprocessing as mp
     from oracle import scheme
     from synth import gen_host
@@ -66,23 +86,23 @@ def test_rowsharded_gloo_world2():
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, panels, q)) for r in range(world)]
     for p in procs:
         p.start()
-    results = [q.get(timeout=300) for _ in range(world)]
+    results = [q.get(timeout=600) for _ in range(world)]
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    A = gen_host(24, 40, "phi", phi=1.0, seed=3, order="C")
-    B = gen_host(40, 10, "phi", phi=1.0, seed=4, order="C")
-    full = scheme.dgemm(A, B, 12).C
+    A = gen_host(M, K, "phi", phi=1.0, seed=3, order="C")
+    B = gen_host(K, NCOL, "phi", phi=1.0, seed=4)
     exact = A @ B
-    for rank, r0, r1, C_local, Bseen in results:
+    pans = col_panels(NCOL, panels)
+    for rank, r0, r1, C_local, Bseen, calls in results:
         assert np.array_equal(Bseen, B)                       # broadcast delivered B
-        want = scheme.dgemm(A[r0:r1], B, 12).C                # per-shard oracle
-        assert np.array_equal(C_local, want)
-        # same accuracy class as the unsharded call (block-local nu, R13)
+        assert calls == [b - a for a, b in pans]              # one call per panel
+        for j0, j1 in pans:                                   # per-block oracle (R13, Q20)
+            want = scheme.dgemm(A[r0:r1], B[:, j0:j1], NMOD).C
+            assert np.array_equal(C_local[:, j0:j1], want)
         rel = np.linalg.norm(C_local - exact[r0:r1]) / np.linalg.norm(exact[r0:r1])
         assert rel < 1e-14
     assert sorted(r[0] for r in results) == [0, 1]
-    assert np.allclose(np.vstack([r[3] for r in sorted(results)]), full, rtol=1e-13, atol=0)

@@ -739,3 +739,50 @@ def test_extreme_exponent_ranges(dev, ea, eb):
     mask = _compare(res, ref, A, B, 13)
     assert mask.all()
     assert np.all(np.isfinite(res["C"]))
+
+
+@pytest.mark.parametrize("k", [32768, 32763, 1000])
+def test_kcat_cross_products_exactness_edge(dev, k, knobs):
+    """K-concatenated square-modulus cross products (OZ2_TUNE_KCAT): A1 B2 + A2 B1
+    accumulate in ONE FP32 accumulator.  Integer inputs 544 = 16 * 33 + 16 give the digits
+    D1 = D2 = 16 for p = 1089, so at k = 2^15 the concatenated sum is exactly 2 k 2^8 =
+    2^24, the edge of the exactness window (eq. error-free-FP8-matmult).  Residues and C
+    equal the oracle's (imported exponents 0) with the concatenation on and off."""
+    from gpu_helpers import run
+    m, n, N = 40, 48, 13
+    rng = np.random.default_rng(k)
+    A = np.full((m, k), 544.0)
+    B = np.full((k, n), 544.0)
+    A[1::2] *= -1.0
+    B[:, ::3] *= -1.0
+    A[5:9] = rng.integers(-2 ** 20, 2 ** 20, size=(4, k))        # generic rows too
+    B[:, 7:11] = rng.integers(-2 ** 20, 2 ** 20, size=(k, 4))
+    e0 = [0] * m
+    f0 = [0] * n
+    I, J = list(range(m)), list(range(n))
+    res_ref, C_ref = scheme.entries(A, B, N, I, J, e0, f0)
+    outs = []
+    for kc in (1, 0):
+        knobs(kcat=kc)
+        out = run(A, B, N, e_mu_in=e0, e_nu_in=f0)
+        assert np.array_equal(np.array(out["residues"]), res_ref)
+        assert np.array_equal(out["C"], C_ref)
+        outs.append(out)
+    assert np.array_equal(outs[0]["C"], outs[1]["C"])
+
+
+@pytest.mark.parametrize("sch", ["fp8", "karatsuba"])
+def test_kcat_on_off_identical_many_tiles(dev, sch, knobs):
+    """The concatenated and the three-product forms give identical residues and C on a
+    multi-tile problem through the full pipeline (k = 8192, both work-item schedules)."""
+    from gpu_helpers import run
+    m, k, n, N = 700, 8192, 600, 13
+    A = gen_host(m, k, "phi", phi=1.0, seed=71)
+    B = gen_host(k, n, "phi", phi=1.0, seed=72)
+    outs = []
+    for kc, split in [(1, 0), (0, 0), (1, 1)]:
+        knobs(kcat=kc, mod_split=split)
+        outs.append(run(A, B, N, scheme=sch))
+    for o in outs[1:]:
+        assert np.array_equal(o["residues"], outs[0]["residues"])
+        assert np.array_equal(o["C"], outs[0]["C"])
