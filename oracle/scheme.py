@@ -146,8 +146,13 @@ def scaling_offset(Rmax: Fraction, k: int, Pp: Fraction, dlt: Fraction):
     int() is floor (reading R8).  Returns None when Rmax == 0 (no bound needed)."""
     if Rmax == 0:
         return None
-    cbar = fp32.round_up(safety_factor(k) * Rmax)
-    return offset_from_cbar(cbar, Pp, dlt)
+    return offset_from_cbar(cbar_of(Rmax, k), Pp, dlt)
+
+
+def cbar_of(Rmax: Fraction, k: int) -> Fraction:
+    """c-bar = f_k * max_j C-bar'_ij "in round-up mode" (eq. barCupper; f_k per
+    reading R5): the smallest binary32 value >= f_k Rmax."""
+    return fp32.round_up(safety_factor(k) * Rmax)
 
 
 def offset_from_cbar(cbar: Fraction, Pp: Fraction, dlt: Fraction) -> int:

@@ -205,3 +205,59 @@ def test_fast_exponents_within_one_of_norm_rule(phi, k):
         assert e_norm - 1 <= e_fast[i] <= e_norm, (i, e_fast[i], e_norm)
         below += e_fast[i] < e_norm
     assert below < A.shape[0]          # mostly equal: the loss is a fraction of a bit
+
+
+# ------------------------------------------------------------------ more hand pins (mutation sweep)
+
+def test_cbar_is_round_up_of_fk_R():
+    """c-bar = RU32(f_k R) ("in round-up mode"): c-bar >= f_k R and its binary32
+    predecessor is below, for R on and off the binary32 grid (R itself is an FP32 value)."""
+    rng = np.random.default_rng(11)
+    for k in (1000, 16384, 65536):
+        fk = scheme.safety_factor(k)
+        for v in np.exp2(rng.uniform(0.0, 34.0, 50)):
+            R = Fraction(float(np.float32(v)))
+            c = scheme.cbar_of(R, k)
+            assert c >= fk * R and _f32(_bits(c) - 1) < fk * R
+
+
+def test_square_digit_ties_are_round_half_even():
+    """Reading R9 ("round", ties to even).  Ties occur only for p = 1024 (s = 32) at
+    r = 16 (mod 32): r = 16 -> 16/32 = 0.5 -> D1 = 0, D2 = 16; r = 48 -> 1.5 -> D1 = 2,
+    D2 = -16; r = -16 -> -0.5 -> D1 = 0, D2 = -16; r = 80 -> 2.5 -> D1 = 2, D2 = 16;
+    r = -48 -> -1.5 -> D1 = -2, D2 = 16 (worked by hand)."""
+    want = {16: (0, 16), 48: (2, -16), -16: (0, -16), 80: (2, 16), -48: (-2, 16), 17: (1, -15)}
+    for r, d in want.items():
+        assert scheme.digits_square(r, 32) == d, r
+
+
+def test_mma_model_is_round_to_nearest_even():
+    """Reading R6: the bound GEMM's FP32 result is modelled as the exact sum rounded once to
+    nearest-even binary32.  In units of 2^-18, binary32 spacing is 4 in [2^25, 2^26) and 8
+    in [2^26, 2^27): 2^25 + 3 -> 2^25 + 4 (nearer; round-down would give 2^25); the ties
+    2^25 + 2 -> 2^25 (significand 2^23, even) and 2^25 + 6 -> 2^25 + 8 (2^23 + 2, even);
+    2^26 + 5 -> 2^26 + 8; 2^26 + 3 -> 2^26 (worked by hand)."""
+    u = Fraction(1, 2 ** 18)
+    want = {2 ** 25 + 3: 2 ** 25 + 4, 2 ** 25 + 2: 2 ** 25, 2 ** 25 + 6: 2 ** 25 + 8,
+            2 ** 26 + 5: 2 ** 26 + 8, 2 ** 26 + 3: 2 ** 26, 12345: 12345}
+    for x, y in want.items():
+        assert scheme.mma_fp32_model(x) == y * u, x
+
+
+def test_apriori_bound_is_nearly_attained():
+    """The closed-form bound sum_h (|b|/mu + |a|/nu + 1/(mu nu)) (from eq. def:A'/def:B',
+    P:157-161) is attained up to ~1 %: positive entries whose scaled values have
+    fractional part 1 - 2^-7 lose almost a whole unit to each truncation.  With fixed
+    exponents (mu = 2^30, nu = 2^31) the exact error |C'/(mu nu) - AB| must lie in
+    [0.98, 1] x bound: a bound off by a factor (or a dropped term) fails one side."""
+    from oracle import exact
+    k, N = 6, 12
+    d = Fraction(127, 128)
+    A = np.array([[float((Fraction(2 ** 45 + 17 * h) + d) / 2 ** 30) for h in range(k)]])
+    B = np.array([[float((Fraction(2 ** 44 + 29 * h) + d) / 2 ** 31)] for h in range(k)])
+    r = scheme.dgemm(A, B, N, e_mu=[30], e_nu=[31])
+    Cp = Fraction(int(r.extra["Cprime"][0, 0]), 2 ** 61)
+    ABx = sum(Fraction(float(A[0, h])) * Fraction(float(B[h, 0])) for h in range(k))
+    err = abs(Cp - ABx)
+    bnd = exact.apriori_bound(A, B, [30], [31])[0, 0]
+    assert 0.98 * bnd <= float(err) <= bnd * (1 + 2 ** -40)
