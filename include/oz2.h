@@ -243,8 +243,9 @@ int oz2_finalize(void);
  *   OZ2_TUNE_CRT_GENERIC 0    1 = the generic standalone CRT kernel (A/B reference)
  *   OZ2_TUNE_HOST_BLOCKS 4    host-pointer calls with pinned C: column blocks of C whose
  *                             device-to-host copies overlap the GEMMs (1 = off)
- *   OZ2_TUNE_KCAT        1    square moduli: accumulate A1B2 + A2B1 in one TMEM
- *                             accumulator (K-concatenated) when k <= 2^15
+ *   OZ2_TUNE_KCAT        0    square moduli: accumulate A1B2 + A2B1 in one TMEM
+ *                             accumulator (K-concatenated) when k <= 2^15 (two
+ *                             accumulator drains instead of three; measured slower)
  *
  * oz2_set_tuning returns -1 for an unknown knob, -2 for a value out of range;
  * oz2_get_tuning writes the current value. */

@@ -87,24 +87,26 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // 2-SM TMA: bytes land in this CTA's smem, completion is counted on the leader's barrier
-__device__ __forceinline__ void tma_load_2d_cg2(const CUtensorMap* m, uint32_t leader_bar, void* smem,
-                                                int32_t c0, int32_t c1, uint64_t cache_hint) {
+__device__ __forceinline__ void tma_load_4d_cg2(const CUtensorMap* m, uint32_t leader_bar, void* smem,
+                                                int32_t c0, int32_t c1, int32_t c2, int32_t c3,
+                                                uint64_t cache_hint) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%3, %4}], [%2], %5;"
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;"
         ::"r"(smem_u32(smem)), "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar),
-          "r"(c0), "r"(c1), "l"(cache_hint)
+          "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(cache_hint)
         : "memory");
 }
 // 2-SM TMA multicast: the box lands at the same smem offset in every CTA of `mask`, and
 // each destination pair's leader barrier (same offset) counts the bytes
-__device__ __forceinline__ void tma_load_2d_cg2_mc(const CUtensorMap* m, uint32_t leader_bar, void* smem,
-                                                   int32_t c0, int32_t c1, uint16_t mask, uint64_t cache_hint) {
+__device__ __forceinline__ void tma_load_4d_cg2_mc(const CUtensorMap* m, uint32_t leader_bar, void* smem,
+                                                   int32_t c0, int32_t c1, int32_t c2, int32_t c3,
+                                                   uint16_t mask, uint64_t cache_hint) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
-        " [%0], [%1, {%4, %5}], [%2], %3, %6;"
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+        " [%0], [%1, {%4, %5, %6, %7}], [%2], %3, %8;"
         ::"r"(smem_u32(smem)), "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar), "h"(mask),
-          "r"(c0), "r"(c1), "l"(cache_hint)
+          "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(cache_hint)
         : "memory");
 }
 __device__ __forceinline__ void mma_f8f6f4_cg2(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
@@ -200,8 +202,12 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         tmem_alloc_cg<CG>(tmem_slot, 512);
     }
     tc_fence_before();
+    // the cluster barrier orders the TMEM-address write of tcgen05.alloc (and the barrier
+    // inits) for the whole cluster; the CTA barrier after it changes nothing for the
+    // hardware but lets compute-sanitizer racecheck, which does not model barrier.cluster,
+    // see the ordering (profiles/round2_sanitizer.md)
     if (CS > 1) cluster_sync_all();
-    else __syncthreads();
+    __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -253,17 +259,18 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 int tm, tn;
                 tile_coords<16 / CG>(tile, P.m_tiles, n_super, tm, tn);
                 tn = tn * MC + static_cast<int>(pairi);
-                const int a_row0 = tm * Cfg::TILE_M + static_cast<int>(rank) * BM + (MC == 2 ? static_cast<int>(pairi) * (BM / 2) : 0);
-                const int b_row0 = tn * BN + static_cast<int>(rank) * Cfg::B_ROWS;
+                const int a_row = tm * Cfg::TILE_M + static_cast<int>(rank) * BM + (MC == 2 ? static_cast<int>(pairi) * (BM / 2) : 0);
+                const int b_row = tn * BN + static_cast<int>(rank) * Cfg::B_ROWS;
                 for (int l = l0; l < l1; ++l)
                 for (int x = 0; x < nprod_of(l); ++x)
                 for (int seg = 0; seg < nseg; ++seg)
                 for (int part = 0; part < nparts_of(l, x); ++part) {
-                    int a_row = a_row0, b_row = b_row0;
+                    // operand planes (interleaved layout: plane = the map's dimension 1)
+                    int a_pl = 0, b_pl = 0;
                     int kb0 = 0, kb1 = nkb;
                     if (MODE == MODE_RESIDUE) {
-                        a_row += (part ? P.mod[l].a_plane2 : P.mod[l].a_plane[x]) * P.rows_per_plane_a;
-                        b_row += (part ? P.mod[l].b_plane2 : P.mod[l].b_plane[x]) * P.rows_per_plane_b;
+                        a_pl = part ? P.mod[l].a_plane2 : P.mod[l].a_plane[x];
+                        b_pl = part ? P.mod[l].b_plane2 : P.mod[l].b_plane[x];
                         kb0 = seg * kseg;
                         kb1 = min(nkb, kb0 + kseg);
                     }
@@ -288,24 +295,28 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                             ++g;
                         }
                         mbar_wait(&empty[stage], phase ^ 1);
+                        // map coordinates {K byte, plane, K chunk, row}: interleaved digit
+                        // planes (plane, chunk kb) or a plain [rows][k] matrix (raw GEMM:
+                        // dimension 0 spans the row, plane and chunk are 0)
+                        const int c0 = P.plain_k ? kb * BK : 0, c2 = P.plain_k ? 0 : kb;
                         if (CG == 1) {
                             mbar_arrive_expect_tx(&full[stage], Cfg::A_STAGE + Cfg::B_STAGE);
-                            tma_load_2d(&tmA, &full[stage], sA + stage * Cfg::A_STAGE, kb * BK, a_row, hint_a);
-                            tma_load_2d(&tmB, &full[stage], sB + stage * Cfg::B_STAGE, kb * BK, b_row, hint_b);
+                            tma_load_4d(&tmA, &full[stage], sA + stage * Cfg::A_STAGE, c0, a_pl, c2, a_row, hint_a);
+                            tma_load_4d(&tmB, &full[stage], sB + stage * Cfg::B_STAGE, c0, b_pl, c2, b_row, hint_b);
                         } else {
                             const uint32_t lb = full0 + stage * 8u;
                             if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (Cfg::A_STAGE + Cfg::B_STAGE));
                             else mbar_arrive_cluster(full_leader + stage * 8u);
                             if (MC == 1) {
-                                tma_load_2d_cg2(&tmA, lb, sA + stage * Cfg::A_STAGE, kb * BK, a_row, hint_a);
+                                tma_load_4d_cg2(&tmA, lb, sA + stage * Cfg::A_STAGE, c0, a_pl, c2, a_row, hint_a);
                             } else {
                                 // this CTA's half of the A tile, multicast to the CTA with the same
                                 // rank in the other pair (which loads the other half for both)
                                 const uint16_t amask = static_cast<uint16_t>((1u << rank) | (1u << (rank + CG)));
-                                tma_load_2d_cg2_mc(&tmA, lb, sA + stage * Cfg::A_STAGE + pairi * (Cfg::A_STAGE / 2),
-                                                   kb * BK, a_row, amask, hint_a);
+                                tma_load_4d_cg2_mc(&tmA, lb, sA + stage * Cfg::A_STAGE + pairi * (Cfg::A_STAGE / 2),
+                                                   c0, a_pl, c2, a_row, amask, hint_a);
                             }
-                            tma_load_2d_cg2(&tmB, lb, sB + stage * Cfg::B_STAGE, kb * BK, b_row, hint_b);
+                            tma_load_4d_cg2(&tmB, lb, sB + stage * Cfg::B_STAGE, c0, b_pl, c2, b_row, hint_b);
                         }
                         if (++stage == NS) { stage = 0; phase ^= 1; }
                     }

@@ -370,7 +370,7 @@ static const int kTuneDefault[OZ2_TUNE_COUNT] = {
     1,    // SQ_ORDER
     0,    // CRT_GENERIC
     4,    // HOST_BLOCKS
-    1,    // KCAT
+    0,    // KCAT (measured 3 % slower at 16384^3: profiles/round2_kcat_ab.md)
 };
 
 struct ThreadState {
@@ -549,24 +549,40 @@ static PFN_encodeTiled_t encode_fn() {
     return fn;
 }
 
-// 2D byte tensor [outer][inner] with row pitch `pitch` bytes, box inner x outer, 128B swizzle
-static bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
-                     uint64_t pitch, uint32_t box_inner, uint32_t box_outer) {
+// 4-D byte tensor maps, box {128 bytes of K, 1 plane, 1 chunk, box_rows rows}, 128B swizzle
+// (the smem tile is the same 128-byte x box_rows block as a 2-D box):
+//   make_map_planes: interleaved digit planes, byte (x, r, h) at ((r KB + h/128) M + x) 128 +
+//                    h mod 128 (KB = k_pad/128 chunks, M planes per chunk group)
+//   make_map_plain:  a plain [rows][pitch] matrix with k bytes per row (the raw GEMM)
+static bool encode_map4(CUtensorMap* map, const void* base, const cuuint64_t (&dims)[4],
+                        const cuuint64_t (&strides)[3], uint32_t box_rows) {
     PFN_encodeTiled_t fn = encode_fn();
     if (!fn) return false;
-    cuuint64_t dims[2] = {inner, outer};
-    cuuint64_t strides[1] = {pitch};
-    cuuint32_t box[2] = {box_inner, box_outer};
-    cuuint32_t es[2] = {1, 1};
+    cuuint32_t box[4] = {static_cast<cuuint32_t>(BK), 1, 1, box_rows};
+    cuuint32_t es[4] = {1, 1, 1, 1};
     // L2 promotion of TMA misses (OZ2_TUNE_L2_PROMO: 0 none, 1 64B, 2 128B, 3 256B)
     const int promo = tune(OZ2_TUNE_L2_PROMO);
     const CUtensorMapL2promotion pr = promo == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
                                     : promo == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
                                     : promo == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
                                                  : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-    return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(base), dims, strides, box, es,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, pr,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+static bool make_map_planes(CUtensorMap* map, const void* base, int M, uint64_t k_pad, uint64_t rows,
+                            uint32_t box_rows) {
+    const uint64_t KB = k_pad / BK;
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(BK), static_cast<cuuint64_t>(M), KB, rows};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(BK), static_cast<cuuint64_t>(BK) * M,
+                                   static_cast<cuuint64_t>(BK) * M * KB};
+    return encode_map4(map, base, dims, strides, box_rows);
+}
+static bool make_map_plain(CUtensorMap* map, const void* base, uint64_t k, uint64_t rows, uint64_t pitch,
+                           uint32_t box_rows) {
+    const cuuint64_t dims[4] = {k, 1, 1, rows};
+    const cuuint64_t strides[3] = {pitch, pitch, pitch};
+    return encode_map4(map, base, dims, strides, box_rows);
 }
 
 static int sync_lead() {   // progress throttle of the residue GEMM (OZ2_TUNE_SYNC_LEAD)
@@ -668,6 +684,9 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
     auto* res = reinterpret_cast<int16_t*>(ws + L.res);
     uint8_t* abar = ws + L.abar;     // unblocked: the first digit plane, dead after step 3
     uint8_t* bbar = ws + L.bbar;
+    // A-bar / B-bar use the interleaved digit-plane layout with `gplanes` planes per chunk
+    // group: M when they live in plane 0 of the digit buffers, 1 in their own buffers
+    const int gplanes = L.blocked ? 1 : pl->M;
     int32_t* e_mu = eexp;
     int32_t* e_nu = eexp + m;
 
@@ -682,29 +701,28 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
         OZ2_CK(launch_rowmax(A, m, k, lda, a_kmajor, maxbits, st));
         OZ2_CK(launch_rowmax(B, n, k, ldb, b_kmajor, maxbits + m, st));
         if (fast) OZ2_CK(cudaMemsetAsync(sumsq, 0, 8 * static_cast<size_t>(m + n), st));
-        OZ2_CK(launch_cast(A, m, k, lda, a_kmajor, maxbits, eprime, abar, L.m_pad, L.k_pad, D().d_status,
+        OZ2_CK(launch_cast(A, m, k, lda, a_kmajor, maxbits, eprime, abar, gplanes, L.m_pad, L.k_pad, D().d_status,
                            fast ? sumsq : nullptr, i8, st));
-        OZ2_CK(launch_cast(B, n, k, ldb, b_kmajor, maxbits + m, eprime + m, bbar, L.n_pad, L.k_pad, D().d_status,
+        OZ2_CK(launch_cast(B, n, k, ldb, b_kmajor, maxbits + m, eprime + m, bbar, gplanes, L.n_pad, L.k_pad, D().d_status,
                            fast ? sumsq + m : nullptr, i8, st));
         if (opt && opt->e_prime_a) OZ2_CK(cudaMemcpyAsync(opt->e_prime_a, eprime, 4 * m, cudaMemcpyDeviceToDevice, st));
         if (opt && opt->e_prime_b) OZ2_CK(cudaMemcpyAsync(opt->e_prime_b, eprime + m, 4 * n, cudaMemcpyDeviceToDevice, st));
         if (opt && opt->abar && k && !fast)
-            OZ2_CK(cudaMemcpy2DAsync(opt->abar, k, abar, L.k_pad, k, m, cudaMemcpyDeviceToDevice, st));
+            OZ2_CK(launch_unpack_plane(opt->abar, abar, gplanes, 0, m, k, L.k_pad, st));
         if (opt && opt->bbar && k && !fast)
-            OZ2_CK(cudaMemcpy2DAsync(opt->bbar, k, bbar, L.k_pad, k, n, cudaMemcpyDeviceToDevice, st));
+            OZ2_CK(launch_unpack_plane(opt->bbar, bbar, gplanes, 0, n, k, L.k_pad, st));
         // ---- step 2: bound GEMM C-bar' = A-bar B-bar, row/column maxima
         phase_mark(1);
         if (!fast) {
             const int cg = cta_group(L.n_pad, i8);
             CUtensorMap ta, tb;
-            if (!make_map(&ta, abar, L.k_pad, L.m_pad, L.k_pad, BK, a_box_rows(cg))) return OZ2_ERR_CUDA;
-            if (!make_map(&tb, bbar, L.k_pad, L.n_pad, L.k_pad, BK, b_box_rows(cg))) return OZ2_ERR_CUDA;
+            if (!make_map_planes(&ta, abar, gplanes, L.k_pad, L.m_pad, a_box_rows(cg))) return OZ2_ERR_CUDA;
+            if (!make_map_planes(&tb, bbar, gplanes, L.k_pad, L.n_pad, b_box_rows(cg))) return OZ2_ERR_CUDA;
             GemmParams gp;
             std::memset(&gp, 0, sizeof(gp));
             gp.m = static_cast<int>(m); gp.n = static_cast<int>(n);
             gp.num_k_blocks = static_cast<int>(L.k_pad / BK);
             gp.m_tiles = static_cast<int>(L.m_pad / tile_m(cg)); gp.n_tiles = static_cast<int>(L.n_pad / BN);
-            gp.rows_per_plane_a = static_cast<int>(L.m_pad); gp.rows_per_plane_b = static_cast<int>(L.n_pad);
             gp.rmax = rsmax; gp.smax = rsmax + m;
             OZ2_CK(launch_gemm(i8 ? MODE_BOUND_I8 : MODE_BOUND, cg, 0, ta, tb, gp, D().num_sms, st));
         }
@@ -760,21 +778,19 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             if (!L.blocked) {
                 if (opt && opt->digits_a && k)
                     for (int x = 0; x < pl->M; ++x)
-                        OZ2_CK(cudaMemcpy2DAsync(opt->digits_a + static_cast<size_t>(x) * m * k, k,
-                                                 digA + static_cast<size_t>(x) * L.m_pad * L.k_pad, L.k_pad, k, m,
-                                                 cudaMemcpyDeviceToDevice, st));
+                        OZ2_CK(launch_unpack_plane(opt->digits_a + static_cast<size_t>(x) * m * k, digA, pl->M, x,
+                                                   m, k, L.k_pad, st));
                 if (opt && opt->digits_b && k)
                     for (int x = 0; x < pl->M; ++x)
-                        OZ2_CK(cudaMemcpy2DAsync(opt->digits_b + static_cast<size_t>(x) * n * k, k,
-                                                 digB + static_cast<size_t>(x) * L.n_pad * L.k_pad, L.k_pad, k, n,
-                                                 cudaMemcpyDeviceToDevice, st));
+                        OZ2_CK(launch_unpack_plane(opt->digits_b + static_cast<size_t>(x) * n * k, digB, pl->M, x,
+                                                   n, k, L.k_pad, st));
                 phase_mark(4);
             }
             // ---- step 5: 3N exact FP8 GEMMs with the modular epilogue
             const int cg = cta_group(nbj_pad, i8);
             CUtensorMap ta, tb;
-            if (!make_map(&ta, digA, L.k_pad, static_cast<uint64_t>(pl->M) * mbi_pad, L.k_pad, BK, a_box_rows(cg))) return OZ2_ERR_CUDA;
-            if (!make_map(&tb, digB, L.k_pad, static_cast<uint64_t>(pl->M) * nbj_pad, L.k_pad, BK, b_box_rows(cg))) return OZ2_ERR_CUDA;
+            if (!make_map_planes(&ta, digA, pl->M, L.k_pad, mbi_pad, a_box_rows(cg))) return OZ2_ERR_CUDA;
+            if (!make_map_planes(&tb, digB, pl->M, L.k_pad, nbj_pad, b_box_rows(cg))) return OZ2_ERR_CUDA;
             // square moduli: A1 B2 + A2 B1 K-concatenated in one accumulator when the sum
             // stays in the FP32 exactness window (k <= 2^15; OZ2_TUNE_KCAT)
             const bool kcat = tune(OZ2_TUNE_KCAT) != 0 && !i8 && pl->nsq > 0 && k <= kMaxK / 2;
@@ -786,7 +802,6 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             gp.kseg_blocks = kMaxK / BK;                                  // 2^16 per segment
             gp.num_kseg = (gp.num_k_blocks + gp.kseg_blocks - 1) / gp.kseg_blocks;
             gp.m_tiles = static_cast<int>(mbi_pad / tile_m(cg)); gp.n_tiles = static_cast<int>(nbj_pad / BN);
-            gp.rows_per_plane_a = static_cast<int>(mbi_pad); gp.rows_per_plane_b = static_cast<int>(nbj_pad);
             gp.num_moduli = N;
             {   // work items (OZ2_TUNE_MOD_SPLIT: -1 auto, 0 tile-major, 1 all (tile, modulus),
                 // 2 hybrid): few tiles (< 8 per persistent unit) -> all split; otherwise
@@ -1193,14 +1208,15 @@ static int gemm_raw(int mode, const uint8_t* a, const uint8_t* b, float* C32, in
     if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15u) return OZ2_ERR_NOT_SUPPORTED;
     const int cg = cta_group(((n + BN - 1) / BN) * BN, mode == MODE_RAW_I8);
     CUtensorMap ta, tb;
-    if (!make_map(&ta, a, k, m, k, BK, a_box_rows(cg))) return OZ2_ERR_CUDA;
-    if (!make_map(&tb, b, k, n, k, BK, b_box_rows(cg))) return OZ2_ERR_CUDA;
+    if (!make_map_plain(&ta, a, k, m, k, a_box_rows(cg))) return OZ2_ERR_CUDA;
+    if (!make_map_plain(&tb, b, k, n, k, b_box_rows(cg))) return OZ2_ERR_CUDA;
     GemmParams gp;
     std::memset(&gp, 0, sizeof(gp));
     gp.m = static_cast<int>(m); gp.n = static_cast<int>(n);
     gp.num_k_blocks = static_cast<int>((k + BK - 1) / BK);
     gp.m_tiles = static_cast<int>((m + tile_m(cg) - 1) / tile_m(cg)); gp.n_tiles = static_cast<int>((n + BN - 1) / BN);
     gp.c32 = C32;
+    gp.plain_k = 1;
     OZ2_CK(launch_gemm(mode, cg, 0, ta, tb, gp, D().num_sms, g_ts.stream));
     return OZ2_SUCCESS;
 }

@@ -70,8 +70,8 @@ struct GemmParams {
     int num_kseg;                // residue mode: K segments of <= kseg_blocks k-blocks
     int kseg_blocks;             // 512 (= 2^16 / BK): FP32 exactness window per segment
     int m_tiles, n_tiles;
-    int rows_per_plane_a;        // m_pad
-    int rows_per_plane_b;        // n_pad
+    int plain_k;                 // 1: operands are plain [rows][k] matrices (raw GEMM);
+                                 // 0: interleaved digit planes
     int num_moduli;
     int tail_head;               // residue mode: tiles [0, head) tile-major, the rest as
                                  // (tile, modulus) items (no fused CRT unless head = all tiles)
@@ -138,7 +138,7 @@ struct FastExpParams {
 cudaError_t launch_rowmax(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
                           unsigned long long* maxbits, cudaStream_t st);
 cudaError_t launch_cast(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
-                        const unsigned long long* maxbits, int32_t* eprime, uint8_t* xbar,
+                        const unsigned long long* maxbits, int32_t* eprime, uint8_t* xbar, int gplanes,
                         int64_t rows_pad, int64_t k_pad, int32_t* status,
                         unsigned long long* sumsq, bool i8, cudaStream_t st);
 cudaError_t launch_exps_fast(const unsigned long long* maxbits, const int32_t* eprime,
@@ -150,6 +150,9 @@ cudaError_t launch_exps(const unsigned long long* maxbits, const int32_t* eprime
 cudaError_t launch_digits(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
                           const int32_t* e, const DigitParams& dp, uint8_t* planes,
                           int64_t rows_pad, int64_t k_pad, cudaStream_t st);
+// plane x of the interleaved layout (gplanes planes per chunk group) -> dst [rows][k]
+cudaError_t launch_unpack_plane(uint8_t* dst, const uint8_t* src, int gplanes, int x, int64_t rows, int64_t k,
+                                int64_t k_pad, cudaStream_t st);
 cudaError_t launch_gemm(int mode, int cg, int fused_limbs, const CUtensorMap& ta, const CUtensorMap& tb,
                         const GemmParams& gp, int num_sms, cudaStream_t st);
 cudaError_t launch_res_symmetric(int16_t* out, const int16_t* in, int64_t per, const CrtParams& cp,

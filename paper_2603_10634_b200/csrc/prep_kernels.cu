@@ -7,8 +7,12 @@
 //
 // An operand is seen as `rows` rows of length k (A: rows = i; B: rows = j of B^T).
 // Element (r, h) lives at X[r + h*ld] (MN-major: A with transa='N', B with 'T') or
-// X[h + r*ld] (K-major: A 'T', B 'N').  Outputs are K-major byte planes
-// [rows_pad][k_pad] (the tcgen05 operand layout), zero in the padding.
+// X[h + r*ld] (K-major: A 'T', B 'N').  Outputs are K-major byte planes in the
+// interleaved layout: byte (plane x, row r, k index h) at
+// ((r KB + h/128) M + x) 128 + h mod 128, KB = k_pad/128, M planes per group -- for each
+// row and 128-wide K chunk the chunks of all M planes are adjacent, so a thread's stores to
+// the planes of one modulus differ by compile-time multiples of 128 bytes.  Zero in the
+// padding.
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "oz2_internal.h"
@@ -146,7 +150,7 @@ template <bool KMAJOR, bool FAST, bool I8>
 __global__ void __launch_bounds__(256) k_cast(const double* __restrict__ X, int64_t rows, int64_t k,
                                               int64_t ld, const unsigned long long* __restrict__ maxbits,
                                               int32_t* __restrict__ eprime, uint8_t* __restrict__ xbar,
-                                              int64_t k_pad, int32_t* __restrict__ status,
+                                              int gplanes, int64_t k_pad, int32_t* __restrict__ status,
                                               unsigned long long* __restrict__ sumsq) {
     __shared__ double tile[TR * TP];
     const int64_t h0 = static_cast<int64_t>(blockIdx.x) * TH;
@@ -182,8 +186,20 @@ __global__ void __launch_bounds__(256) k_cast(const double* __restrict__ X, int6
                 if (I8) {
                     c = static_cast<uint32_t>(ceil((fabs(x) * s1) * s2));   // exact: < 2^7 scaled
                 } else {
-                    c = fp8_ru_code((fabs(x) * s1) * s2);
-                    c = c ? c : 1u;           // an underflowed nonzero still rounds up to 2^-9
+                    // RU_e4m3(|x| 2^e) on the integer pipes (no F2F): in the E4M3 normal range
+                    // y = |x| 2^e >= 2^-6 the scaling is an exponent-field add and the round-up
+                    // to 3 significand bits an add of the sticky bit at bit 49
+                    const uint32_t hx = static_cast<uint32_t>(__double2hiint(x)) & 0x7FFFFFFFu;
+                    const uint32_t lx = static_cast<uint32_t>(__double2loint(x));
+                    const int ey = static_cast<int>(hx >> 20) + e;
+                    if ((hx >> 20) != 0u && ey >= 1017) {
+                        const uint32_t hy = hx + (static_cast<uint32_t>(e) << 20);
+                        const uint32_t sticky = ((hy & 0x1FFFFu) | lx) != 0u ? 0x20000u : 0u;
+                        c = (((hy & ~0x1FFFFu) + sticky) >> 17) - 8128u;     // (E + 7) 8 + M3
+                    } else {
+                        c = fp8_ru_code((fabs(x) * s1) * s2);   // E4M3 subnormal grid (or tiny x)
+                        c = c ? c : 1u;           // an underflowed nonzero still rounds up to 2^-9
+                    }
                 }
             }
             if (FAST) sq += I8 ? static_cast<unsigned long long>(c * c) : fp8_sq_units(c);
@@ -194,7 +210,7 @@ __global__ void __launch_bounds__(256) k_cast(const double* __restrict__ X, int6
             for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
             if (lane == 0 && sq && r < rows) atomicAdd(sumsq + r, sq);
         } else {
-            *reinterpret_cast<uint32_t*>(xbar + r * k_pad + h0 + lane * 4) = word;
+            *reinterpret_cast<uint32_t*>(xbar + ((r * (k_pad / TH) + blockIdx.x) * gplanes) * TH + lane * 4) = word;
         }
     }
 }
@@ -277,6 +293,7 @@ __device__ __forceinline__ double dfma_rn(double a, double b, double c) {   // k
 // digit plane (kEPL = 8 -- one 8-byte store per plane -- was measured: 4 % fewer
 // instructions but 17 % slower for the MN-major operand, 78 vs 50 registers)
 constexpr int kEPL = 4;
+constexpr int kPlanePitch = TH;  // bytes between the same chunk of consecutive planes
 using DWord = uint32_t;          // kEPL bytes of one digit plane
 static_assert(sizeof(DWord) == kEPL && TH % kEPL == 0 && 32 % (TH / kEPL) == 0, "k_digits lane map");
 
@@ -288,14 +305,13 @@ static_assert(sizeof(DWord) == kEPL && TH % kEPL == 0 && 32 % (TH / kEPL) == 0, 
 // SQ: 1 square, 0 non-square, -1 read md.square at run time, 2 INT8 scheme (the residue
 // itself, as a two's-complement byte, is the single operand plane of the modulus)
 template <int SQ>
-__device__ __forceinline__ void emit_digits(const ModDig& md, const float (&rf)[kEPL], uint8_t* o,
-                                            int64_t plane_stride);
+__device__ __forceinline__ void emit_digits(const ModDig& md, const float (&rf)[kEPL], uint8_t* o);
 
 template <int NSTEP, int SQ>
 __device__ __forceinline__ void digits_one_modulus(const ModDig& md, int l, int plane0, const double (&y)[kEPL],
                                                    const double (&M)[kEPL], const int (&E)[kEPL],
                                                    const uint16_t* __restrict__ pow2tab,
-                                                   uint8_t* out, int64_t plane_stride) {
+                                                   uint8_t* out) {
     const double pinv = md.pinv_d, pd = md.p_d, magic = kMagic52;
     float rf[kEPL];
 #pragma unroll
@@ -338,14 +354,13 @@ __device__ __forceinline__ void digits_one_modulus(const ModDig& md, int l, int 
             rf[q + 1] = rs.y;
         }
     }
-    emit_digits<SQ>(md, rf, out + static_cast<int64_t>(plane0) * plane_stride, plane_stride);
+    emit_digits<SQ>(md, rf, out + plane0 * kPlanePitch);
 }
 
 // the digit planes (or the INT8 residue plane) of one modulus from the exact symmetric
 // residues rf[kEPL] of the lane's kEPL consecutive elements
 template <int SQ>
-__device__ __forceinline__ void emit_digits(const ModDig& md, const float (&rf)[kEPL], uint8_t* o,
-                                            int64_t plane_stride) {
+__device__ __forceinline__ void emit_digits(const ModDig& md, const float (&rf)[kEPL], uint8_t* o) {
     if (SQ == 2) {
         DWord w = 0;
 #pragma unroll
@@ -371,7 +386,7 @@ __device__ __forceinline__ void emit_digits(const ModDig& md, const float (&rf)[
             w2 |= static_cast<DWord>(cvt_e4m3x2(d2.x, d2.y)) << (8 * q);
         }
         *reinterpret_cast<DWord*>(o) = w1;
-        *reinterpret_cast<DWord*>(o + plane_stride) = w2;
+        *reinterpret_cast<DWord*>(o + kPlanePitch) = w2;
     } else {
         // D1 = sign(r) ceil(|r|/16), D2 = r - 16 D1, D3 = D1 + D2
         const float2 s16 = make_float2(0.0625f, 0.0625f), n16 = make_float2(-16.0f, -16.0f);
@@ -389,40 +404,40 @@ __device__ __forceinline__ void emit_digits(const ModDig& md, const float (&rf)[
             w3 |= static_cast<DWord>(cvt_e4m3x2(d3.x, d3.y)) << (8 * q);
         }
         *reinterpret_cast<DWord*>(o) = w1;
-        *reinterpret_cast<DWord*>(o + plane_stride) = w2;
-        *reinterpret_cast<DWord*>(o + 2 * plane_stride) = w3;
+        *reinterpret_cast<DWord*>(o + kPlanePitch) = w2;
+        *reinterpret_cast<DWord*>(o + 2 * kPlanePitch) = w3;
     }
 }
 
 template <int NSTEP, int NMOD, bool I8, int NSQ>
 __device__ __forceinline__ void digits_all_moduli(const DigitParams& dp, const double (&y)[kEPL],
                                                   const double (&M)[kEPL], const int (&E)[kEPL],
-                                                  uint8_t* out, int64_t plane_stride) {
+                                                  uint8_t* out) {
     if (I8) {
         // INT8 scheme: one S8 plane per modulus, plane l
         if (NMOD > 0) {
 #pragma unroll
             for (int l = 0; l < NMOD; ++l)
-                digits_one_modulus<NSTEP, 2>(dp.mod[l], l, l, y, M, E, dp.pow2tab, out, plane_stride);
+                digits_one_modulus<NSTEP, 2>(dp.mod[l], l, l, y, M, E, dp.pow2tab, out);
         } else {
 #pragma unroll 1
             for (int l = 0; l < dp.num_moduli; ++l)
-                digits_one_modulus<NSTEP, 2>(dp.mod[l], l, l, y, M, E, dp.pow2tab, out, plane_stride);
+                digits_one_modulus<NSTEP, 2>(dp.mod[l], l, l, y, M, E, dp.pow2tab, out);
         }
     } else if (NMOD > 0) {
         // hybrid order (eq. p_list_hybrid): the first min(N, 6) moduli are the squares;
         // Karatsuba family (eq. p_list_karatsuba, NSQ = 0): none
 #pragma unroll
         for (int l = 0; l < NMOD && l < NSQ; ++l)
-            digits_one_modulus<NSTEP, 1>(dp.mod[l], l, 2 * l, y, M, E, dp.pow2tab, out, plane_stride);
+            digits_one_modulus<NSTEP, 1>(dp.mod[l], l, 2 * l, y, M, E, dp.pow2tab, out);
 #pragma unroll
         for (int l = NSQ; l < NMOD; ++l)
             digits_one_modulus<NSTEP, 0>(dp.mod[l], l, 2 * NSQ + 3 * (l - NSQ), y, M, E,
-                                         dp.pow2tab, out, plane_stride);
+                                         dp.pow2tab, out);
     } else {
 #pragma unroll 1
         for (int l = 0; l < dp.num_moduli; ++l)
-            digits_one_modulus<NSTEP, -1>(dp.mod[l], l, dp.mod[l].plane0, y, M, E, dp.pow2tab, out, plane_stride);
+            digits_one_modulus<NSTEP, -1>(dp.mod[l], l, dp.mod[l].plane0, y, M, E, dp.pow2tab, out);
     }
 }
 
@@ -435,8 +450,7 @@ __device__ __forceinline__ void digits_all_moduli(const DigitParams& dp, const d
 // closer than 1/(2p) to a half-integer, so the rounding is exact.  Bit-identical to
 // digits_one_modulus<1, .> (same residues, same digit code).
 template <int NMOD, bool I8, int NSQ, int EVEN>
-__device__ __forceinline__ void digits_paired(const DigitParams& dp, const double (&y)[kEPL], uint8_t* out,
-                                              int64_t plane_stride) {
+__device__ __forceinline__ void digits_paired(const DigitParams& dp, const double (&y)[kEPL], uint8_t* out) {
     const float2 M2 = make_float2(kMagic23, kMagic23), nM2 = make_float2(-kMagic23, -kMagic23);
 #pragma unroll
     for (int l = 0; l < NMOD; l += 2) {
@@ -467,12 +481,11 @@ __device__ __forceinline__ void digits_paired(const DigitParams& dp, const doubl
                 rf[q + 1] = sv.y;
             }
             if (I8) {
-                emit_digits<2>(md, rf, out + static_cast<int64_t>(lm) * plane_stride, plane_stride);
+                emit_digits<2>(md, rf, out + lm * kPlanePitch);
             } else if (lm < NSQ) {
-                emit_digits<1>(md, rf, out + static_cast<int64_t>(2 * lm) * plane_stride, plane_stride);
+                emit_digits<1>(md, rf, out + 2 * lm * kPlanePitch);
             } else {
-                emit_digits<0>(md, rf, out + static_cast<int64_t>(2 * NSQ + 3 * (lm - NSQ)) * plane_stride,
-                               plane_stride);
+                emit_digits<0>(md, rf, out + (2 * NSQ + 3 * (lm - NSQ)) * kPlanePitch);
             }
         }
     }
@@ -491,7 +504,7 @@ __global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, in
     load_tile<KMAJOR>(X, rows, k, ld, r0, h0, tile);
     __syncthreads();
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const int64_t plane_stride = rows_pad * k_pad;
+    const int64_t group = static_cast<int64_t>(dp.num_planes) * kPlanePitch;   // bytes per (row, chunk)
     // a lane owns kEPL consecutive k of one row: kLPR lanes per row, 32 / kLPR rows per warp
     constexpr int kLPR = TH / kEPL, kRPW = 32 / kLPR;
     const int lrow = lane / kLPR, hl = (lane % kLPR) * kEPL;
@@ -513,11 +526,8 @@ __global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, in
             y[q] = copysign(a, v);
             amax = fmax(amax, a);
         }
-        uint8_t* out = planes + r * k_pad + h0 + hl;
-        // opaque per iteration: keeps the compiler from hoisting all M_N plane offsets
-        // (64-bit each) out of the row loop into registers
-        int64_t ps;
-        asm volatile("mov.b64 %0, %1;" : "=l"(ps) : "l"(plane_stride));
+        // plane x of this (row, chunk) at out + x 128: immediate store offsets
+        uint8_t* out = planes + (r * (k_pad / TH) + blockIdx.x) * group + hl;
         // warp-uniform choice of the reduction depth
         const bool need2 = __any_sync(0xffffffffu, amax >= dp.lim1);   // 2^50 p_min (~2^59 hybrid)
         const bool need0 = __any_sync(0xffffffffu, amax >= dp.lim2);   // 2^86 p_min
@@ -534,13 +544,13 @@ __global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, in
                 M[q] = a;
                 E[q] = ee;
             }
-            digits_all_moduli<0, NMOD, I8, NSQ>(dp, y, M, E, out, ps);
+            digits_all_moduli<0, NMOD, I8, NSQ>(dp, y, M, E, out);
         } else if (need2) {
-            digits_all_moduli<2, NMOD, I8, NSQ>(dp, y, M, E, out, ps);
+            digits_all_moduli<2, NMOD, I8, NSQ>(dp, y, M, E, out);
         } else if (NMOD > 0) {
-            digits_paired<NMOD, I8, NSQ, I8 ? 0 : 1>(dp, y, out, ps);   // the even modulus: 256 / 1024 / 512
+            digits_paired<NMOD, I8, NSQ, I8 ? 0 : 1>(dp, y, out);   // the even modulus: 256 / 1024 / 512
         } else {
-            digits_all_moduli<1, NMOD, I8, NSQ>(dp, y, M, E, out, ps);
+            digits_all_moduli<1, NMOD, I8, NSQ>(dp, y, M, E, out);
         }
     }
 }
@@ -552,8 +562,27 @@ __global__ void k_scale(double* C, int64_t m, int64_t n, int64_t ldc, double bet
     }
 }
 
+// plane x of the interleaved layout -> [rows][k] (debug outputs of oz2_dgemm_ex only)
+__global__ void k_unpack_plane(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, int gplanes, int x,
+                               int64_t rows, int64_t k, int64_t k_pad) {
+    const int64_t kb = k_pad / TH;
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y)
+        for (int64_t h = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; h < k;
+             h += static_cast<int64_t>(gridDim.x) * blockDim.x)
+            dst[r * k + h] = src[((r * kb + h / TH) * gplanes + x) * TH + h % TH];
+}
+
 // ---------------------------------------------------------------------------------
 // launchers
+
+cudaError_t launch_unpack_plane(uint8_t* dst, const uint8_t* src, int gplanes, int x, int64_t rows, int64_t k,
+                                int64_t k_pad, cudaStream_t st) {
+    if (rows == 0 || k == 0) return cudaSuccess;
+    const int64_t gx = (k + 255) / 256;
+    dim3 grid(static_cast<unsigned>(gx < 64 ? gx : 64), static_cast<unsigned>(rows < 65535 ? rows : 65535));
+    k_unpack_plane<<<grid, 256, 0, st>>>(dst, src, gplanes, x, rows, k, k_pad);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_rowmax(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
                           unsigned long long* maxbits, cudaStream_t st) {
@@ -569,11 +598,11 @@ cudaError_t launch_rowmax(const double* X, int64_t rows, int64_t k, int64_t ld, 
 }
 
 cudaError_t launch_cast(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
-                        const unsigned long long* maxbits, int32_t* eprime, uint8_t* xbar,
+                        const unsigned long long* maxbits, int32_t* eprime, uint8_t* xbar, int gplanes,
                         int64_t rows_pad, int64_t k_pad, int32_t* status,
                         unsigned long long* sumsq, bool i8, cudaStream_t st) {
     dim3 grid(static_cast<unsigned>(k_pad / TH), static_cast<unsigned>(rows_pad / TR));
-#define OZ2_CAST(KM, FA, I8_) k_cast<KM, FA, I8_><<<grid, 256, 0, st>>>(X, rows, k, ld, maxbits, eprime, xbar, k_pad, status, sumsq)
+#define OZ2_CAST(KM, FA, I8_) k_cast<KM, FA, I8_><<<grid, 256, 0, st>>>(X, rows, k, ld, maxbits, eprime, xbar, gplanes, k_pad, status, sumsq)
     const int sel = (kmajor ? 4 : 0) | (sumsq ? 2 : 0) | (i8 ? 1 : 0);
     switch (sel) {
         case 0: OZ2_CAST(false, false, false); break;
