@@ -246,6 +246,11 @@ int oz2_finalize(void);
  *   OZ2_TUNE_KCAT        0    square moduli: accumulate A1B2 + A2B1 in one TMEM
  *                             accumulator (K-concatenated) when k <= 2^15 (two
  *                             accumulator drains instead of three; measured slower)
+ *   OZ2_TUNE_PRESCALE_2READ 0 accurate-mode step 1: 0 = one read of A and B (chunk-local
+ *                             casts, then a rescale of A-bar/B-bar to the row exponent),
+ *                             1 = row maxima then cast (two reads; fast mode always)
+ *   OZ2_TUNE_EPI_SLEEP 1000   residue GEMM: ns the epilogue warps sleep between polls of a
+ *                             filling accumulator (0 = spin on mbarrier.try_wait)
  *
  * oz2_set_tuning returns -1 for an unknown knob, -2 for a value out of range;
  * oz2_get_tuning writes the current value. */
@@ -262,7 +267,9 @@ int oz2_finalize(void);
 #define OZ2_TUNE_CRT_GENERIC 10
 #define OZ2_TUNE_HOST_BLOCKS 11
 #define OZ2_TUNE_KCAT        12
-#define OZ2_TUNE_COUNT       13
+#define OZ2_TUNE_PRESCALE_2READ 13
+#define OZ2_TUNE_EPI_SLEEP   14
+#define OZ2_TUNE_COUNT       15
 int oz2_set_tuning(int knob, int value);
 int oz2_get_tuning(int knob, int* value);
 void oz2_reset_tuning(void);
@@ -303,6 +310,16 @@ const char* oz2_version(void);
  */
 int oz2_fp8_gemm_raw(const uint8_t* a, const uint8_t* b, float* C32,
                      int64_t m, int64_t n, int64_t k);
+
+/* Step 2's kernel on plain operands (the bound GEMM of P:352-362, MODE_BOUND):
+ * rmax[i] = max over j and smax[j] = max over i of the FP32 accumulator C32[i][j] =
+ * sum_h a[i][h] b[j][h], as float bit patterns merged with atomicMax into the caller's
+ * arrays (zero them first; the bit order is the numeric order for non-negative results, as
+ * for the RU-cast operands of step 1).  a, b as for oz2_fp8_gemm_raw.  Used to time the
+ * tensor-core pipeline with a near-empty epilogue against the vendor FP8 GEMM on the same
+ * data (tools/power_probe.py). */
+int oz2_fp8_gemm_bound(const uint8_t* a, const uint8_t* b, uint32_t* rmax, uint32_t* smax,
+                       int64_t m, int64_t n, int64_t k);
 
 /* The same on the INT8 path (kind::i8): C32[i][j] = sum_h a[i][h] b[j][h], S8 inputs,
  * S32 accumulation (exact while |sum| < 2^31). */

@@ -147,8 +147,12 @@ __device__ __forceinline__ void tmem_dealloc_cg(uint32_t taddr, uint32_t ncols) 
     else asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
 
+__device__ constexpr float2 kM2 = {12582912.0f, 12582912.0f};      // 1.5 2^23
+__device__ constexpr float2 kNM2 = {-12582912.0f, -12582912.0f};
+__device__ constexpr float2 kNM2b = {-8388608.0f, -8388608.0f};     // -2^23
+
 template <int MODE_, int CG, int FL, int MC>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __maxnreg__(200)   // 320 threads, one CTA per SM (launch_bounds would cap at 168 and spill)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
             const __grid_constant__ GemmParams P) {
     // INT8 variants run the same pipeline on kind::i8 (S32 accumulators)
@@ -248,7 +252,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             long long g = 0;                         // throttle chunks started by this unit
             bool throttle_on = true;
             const long long nunits = units;
-            const int kc = P.sync_chunk > 0 ? P.sync_chunk : nkb;   // k-blocks per chunk
+            const int kc = P.sync_chunk > 0 ? P.sync_chunk : 1 << 30;   // k-blocks per chunk (power of two)
             const long long chunks_per_prod = (nkb + kc - 1) / kc;
             const uint32_t full0 = smem_u32(&full[0]) & 0xFEFFFFFFu;   // pair leader's barrier (TMA operand)
             const uint32_t full_leader = (CS > 1) ? mapa_shared(smem_u32(&full[0]), crank & ~(CG - 1u)) : 0u;
@@ -275,7 +279,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         kb1 = min(nkb, kb0 + kseg);
                     }
                     for (int kb = kb0; kb < kb1; ++kb) {
-                        if (P.sync_lead > 0 && kb % kc == 0) {
+                        if (P.sync_lead > 0 && (kb & (kc - 1)) == 0) {     // kc: a power of two
                             // progress throttle: a unit may not run more than sync_lead chunks
                             // (sync_chunk k-blocks each) ahead of the chip-wide average, so
                             // the operand panels streamed by all units stay L2-resident
@@ -295,10 +299,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                             ++g;
                         }
                         mbar_wait(&empty[stage], phase ^ 1);
-                        // map coordinates {K byte, plane, K chunk, row}: interleaved digit
-                        // planes (plane, chunk kb) or a plain [rows][k] matrix (raw GEMM:
-                        // dimension 0 spans the row, plane and chunk are 0)
-                        const int c0 = P.plain_k ? kb * BK : 0, c2 = P.plain_k ? 0 : kb;
+                        // map coordinates {K byte in the super-chunk, plane, super-chunk, row}
+                        // (digit planes; a plain [rows][k] matrix for the
+                        // raw GEMM: shift 30, dimension 0 spans the row)
+                        const int c0 = (kb & ((1 << P.super_shift) - 1)) * BK, c2 = kb >> P.super_shift;
                         if (CG == 1) {
                             mbar_arrive_expect_tx(&full[stage], Cfg::A_STAGE + Cfg::B_STAGE);
                             tma_load_4d(&tmA, &full[stage], sA + stage * Cfg::A_STAGE, c0, a_pl, c2, a_row, hint_a);
@@ -441,7 +445,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         const bool first = (x == 0) && (seg == 0);
                         const bool last = (x == npl - 1) && (seg == nseg - 1);
                         const uint32_t slot = g & 1u, use = g >> 1;
-                        mbar_wait(&tfull[slot], use & 1u);
+                        // the other slot's product is still running: no hurry (the MMAs of
+                        // product g+2 need this slot only after product g+1, ~60 us away)
+                        if (P.epi_sleep_ns) mbar_wait_sleep(&tfull[slot], use & 1u, P.epi_sleep_ns);
+                        else mbar_wait(&tfull[slot], use & 1u);
                         tc_fence_after();
                         const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + slot * BN + half * 128u;
 #pragma unroll
@@ -452,36 +459,31 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                             if (c == 3) release_slot(slot);   // the whole slot is in registers
 #pragma unroll
                             for (int j = 0; j < 32; j += 2) {
-                                float acc[2];
-#pragma unroll
-                                for (int u = 0; u < 2; ++u) {
-                                    float f;
-                                    if (I8) {
-                                        // S32 sum (|.| <= 2^30) == hi w16 + lo (mod p): both
-                                        // halves exact floats via the 2^23 exponent trick,
-                                        // |f| < 2^15 128 + 2^16 < 2^23 exact
-                                        const int iv = static_cast<int>(v[j + u]);
-                                        const float hi = __int_as_float(0x4B400000 + (iv >> 16)) - 12582912.0f;
-                                        const float lo = __int_as_float(0x4B000000 | (iv & 0xFFFF)) - 8388608.0f;
-                                        f = fmaf(hi, w16, lo);
-                                    } else {
-                                        f = __uint_as_float(v[j + u]);                // exact integer, |f| <= 2^24
-                                    }
-                                    // f mod p: |r| <= p/2 + 1 (FP8) or <= 3p/2 (INT8, reduced again below)
-                                    const float r = fmaf(-rintf(f * pinv), p, f);
-                                    acc[u] = r;
-                                }
-                                const int idx = (c * 32 + j) >> 1;
-                                if (first) {
-                                    acc[0] *= coef;
-                                    acc[1] *= coef;
+                                // packed FP32 pairs; x - p rint(x/p) by the 1.5 2^23 magic-number
+                                // rounding of one FFMA2 (exact: |x/p| < 2^22)
+                                float2 f;
+                                if (I8) {
+                                    // S32 sum (|.| <= 2^30) == hi w16 + lo (mod p): both halves
+                                    // exact floats via the 2^23 exponent trick, |f| < 2^23
+                                    const int i0 = static_cast<int>(v[j]), i1 = static_cast<int>(v[j + 1]);
+                                    const float2 hi = __fadd2_rn(make_float2(__int_as_float(0x4B400000 + (i0 >> 16)),
+                                                                             __int_as_float(0x4B400000 + (i1 >> 16))), kNM2);
+                                    const float2 lo = __fadd2_rn(make_float2(__int_as_float(0x4B000000 | (i0 & 0xFFFF)),
+                                                                             __int_as_float(0x4B000000 | (i1 & 0xFFFF))), kNM2b);
+                                    f = __ffma2_rn(hi, make_float2(w16, w16), lo);
                                 } else {
-                                    const float2 pv = __half22float2(part[idx]);
-                                    acc[0] = fmaf(coef, acc[0], pv.x);
-                                    acc[1] = fmaf(coef, acc[1], pv.y);
+                                    f = make_float2(__uint_as_float(v[j]), __uint_as_float(v[j + 1]));   // exact, <= 2^24
                                 }
-#pragma unroll
-                                for (int u = 0; u < 2; ++u) acc[u] = fmaf(-rintf(acc[u] * pinv), p, acc[u]);
+                                const float2 pinv2 = make_float2(pinv, pinv), np2 = make_float2(-p, -p);
+                                float2 q = __fadd2_rn(__ffma2_rn(f, pinv2, kM2), kNM2);
+                                float2 a2 = __ffma2_rn(q, np2, f);
+                                const int idx = (c * 32 + j) >> 1;
+                                const float2 cf = make_float2(coef, coef);
+                                if (first) a2 = __fmul2_rn(a2, cf);
+                                else a2 = __ffma2_rn(a2, cf, __half22float2(part[idx]));
+                                q = __fadd2_rn(__ffma2_rn(a2, pinv2, kM2), kNM2);
+                                a2 = __ffma2_rn(q, np2, a2);
+                                float acc[2] = {a2.x, a2.y};
                                 if (!last) {
                                     part[idx] = __floats2half2_rn(acc[0], acc[1]);  // exact (|acc| <= 546)
                                 } else {

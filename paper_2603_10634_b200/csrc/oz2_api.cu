@@ -370,7 +370,9 @@ static const int kTuneDefault[OZ2_TUNE_COUNT] = {
     1,    // SQ_ORDER
     0,    // CRT_GENERIC
     4,    // HOST_BLOCKS
-    0,    // KCAT (measured 3 % slower at 16384^3: profiles/round2_kcat_ab.md)
+    0,    // KCAT (no measurable gain at 16384^3: profiles/round2_layout_ab.md)
+    0,    // PRESCALE_2READ
+    1000, // EPI_SLEEP (ns)
 };
 
 struct ThreadState {
@@ -471,14 +473,14 @@ struct Layout {
     int64_t m_pad, n_pad, k_pad, mb, nb, mb_pad, nb_pad;
     int M;
     bool blocked;
-    size_t maxbits, eprime, rsmax, sumsq, eexp, abar, bbar, digA, digB, res, total;
+    size_t maxbits, eprime, rsmax, sumsq, eexp, eloc, abar, bbar, digA, digB, res, total;
 };
 
 static Layout make_layout(int64_t m, int64_t n, int64_t k, int N, int M, int64_t mb = 0, int64_t nb = 0) {
     Layout L{};
     L.m_pad = round_up(m, PAD_M);
     L.n_pad = round_up(n, PAD_N);
-    L.k_pad = round_up(k, PAD_K);
+    L.k_pad = pad_k(k);            // super-chunk layout (oz2_internal.h)
     L.mb = (mb <= 0 || mb >= m) ? m : mb;
     L.nb = (nb <= 0 || nb >= n) ? n : nb;
     L.mb_pad = round_up(L.mb, PAD_M);
@@ -491,7 +493,8 @@ static Layout make_layout(int64_t m, int64_t n, int64_t k, int N, int M, int64_t
     L.eprime = off;  off = align_up(off + 4 * mn, 256);
     L.rsmax = off;   off = align_up(off + 4 * mn, 256);
     L.sumsq = off;   off = align_up(off + 8 * mn, 256);
-    L.eexp = off;    off = align_up(off + 4 * mn, 1024);
+    L.eexp = off;    off = align_up(off + 4 * mn, 256);
+    L.eloc = off;    off = align_up(off + 2 * mn * static_cast<size_t>((k + BK - 1) / BK), 1024);   // chunk exponents
     if (L.blocked) {
         L.abar = off; off = align_up(off + static_cast<size_t>(L.m_pad) * L.k_pad, 1024);
         L.bbar = off; off = align_up(off + static_cast<size_t>(L.n_pad) * L.k_pad, 1024);
@@ -549,10 +552,10 @@ static PFN_encodeTiled_t encode_fn() {
     return fn;
 }
 
-// 4-D byte tensor maps, box {128 bytes of K, 1 plane, 1 chunk, box_rows rows}, 128B swizzle
-// (the smem tile is the same 128-byte x box_rows block as a 2-D box):
-//   make_map_planes: interleaved digit planes, byte (x, r, h) at ((r KB + h/128) M + x) 128 +
-//                    h mod 128 (KB = k_pad/128 chunks, M planes per chunk group)
+// 4-D byte tensor maps, box {128 bytes of K, 1 plane, 1 super-chunk, box_rows rows}, 128B
+// swizzle (the smem tile is the same 128-byte x box_rows block as a 2-D box):
+//   make_map_planes: digit planes, byte (x, r, h) at ((r KS + h/S) M + x) S + h mod S
+//                    (S = super_bytes(k_pad), KS = k_pad/S super-chunks, M planes per group)
 //   make_map_plain:  a plain [rows][pitch] matrix with k bytes per row (the raw GEMM)
 static bool encode_map4(CUtensorMap* map, const void* base, const cuuint64_t (&dims)[4],
                         const cuuint64_t (&strides)[3], uint32_t box_rows) {
@@ -572,10 +575,9 @@ static bool encode_map4(CUtensorMap* map, const void* base, const cuuint64_t (&d
 }
 static bool make_map_planes(CUtensorMap* map, const void* base, int M, uint64_t k_pad, uint64_t rows,
                             uint32_t box_rows) {
-    const uint64_t KB = k_pad / BK;
-    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(BK), static_cast<cuuint64_t>(M), KB, rows};
-    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(BK), static_cast<cuuint64_t>(BK) * M,
-                                   static_cast<cuuint64_t>(BK) * M * KB};
+    const uint64_t S = static_cast<uint64_t>(super_bytes(static_cast<int64_t>(k_pad))), KS = k_pad / S;
+    const cuuint64_t dims[4] = {S, static_cast<cuuint64_t>(M), KS, rows};
+    const cuuint64_t strides[3] = {S, S * M, S * M * KS};
     return encode_map4(map, base, dims, strides, box_rows);
 }
 static bool make_map_plain(CUtensorMap* map, const void* base, uint64_t k, uint64_t rows, uint64_t pitch,
@@ -583,6 +585,13 @@ static bool make_map_plain(CUtensorMap* map, const void* base, uint64_t k, uint6
     const cuuint64_t dims[4] = {k, 1, 1, rows};
     const cuuint64_t strides[3] = {pitch, pitch, pitch};
     return encode_map4(map, base, dims, strides, box_rows);
+}
+
+static int super_shift_of(int64_t k_pad) {   // log2(S / BK) of the digit-plane layout
+    if (super_bytes(k_pad) != kSuper) return 30;   // one super-chunk per row (S = k_pad)
+    int s = 0;
+    while ((BK << (s + 1)) <= kSuper) ++s;
+    return s;
 }
 
 static int sync_lead() {   // progress throttle of the residue GEMM (OZ2_TUNE_SYNC_LEAD)
@@ -684,8 +693,8 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
     auto* res = reinterpret_cast<int16_t*>(ws + L.res);
     uint8_t* abar = ws + L.abar;     // unblocked: the first digit plane, dead after step 3
     uint8_t* bbar = ws + L.bbar;
-    // A-bar / B-bar use the interleaved digit-plane layout with `gplanes` planes per chunk
-    // group: M when they live in plane 0 of the digit buffers, 1 in their own buffers
+    // A-bar / B-bar use the digit-plane layout with `gplanes` planes per super-chunk group:
+    // M when they live in plane 0 of the digit buffers, 1 in their own buffers
     const int gplanes = L.blocked ? 1 : pl->M;
     int32_t* e_mu = eexp;
     int32_t* e_nu = eexp + m;
@@ -698,13 +707,26 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
         // ---- step 1: prescale (eq. def:mu'nu')
         OZ2_CK(cudaMemsetAsync(maxbits, 0, 8 * static_cast<size_t>(m + n), st));
         OZ2_CK(cudaMemsetAsync(rsmax, 0, 4 * static_cast<size_t>(m + n), st));
-        OZ2_CK(launch_rowmax(A, m, k, lda, a_kmajor, maxbits, st));
-        OZ2_CK(launch_rowmax(B, n, k, ldb, b_kmajor, maxbits + m, st));
-        if (fast) OZ2_CK(cudaMemsetAsync(sumsq, 0, 8 * static_cast<size_t>(m + n), st));
-        OZ2_CK(launch_cast(A, m, k, lda, a_kmajor, maxbits, eprime, abar, gplanes, L.m_pad, L.k_pad, D().d_status,
-                           fast ? sumsq : nullptr, i8, st));
-        OZ2_CK(launch_cast(B, n, k, ldb, b_kmajor, maxbits + m, eprime + m, bbar, gplanes, L.n_pad, L.k_pad, D().d_status,
-                           fast ? sumsq + m : nullptr, i8, st));
+        if (fast || tune(OZ2_TUNE_PRESCALE_2READ)) {
+            // row maxima, then the cast (fast mode: sums of squares instead of A-bar)
+            OZ2_CK(launch_rowmax(A, m, k, lda, a_kmajor, maxbits, st));
+            OZ2_CK(launch_rowmax(B, n, k, ldb, b_kmajor, maxbits + m, st));
+            if (fast) OZ2_CK(cudaMemsetAsync(sumsq, 0, 8 * static_cast<size_t>(m + n), st));
+            OZ2_CK(launch_cast(A, m, k, lda, a_kmajor, maxbits, eprime, abar, gplanes, L.m_pad, L.k_pad,
+                               D().d_status, fast ? sumsq : nullptr, i8, st));
+            OZ2_CK(launch_cast(B, n, k, ldb, b_kmajor, maxbits + m, eprime + m, bbar, gplanes, L.n_pad, L.k_pad,
+                               D().d_status, fast ? sumsq + m : nullptr, i8, st));
+        } else {
+            // one read of A and B: chunk-local casts, then the rescale to the row exponent
+            auto* eloc = reinterpret_cast<int16_t*>(ws + L.eloc);
+            const int64_t kc = (k + BK - 1) / BK;
+            OZ2_CK(launch_cast_local(A, m, k, lda, a_kmajor, maxbits, eloc, abar, gplanes, L.m_pad, L.k_pad, i8, st));
+            OZ2_CK(launch_cast_local(B, n, k, ldb, b_kmajor, maxbits + m, eloc + m * kc, bbar, gplanes, L.n_pad,
+                                     L.k_pad, i8, st));
+            OZ2_CK(launch_rescale(m, k, maxbits, eloc, eprime, D().d_status, abar, gplanes, L.k_pad, i8, st));
+            OZ2_CK(launch_rescale(n, k, maxbits + m, eloc + m * kc, eprime + m, D().d_status, bbar, gplanes,
+                                  L.k_pad, i8, st));
+        }
         if (opt && opt->e_prime_a) OZ2_CK(cudaMemcpyAsync(opt->e_prime_a, eprime, 4 * m, cudaMemcpyDeviceToDevice, st));
         if (opt && opt->e_prime_b) OZ2_CK(cudaMemcpyAsync(opt->e_prime_b, eprime + m, 4 * n, cudaMemcpyDeviceToDevice, st));
         if (opt && opt->abar && k && !fast)
@@ -721,7 +743,8 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             GemmParams gp;
             std::memset(&gp, 0, sizeof(gp));
             gp.m = static_cast<int>(m); gp.n = static_cast<int>(n);
-            gp.num_k_blocks = static_cast<int>(L.k_pad / BK);
+            gp.num_k_blocks = static_cast<int>((k + BK - 1) / BK);   // not the layout's padding
+            gp.super_shift = super_shift_of(L.k_pad);
             gp.m_tiles = static_cast<int>(L.m_pad / tile_m(cg)); gp.n_tiles = static_cast<int>(L.n_pad / BN);
             gp.rmax = rsmax; gp.smax = rsmax + m;
             OZ2_CK(launch_gemm(i8 ? MODE_BOUND_I8 : MODE_BOUND, cg, 0, ta, tb, gp, D().num_sms, st));
@@ -798,7 +821,8 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             gp.prods_per_tile = 0;
             for (int l = 0; l < N; ++l) gp.prods_per_tile += gp.mod[l].nprod;
             gp.m = static_cast<int>(mbi); gp.n = static_cast<int>(nbj);
-            gp.num_k_blocks = static_cast<int>(L.k_pad / BK);
+            gp.num_k_blocks = static_cast<int>((k + BK - 1) / BK);   // not the layout's padding
+            gp.super_shift = super_shift_of(L.k_pad);
             gp.kseg_blocks = kMaxK / BK;                                  // 2^16 per segment
             gp.num_kseg = (gp.num_k_blocks + gp.kseg_blocks - 1) / gp.kseg_blocks;
             gp.m_tiles = static_cast<int>(mbi_pad / tile_m(cg)); gp.n_tiles = static_cast<int>(nbj_pad / BN);
@@ -824,6 +848,7 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             gp.residues = res;
             gp.sync_lead = sync_lead();
             gp.sync_chunk = sync_chunk;
+            gp.epi_sleep_ns = static_cast<unsigned>(tune(OZ2_TUNE_EPI_SLEEP));
             gp.max_units = tune(OZ2_TUNE_MAX_UNITS);
             {   // OZ2_TUNE_TMA_HINT_A / _B: 0 evict-normal (default), 1 evict-last, 2 evict-first
                 auto hint = [](int v) -> unsigned long long {
@@ -1137,8 +1162,10 @@ int oz2_set_tuning(int knob, int value) {
         case OZ2_TUNE_FUSED_CRT: ok = value >= -1 && value <= 1; break;
         case OZ2_TUNE_SQ_ORDER:
         case OZ2_TUNE_CRT_GENERIC:
-        case OZ2_TUNE_KCAT: ok = value == 0 || value == 1; break;
+        case OZ2_TUNE_KCAT:
+        case OZ2_TUNE_PRESCALE_2READ: ok = value == 0 || value == 1; break;
         case OZ2_TUNE_HOST_BLOCKS: ok = value >= 1 && value <= 64; break;
+        case OZ2_TUNE_EPI_SLEEP: ok = value >= 0 && value <= 100000; break;
         default: break;
     }
     if (!ok) return -2;
@@ -1186,7 +1213,15 @@ int oz2_plan_query(int num_moduli, int64_t k, oz2_plan_info* out) {
 
 const char* oz2_version(void) { return "oz2 0.1.0 sm_100a"; }
 
-static int gemm_raw(int mode, const uint8_t* a, const uint8_t* b, float* C32, int64_t m, int64_t n, int64_t k);
+static int gemm_raw(int mode, const uint8_t* a, const uint8_t* b, float* C32, int64_t m, int64_t n, int64_t k,
+                    uint32_t* rmax = nullptr, uint32_t* smax = nullptr);
+
+int oz2_fp8_gemm_bound(const uint8_t* a, const uint8_t* b, uint32_t* rmax, uint32_t* smax, int64_t m, int64_t n,
+                       int64_t k) {
+    if (!rmax && m > 0) return -3;
+    if (!smax && n > 0) return -4;
+    return gemm_raw(MODE_BOUND, a, b, nullptr, m, n, k, rmax, smax);
+}
 
 int oz2_fp8_gemm_raw(const uint8_t* a, const uint8_t* b, float* C32, int64_t m, int64_t n, int64_t k) {
     return gemm_raw(MODE_RAW, a, b, C32, m, n, k);
@@ -1197,14 +1232,18 @@ int oz2_int8_gemm_raw(const int8_t* a, const int8_t* b, int32_t* C32, int64_t m,
                     reinterpret_cast<float*>(C32), m, n, k);
 }
 
-static int gemm_raw(int mode, const uint8_t* a, const uint8_t* b, float* C32, int64_t m, int64_t n, int64_t k) {
+static int gemm_raw(int mode, const uint8_t* a, const uint8_t* b, float* C32, int64_t m, int64_t n, int64_t k,
+                    uint32_t* rmax, uint32_t* smax) {
     if (m < 0) return -4;
     if (n < 0) return -5;
     if (k < 0 || (k % 16) != 0) return -6;
     if (m == 0 || n == 0) return OZ2_SUCCESS;
     int e = ensure_device();
     if (e) return e;
-    if (k == 0) { OZ2_CK(cudaMemsetAsync(C32, 0, 4ull * m * n, g_ts.stream)); return OZ2_SUCCESS; }
+    if (k == 0) {
+        if (C32) OZ2_CK(cudaMemsetAsync(C32, 0, 4ull * m * n, g_ts.stream));
+        return OZ2_SUCCESS;
+    }
     if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15u) return OZ2_ERR_NOT_SUPPORTED;
     const int cg = cta_group(((n + BN - 1) / BN) * BN, mode == MODE_RAW_I8);
     CUtensorMap ta, tb;
@@ -1216,7 +1255,9 @@ static int gemm_raw(int mode, const uint8_t* a, const uint8_t* b, float* C32, in
     gp.num_k_blocks = static_cast<int>((k + BK - 1) / BK);
     gp.m_tiles = static_cast<int>((m + tile_m(cg) - 1) / tile_m(cg)); gp.n_tiles = static_cast<int>((n + BN - 1) / BN);
     gp.c32 = C32;
-    gp.plain_k = 1;
+    gp.rmax = rmax;
+    gp.smax = smax;
+    gp.super_shift = 30;           // plain [rows][k] operands
     OZ2_CK(launch_gemm(mode, cg, 0, ta, tb, gp, D().num_sms, g_ts.stream));
     return OZ2_SUCCESS;
 }

@@ -30,6 +30,19 @@ constexpr int GEMM_THREADS = 320;       // warp0 TMA, warp1 MMA, warps 2..9 epil
 constexpr int PAD_M = 256;       // row padding of operand planes (tile multiple)
 constexpr int PAD_N = 256;
 constexpr int PAD_K = 128;
+// Digit-plane layout: the K extent of every plane is cut into super-chunks
+// of kSuper bytes; byte (plane x, row r, k index h) lives at
+//   ((r KS + h / S) M + x) S + h mod S,   S = super_bytes(k_pad), KS = k_pad / S,
+// i.e. for one row and one super-chunk the S-byte runs of all M planes are adjacent.  Each
+// plane keeps S contiguous bytes of K per row (DRAM page / L2-promotion locality for the
+// GEMM's TMA loads: 128-byte runs cost 6 % of residue-GEMM time, measured), and a digit
+// kernel thread stores its planes at compile-time offsets x S from one address.
+constexpr int kSuper = 2048;
+__host__ __device__ inline int64_t pad_k(int64_t k) {          // k_pad: 128 multiple up to kSuper, then kSuper multiple
+    const int64_t k128 = (k + PAD_K - 1) / PAD_K * PAD_K;
+    return k128 <= kSuper ? k128 : (k + kSuper - 1) / kSuper * kSuper;
+}
+__host__ __device__ inline int64_t super_bytes(int64_t k_pad) { return k_pad < kSuper ? k_pad : kSuper; }
 
 // FP8 (kind::f8f6f4, E4M3 -> FP32) modes, and the same three on the INT8 tensor path
 // (kind::i8, S8/U8 -> S32) of the INT8 Ozaki-II scheme (NEXT-3): MODE_X_I8 = MODE_X + 3
@@ -70,8 +83,9 @@ struct GemmParams {
     int num_kseg;                // residue mode: K segments of <= kseg_blocks k-blocks
     int kseg_blocks;             // 512 (= 2^16 / BK): FP32 exactness window per segment
     int m_tiles, n_tiles;
-    int plain_k;                 // 1: operands are plain [rows][k] matrices (raw GEMM);
-                                 // 0: interleaved digit planes
+    int super_shift;             // log2(S / BK): k-block kb sits in super-chunk kb >> shift at
+                                 // byte (kb mod 2^shift) BK (digit planes);
+                                 // 30 for a plain [rows][k] matrix (raw GEMM)
     int num_moduli;
     int tail_head;               // residue mode: tiles [0, head) tile-major, the rest as
                                  // (tile, modulus) items (no fused CRT unless head = all tiles)
@@ -92,6 +106,7 @@ struct GemmParams {
     int sync_chunk;              // k-blocks per throttle chunk (0 = one chunk per product)
     int prods_per_tile;          // residue mode: sum of mod[l].nprod (accumulator drains per tile)
     int max_units;               // host only: cap on persistent units (0 = all)
+    unsigned epi_sleep_ns;       // residue mode: epilogue poll interval while an accumulator fills
     ModEpi mod[kMaxModuli];
 };
 
@@ -141,6 +156,13 @@ cudaError_t launch_cast(const double* X, int64_t rows, int64_t k, int64_t ld, bo
                         const unsigned long long* maxbits, int32_t* eprime, uint8_t* xbar, int gplanes,
                         int64_t rows_pad, int64_t k_pad, int32_t* status,
                         unsigned long long* sumsq, bool i8, cudaStream_t st);
+// one-read prescale (accurate mode): chunk-local casts + rescale to the row exponent
+cudaError_t launch_cast_local(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
+                              unsigned long long* maxbits, int16_t* eloc, uint8_t* xbar, int gplanes,
+                              int64_t rows_pad, int64_t k_pad, bool i8, cudaStream_t st);
+cudaError_t launch_rescale(int64_t rows, int64_t k, const unsigned long long* maxbits, const int16_t* eloc,
+                           int32_t* eprime, int32_t* status, uint8_t* xbar, int gplanes, int64_t k_pad, bool i8,
+                           cudaStream_t st);
 cudaError_t launch_exps_fast(const unsigned long long* maxbits, const int32_t* eprime,
                              const unsigned long long* sumsq, const uint32_t* u32, int64_t count,
                              FastExpParams fp, int ushift, int32_t* e_out, cudaStream_t st);
@@ -150,7 +172,7 @@ cudaError_t launch_exps(const unsigned long long* maxbits, const int32_t* eprime
 cudaError_t launch_digits(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
                           const int32_t* e, const DigitParams& dp, uint8_t* planes,
                           int64_t rows_pad, int64_t k_pad, cudaStream_t st);
-// plane x of the interleaved layout (gplanes planes per chunk group) -> dst [rows][k]
+// plane x of the digit-plane layout (gplanes planes per super-chunk group) -> dst [rows][k]
 cudaError_t launch_unpack_plane(uint8_t* dst, const uint8_t* src, int gplanes, int x, int64_t rows, int64_t k,
                                 int64_t k_pad, cudaStream_t st);
 cudaError_t launch_gemm(int mode, int cg, int fused_limbs, const CUtensorMap& ta, const CUtensorMap& tb,

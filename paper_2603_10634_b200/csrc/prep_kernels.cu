@@ -8,11 +8,11 @@
 // An operand is seen as `rows` rows of length k (A: rows = i; B: rows = j of B^T).
 // Element (r, h) lives at X[r + h*ld] (MN-major: A with transa='N', B with 'T') or
 // X[h + r*ld] (K-major: A 'T', B 'N').  Outputs are K-major byte planes in the
-// interleaved layout: byte (plane x, row r, k index h) at
-// ((r KB + h/128) M + x) 128 + h mod 128, KB = k_pad/128, M planes per group -- for each
-// row and 128-wide K chunk the chunks of all M planes are adjacent, so a thread's stores to
-// the planes of one modulus differ by compile-time multiples of 128 bytes.  Zero in the
-// padding.
+// super-chunk layout (oz2_internal.h): byte (plane x, row r, k index h) at
+// ((r KS + h/S) M + x) S + h mod S, S = super_bytes(k_pad), KS = k_pad/S, M planes per
+// group -- for each row and S-wide K super-chunk the runs of all M planes are adjacent, so
+// (S = kSuper) a thread's stores to its planes differ by compile-time multiples of S bytes.
+// Zero in the padding.
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "oz2_internal.h"
@@ -128,6 +128,14 @@ __device__ __forceinline__ void load_tile(const double* __restrict__ X, int64_t 
     }
 }
 
+// byte offset of (row r, 128-byte chunk c) in the super-chunk layout with `gplanes` planes
+// per group (plane 0); S = kSuper (16 chunks per super-chunk) or S = k_pad (one super-chunk)
+__device__ __forceinline__ int64_t chunk_offset(int64_t r, uint32_t c, int gplanes, int64_t k_pad) {
+    if (k_pad >= kSuper)
+        return (r * (k_pad / kSuper) + (c >> 4)) * gplanes * kSuper + (c & 15u) * TH;
+    return r * gplanes * k_pad + c * TH;
+}
+
 __device__ __forceinline__ double pow2d(int e) {          // 2^e, |e| <= 1022
     return __longlong_as_double(static_cast<long long>(e + 1023) << 52);
 }
@@ -150,7 +158,8 @@ template <bool KMAJOR, bool FAST, bool I8>
 __global__ void __launch_bounds__(256) k_cast(const double* __restrict__ X, int64_t rows, int64_t k,
                                               int64_t ld, const unsigned long long* __restrict__ maxbits,
                                               int32_t* __restrict__ eprime, uint8_t* __restrict__ xbar,
-                                              int gplanes, int64_t k_pad, int32_t* __restrict__ status,
+                                              int gplanes, int64_t k_pad,
+                                              int32_t* __restrict__ status,
                                               unsigned long long* __restrict__ sumsq) {
     __shared__ double tile[TR * TP];
     const int64_t h0 = static_cast<int64_t>(blockIdx.x) * TH;
@@ -210,10 +219,145 @@ __global__ void __launch_bounds__(256) k_cast(const double* __restrict__ X, int6
             for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
             if (lane == 0 && sq && r < rows) atomicAdd(sumsq + r, sq);
         } else {
-            *reinterpret_cast<uint32_t*>(xbar + ((r * (k_pad / TH) + blockIdx.x) * gplanes) * TH + lane * 4) = word;
+            *reinterpret_cast<uint32_t*>(xbar + chunk_offset(r, blockIdx.x, gplanes, k_pad) + lane * 4) = word;
         }
     }
 }
+
+// ---------------------------------------------------------------------------------
+// One-read prescale (accurate mode): step 1 needs the row maximum before it can cast, so
+// the plain form reads X twice (k_rowmax, then k_cast).  Here X is read once:
+//   k_cast_local  casts every 128-wide chunk of a row with the chunk's own exponent
+//                 e_loc = 7 - floor(log2 max_chunk|x|) >= e' (codes RU_e4m3(|x| 2^e_loc)),
+//                 records e_loc and merges the chunk maximum into the row maximum;
+//   k_rescale     then moves each chunk to the row exponent: code <- RU_e4m3(v 2^-d),
+//                 d = e_loc - e' >= 0, touching only chunks with d > 0.
+// Exact: both roundings are upward and the row-scale E4M3 grid {i 2^q : i < 16, q >= -9}
+// is a subset of the chunk grid scaled by 2^-d ({i 2^q : q >= -9-d}) wherever the values
+// live (< 2^(8-d)), so RU_row(RU_chunk(y)) = RU_row(y) -- the same A-bar as k_cast,
+// bit for bit (tests).  INT8 (R16): ceil(ceil(y) / 2^d) = ceil(y / 2^d).
+constexpr int16_t kZeroChunk = 32767;      // e_loc of an all-zero chunk (nothing to rescale)
+
+template <bool KMAJOR, bool I8>
+__global__ void __launch_bounds__(256) k_cast_local(const double* __restrict__ X, int64_t rows, int64_t k,
+                                                    int64_t ld, unsigned long long* __restrict__ maxbits,
+                                                    int16_t* __restrict__ eloc, int64_t kc,
+                                                    uint8_t* __restrict__ xbar, int gplanes, int64_t k_pad) {
+    __shared__ double tile[TR * TP];
+    const int64_t h0 = static_cast<int64_t>(blockIdx.x) * TH;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.y) * TR;
+    load_tile<KMAJOR>(X, rows, k, ld, r0, h0, tile);
+    __syncthreads();
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+#pragma unroll
+    for (int j = 0; j < TR / 8; ++j) {
+        const int rr = w + 8 * j;
+        const int64_t r = r0 + rr;
+        double x[4];
+        unsigned long long mx = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            x[q] = tile[rr * TP + lane * 4 + q];
+            const unsigned long long b = __double_as_longlong(fabs(x[q]));
+            mx = b > mx ? b : mx;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long v = __shfl_xor_sync(0xffffffffu, mx, o);
+            mx = v > mx ? v : mx;
+        }
+        const int e = eprime_of<I8>(mx);
+        if (lane == 0 && r < rows) {
+            if (mx) atomicMax(maxbits + r, mx);
+            eloc[r * kc + blockIdx.x] = mx ? static_cast<int16_t>(e) : kZeroChunk;
+        }
+        const double s1 = pow2d(e >> 1), s2 = pow2d(e - (e >> 1));
+        uint32_t word = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t c = 0;
+            if (x[q] != 0.0 && mx < 0x7FF0000000000000ull) {
+                if (I8) {
+                    c = static_cast<uint32_t>(ceil((fabs(x[q]) * s1) * s2));
+                } else {
+                    const uint32_t hx = static_cast<uint32_t>(__double2hiint(x[q])) & 0x7FFFFFFFu;
+                    const uint32_t lx = static_cast<uint32_t>(__double2loint(x[q]));
+                    const int ey = static_cast<int>(hx >> 20) + e;
+                    if ((hx >> 20) != 0u && ey >= 1017) {
+                        const uint32_t hy = hx + (static_cast<uint32_t>(e) << 20);
+                        const uint32_t sticky = ((hy & 0x1FFFFu) | lx) != 0u ? 0x20000u : 0u;
+                        c = (((hy & ~0x1FFFFu) + sticky) >> 17) - 8128u;
+                    } else {
+                        c = fp8_ru_code((fabs(x[q]) * s1) * s2);
+                        c = c ? c : 1u;
+                    }
+                }
+            }
+            word |= c << (8 * q);
+        }
+        // padding rows too (zero codes): the buffer is reused across calls
+        *reinterpret_cast<uint32_t*>(xbar + chunk_offset(r, blockIdx.x, gplanes, k_pad) + lane * 4) = word;
+    }
+}
+
+// one E4M3 code (non-negative) of value v -> RU_e4m3(v 2^-d), d >= 1
+__device__ __forceinline__ uint32_t fp8_code_shift_ru(uint32_t c, int d) {
+    const uint32_t E = c >> 3, M = c & 7u;
+    if (static_cast<int>(E) > d) return c - (static_cast<uint32_t>(d) << 3);   // stays normal: exact
+    if (c == 0u) return 0u;
+    if (d >= 16) return 1u;                                       // below 2^-9: the smallest subnormal
+    const uint32_t v = E ? (8u + M) << (E - 1u) : M;              // value in units of 2^-9 (< 2^15)
+    return (v + (1u << d) - 1u) >> d;                             // ceil, a subnormal code 1..8
+}
+
+// Warp per row and 32-chunk range (blockIdx.x), 8 rows per block (grid-stride over row
+// groups); each lane moves 16 bytes, so one pass of the warp covers 4 chunks (512 B) and
+// the 8 passes are independent (loads in flight together).  The row's exponent is read once.
+template <bool I8>
+__global__ void __launch_bounds__(256) k_rescale(int64_t rows, const unsigned long long* __restrict__ maxbits,
+                                                 const int16_t* __restrict__ eloc, int64_t kc,
+                                                 int32_t* __restrict__ eprime, int32_t* __restrict__ status,
+                                                 uint8_t* __restrict__ xbar, int gplanes, int64_t k_pad) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t c0 = blockIdx.x * 32u;
+    for (int64_t r = static_cast<int64_t>(blockIdx.y) * 8 + (threadIdx.x >> 5); r < rows;
+         r += static_cast<int64_t>(gridDim.y) * 8) {
+        const unsigned long long mb = maxbits[r];
+        const int ep = eprime_of<I8>(mb);
+        const bool bad = mb >= 0x7FF0000000000000ull;             // NaN / Inf row: zero bounds (R12)
+        if (c0 == 0 && lane == 0) {
+            eprime[r] = ep;
+            if (bad) atomicOr(status, 1);
+        }
+#pragma unroll 4
+        for (int it = 0; it < 8; ++it) {
+            const uint32_t c = c0 + it * 4 + (lane >> 3);
+            if (c >= kc) break;
+            const int el = eloc[r * kc + c];
+            if (el == kZeroChunk) continue;                       // zero chunk: codes are 0 already
+            const int d = el - ep;
+            if (d == 0 && !bad) continue;
+            uint4* p = reinterpret_cast<uint4*>(xbar + chunk_offset(r, c, gplanes, k_pad) + (lane & 7) * 16);
+            if (bad) { *p = make_uint4(0u, 0u, 0u, 0u); continue; }
+            uint4 w = *p;
+            uint32_t* wv = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                uint32_t o = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t b = (wv[t] >> (8 * q)) & 0xFFu;
+                    const uint32_t nb = I8 ? (d >= 8 ? (b ? 1u : 0u) : (b + (1u << d) - 1u) >> d)
+                                           : fp8_code_shift_ru(b, d);
+                    o |= nb << (8 * q);
+                }
+                wv[t] = o;
+            }
+            *p = w;
+        }
+    }
+}
+
 
 // ---------------------------------------------------------------------------------
 // k_exps: scaling exponents from the bound maxima (eq. mu-computation)
@@ -293,7 +437,6 @@ __device__ __forceinline__ double dfma_rn(double a, double b, double c) {   // k
 // digit plane (kEPL = 8 -- one 8-byte store per plane -- was measured: 4 % fewer
 // instructions but 17 % slower for the MN-major operand, 78 vs 50 registers)
 constexpr int kEPL = 4;
-constexpr int kPlanePitch = TH;  // bytes between the same chunk of consecutive planes
 using DWord = uint32_t;          // kEPL bytes of one digit plane
 static_assert(sizeof(DWord) == kEPL && TH % kEPL == 0 && 32 % (TH / kEPL) == 0, "k_digits lane map");
 
@@ -305,13 +448,13 @@ static_assert(sizeof(DWord) == kEPL && TH % kEPL == 0 && 32 % (TH / kEPL) == 0, 
 // SQ: 1 square, 0 non-square, -1 read md.square at run time, 2 INT8 scheme (the residue
 // itself, as a two's-complement byte, is the single operand plane of the modulus)
 template <int SQ>
-__device__ __forceinline__ void emit_digits(const ModDig& md, const float (&rf)[kEPL], uint8_t* o);
+__device__ __forceinline__ void emit_digits(const ModDig& md, const float (&rf)[kEPL], uint8_t* o, int pitch);
 
 template <int NSTEP, int SQ>
 __device__ __forceinline__ void digits_one_modulus(const ModDig& md, int l, int plane0, const double (&y)[kEPL],
                                                    const double (&M)[kEPL], const int (&E)[kEPL],
                                                    const uint16_t* __restrict__ pow2tab,
-                                                   uint8_t* out) {
+                                                   uint8_t* out, int pitch) {
     const double pinv = md.pinv_d, pd = md.p_d, magic = kMagic52;
     float rf[kEPL];
 #pragma unroll
@@ -354,13 +497,13 @@ __device__ __forceinline__ void digits_one_modulus(const ModDig& md, int l, int 
             rf[q + 1] = rs.y;
         }
     }
-    emit_digits<SQ>(md, rf, out + plane0 * kPlanePitch);
+    emit_digits<SQ>(md, rf, out + plane0 * pitch, pitch);
 }
 
 // the digit planes (or the INT8 residue plane) of one modulus from the exact symmetric
-// residues rf[kEPL] of the lane's kEPL consecutive elements
+// residues rf[kEPL] of the lane's kEPL consecutive elements; `pitch` = bytes between planes
 template <int SQ>
-__device__ __forceinline__ void emit_digits(const ModDig& md, const float (&rf)[kEPL], uint8_t* o) {
+__device__ __forceinline__ void emit_digits(const ModDig& md, const float (&rf)[kEPL], uint8_t* o, int pitch) {
     if (SQ == 2) {
         DWord w = 0;
 #pragma unroll
@@ -386,7 +529,7 @@ __device__ __forceinline__ void emit_digits(const ModDig& md, const float (&rf)[
             w2 |= static_cast<DWord>(cvt_e4m3x2(d2.x, d2.y)) << (8 * q);
         }
         *reinterpret_cast<DWord*>(o) = w1;
-        *reinterpret_cast<DWord*>(o + kPlanePitch) = w2;
+        *reinterpret_cast<DWord*>(o + pitch) = w2;
     } else {
         // D1 = sign(r) ceil(|r|/16), D2 = r - 16 D1, D3 = D1 + D2
         const float2 s16 = make_float2(0.0625f, 0.0625f), n16 = make_float2(-16.0f, -16.0f);
@@ -404,40 +547,40 @@ __device__ __forceinline__ void emit_digits(const ModDig& md, const float (&rf)[
             w3 |= static_cast<DWord>(cvt_e4m3x2(d3.x, d3.y)) << (8 * q);
         }
         *reinterpret_cast<DWord*>(o) = w1;
-        *reinterpret_cast<DWord*>(o + kPlanePitch) = w2;
-        *reinterpret_cast<DWord*>(o + 2 * kPlanePitch) = w3;
+        *reinterpret_cast<DWord*>(o + pitch) = w2;
+        *reinterpret_cast<DWord*>(o + 2 * pitch) = w3;
     }
 }
 
 template <int NSTEP, int NMOD, bool I8, int NSQ>
 __device__ __forceinline__ void digits_all_moduli(const DigitParams& dp, const double (&y)[kEPL],
                                                   const double (&M)[kEPL], const int (&E)[kEPL],
-                                                  uint8_t* out) {
+                                                  uint8_t* out, int pitch) {
     if (I8) {
         // INT8 scheme: one S8 plane per modulus, plane l
         if (NMOD > 0) {
 #pragma unroll
             for (int l = 0; l < NMOD; ++l)
-                digits_one_modulus<NSTEP, 2>(dp.mod[l], l, l, y, M, E, dp.pow2tab, out);
+                digits_one_modulus<NSTEP, 2>(dp.mod[l], l, l, y, M, E, dp.pow2tab, out, pitch);
         } else {
 #pragma unroll 1
             for (int l = 0; l < dp.num_moduli; ++l)
-                digits_one_modulus<NSTEP, 2>(dp.mod[l], l, l, y, M, E, dp.pow2tab, out);
+                digits_one_modulus<NSTEP, 2>(dp.mod[l], l, l, y, M, E, dp.pow2tab, out, pitch);
         }
     } else if (NMOD > 0) {
         // hybrid order (eq. p_list_hybrid): the first min(N, 6) moduli are the squares;
         // Karatsuba family (eq. p_list_karatsuba, NSQ = 0): none
 #pragma unroll
         for (int l = 0; l < NMOD && l < NSQ; ++l)
-            digits_one_modulus<NSTEP, 1>(dp.mod[l], l, 2 * l, y, M, E, dp.pow2tab, out);
+            digits_one_modulus<NSTEP, 1>(dp.mod[l], l, 2 * l, y, M, E, dp.pow2tab, out, pitch);
 #pragma unroll
         for (int l = NSQ; l < NMOD; ++l)
             digits_one_modulus<NSTEP, 0>(dp.mod[l], l, 2 * NSQ + 3 * (l - NSQ), y, M, E,
-                                         dp.pow2tab, out);
+                                         dp.pow2tab, out, pitch);
     } else {
 #pragma unroll 1
         for (int l = 0; l < dp.num_moduli; ++l)
-            digits_one_modulus<NSTEP, -1>(dp.mod[l], l, dp.mod[l].plane0, y, M, E, dp.pow2tab, out);
+            digits_one_modulus<NSTEP, -1>(dp.mod[l], l, dp.mod[l].plane0, y, M, E, dp.pow2tab, out, pitch);
     }
 }
 
@@ -450,7 +593,7 @@ __device__ __forceinline__ void digits_all_moduli(const DigitParams& dp, const d
 // closer than 1/(2p) to a half-integer, so the rounding is exact.  Bit-identical to
 // digits_one_modulus<1, .> (same residues, same digit code).
 template <int NMOD, bool I8, int NSQ, int EVEN>
-__device__ __forceinline__ void digits_paired(const DigitParams& dp, const double (&y)[kEPL], uint8_t* out) {
+__device__ __forceinline__ void digits_paired(const DigitParams& dp, const double (&y)[kEPL], uint8_t* out, int pitch) {
     const float2 M2 = make_float2(kMagic23, kMagic23), nM2 = make_float2(-kMagic23, -kMagic23);
 #pragma unroll
     for (int l = 0; l < NMOD; l += 2) {
@@ -481,17 +624,19 @@ __device__ __forceinline__ void digits_paired(const DigitParams& dp, const doubl
                 rf[q + 1] = sv.y;
             }
             if (I8) {
-                emit_digits<2>(md, rf, out + lm * kPlanePitch);
+                emit_digits<2>(md, rf, out + lm * pitch, pitch);
             } else if (lm < NSQ) {
-                emit_digits<1>(md, rf, out + 2 * lm * kPlanePitch);
+                emit_digits<1>(md, rf, out + 2 * lm * pitch, pitch);
             } else {
-                emit_digits<0>(md, rf, out + (2 * NSQ + 3 * (lm - NSQ)) * kPlanePitch);
+                emit_digits<0>(md, rf, out + (2 * NSQ + 3 * (lm - NSQ)) * pitch, pitch);
             }
         }
     }
 }
 
-template <bool KMAJOR, int NMOD, bool I8, int NSQ>
+// SUP: the super-chunk is kSuper bytes (k_pad >= kSuper), so plane offsets are immediates;
+// otherwise S = k_pad (< kSuper, one super-chunk per row), a run-time pitch.
+template <bool KMAJOR, int NMOD, bool I8, int NSQ, bool SUP>
 __global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, int64_t rows,
                                                 int64_t k, int64_t ld,
                                                 const int32_t* __restrict__ e_scale,
@@ -504,7 +649,11 @@ __global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, in
     load_tile<KMAJOR>(X, rows, k, ld, r0, h0, tile);
     __syncthreads();
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const int64_t group = static_cast<int64_t>(dp.num_planes) * kPlanePitch;   // bytes per (row, chunk)
+    const int pitch = SUP ? kSuper : static_cast<int>(k_pad);                 // S: bytes between planes
+    const int64_t group = static_cast<int64_t>(dp.num_planes) * pitch;       // bytes per (row, super-chunk)
+    constexpr int kCps = kSuper / TH;                                        // chunks per super-chunk (SUP)
+    const int64_t sc = SUP ? blockIdx.x / kCps : 0, within = SUP ? (blockIdx.x % kCps) * TH : blockIdx.x * TH;
+    const int64_t ks = SUP ? k_pad / kSuper : 1;
     // a lane owns kEPL consecutive k of one row: kLPR lanes per row, 32 / kLPR rows per warp
     constexpr int kLPR = TH / kEPL, kRPW = 32 / kLPR;
     const int lrow = lane / kLPR, hl = (lane % kLPR) * kEPL;
@@ -526,8 +675,8 @@ __global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, in
             y[q] = copysign(a, v);
             amax = fmax(amax, a);
         }
-        // plane x of this (row, chunk) at out + x 128: immediate store offsets
-        uint8_t* out = planes + (r * (k_pad / TH) + blockIdx.x) * group + hl;
+        // plane x of this (row, super-chunk) at out + x S: immediate store offsets (SUP)
+        uint8_t* out = planes + (r * ks + sc) * group + within + hl;
         // warp-uniform choice of the reduction depth
         const bool need2 = __any_sync(0xffffffffu, amax >= dp.lim1);   // 2^50 p_min (~2^59 hybrid)
         const bool need0 = __any_sync(0xffffffffu, amax >= dp.lim2);   // 2^86 p_min
@@ -544,13 +693,13 @@ __global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, in
                 M[q] = a;
                 E[q] = ee;
             }
-            digits_all_moduli<0, NMOD, I8, NSQ>(dp, y, M, E, out);
+            digits_all_moduli<0, NMOD, I8, NSQ>(dp, y, M, E, out, pitch);
         } else if (need2) {
-            digits_all_moduli<2, NMOD, I8, NSQ>(dp, y, M, E, out);
+            digits_all_moduli<2, NMOD, I8, NSQ>(dp, y, M, E, out, pitch);
         } else if (NMOD > 0) {
-            digits_paired<NMOD, I8, NSQ, I8 ? 0 : 1>(dp, y, out);   // the even modulus: 256 / 1024 / 512
+            digits_paired<NMOD, I8, NSQ, I8 ? 0 : 1>(dp, y, out, pitch);   // the even modulus: 256 / 1024 / 512
         } else {
-            digits_all_moduli<1, NMOD, I8, NSQ>(dp, y, M, E, out);
+            digits_all_moduli<1, NMOD, I8, NSQ>(dp, y, M, E, out, pitch);
         }
     }
 }
@@ -562,14 +711,14 @@ __global__ void k_scale(double* C, int64_t m, int64_t n, int64_t ldc, double bet
     }
 }
 
-// plane x of the interleaved layout -> [rows][k] (debug outputs of oz2_dgemm_ex only)
+// plane x of the super-chunk layout -> [rows][k] (debug outputs of oz2_dgemm_ex only)
 __global__ void k_unpack_plane(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, int gplanes, int x,
                                int64_t rows, int64_t k, int64_t k_pad) {
-    const int64_t kb = k_pad / TH;
+    const int64_t S = super_bytes(k_pad), ks = k_pad / S;
     for (int64_t r = blockIdx.y; r < rows; r += gridDim.y)
         for (int64_t h = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; h < k;
              h += static_cast<int64_t>(gridDim.x) * blockDim.x)
-            dst[r * k + h] = src[((r * kb + h / TH) * gplanes + x) * TH + h % TH];
+            dst[r * k + h] = src[((r * ks + h / S) * gplanes + x) * S + h % S];
 }
 
 // ---------------------------------------------------------------------------------
@@ -601,7 +750,8 @@ cudaError_t launch_cast(const double* X, int64_t rows, int64_t k, int64_t ld, bo
                         const unsigned long long* maxbits, int32_t* eprime, uint8_t* xbar, int gplanes,
                         int64_t rows_pad, int64_t k_pad, int32_t* status,
                         unsigned long long* sumsq, bool i8, cudaStream_t st) {
-    dim3 grid(static_cast<unsigned>(k_pad / TH), static_cast<unsigned>(rows_pad / TR));
+    // K tiles up to round_up(k, 128): beyond that the layout's padding is never read
+    dim3 grid(static_cast<unsigned>((k + TH - 1) / TH), static_cast<unsigned>(rows_pad / TR));
 #define OZ2_CAST(KM, FA, I8_) k_cast<KM, FA, I8_><<<grid, 256, 0, st>>>(X, rows, k, ld, maxbits, eprime, xbar, gplanes, k_pad, status, sumsq)
     const int sel = (kmajor ? 4 : 0) | (sumsq ? 2 : 0) | (i8 ? 1 : 0);
     switch (sel) {
@@ -615,6 +765,30 @@ cudaError_t launch_cast(const double* X, int64_t rows, int64_t k, int64_t ld, bo
         default: OZ2_CAST(true, true, true); break;
     }
 #undef OZ2_CAST
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cast_local(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
+                              unsigned long long* maxbits, int16_t* eloc, uint8_t* xbar, int gplanes,
+                              int64_t rows_pad, int64_t k_pad, bool i8, cudaStream_t st) {
+    if (rows == 0 || k == 0) return cudaSuccess;
+    const int64_t kc = (k + TH - 1) / TH;
+    dim3 grid(static_cast<unsigned>(kc), static_cast<unsigned>(rows_pad / TR));
+#define OZ2_CL(KM, I8_) k_cast_local<KM, I8_><<<grid, 256, 0, st>>>(X, rows, k, ld, maxbits, eloc, kc, xbar, gplanes, k_pad)
+    if (kmajor) { if (i8) OZ2_CL(true, true); else OZ2_CL(true, false); }
+    else { if (i8) OZ2_CL(false, true); else OZ2_CL(false, false); }
+#undef OZ2_CL
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rescale(int64_t rows, int64_t k, const unsigned long long* maxbits, const int16_t* eloc,
+                           int32_t* eprime, int32_t* status, uint8_t* xbar, int gplanes, int64_t k_pad, bool i8,
+                           cudaStream_t st) {
+    if (rows == 0 || k == 0) return cudaSuccess;
+    const int64_t kc = (k + TH - 1) / TH, groups = (rows + 7) / 8;   // 8 rows (warps) per block
+    dim3 grid(static_cast<unsigned>((kc + 31) / 32), static_cast<unsigned>(groups < 65535 ? groups : 65535));
+    if (i8) k_rescale<true><<<grid, 256, 0, st>>>(rows, maxbits, eloc, kc, eprime, status, xbar, gplanes, k_pad);
+    else k_rescale<false><<<grid, 256, 0, st>>>(rows, maxbits, eloc, kc, eprime, status, xbar, gplanes, k_pad);
     return cudaGetLastError();
 }
 
@@ -638,11 +812,19 @@ cudaError_t launch_exps(const unsigned long long* maxbits, const int32_t* eprime
 cudaError_t launch_digits(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
                           const int32_t* e, const DigitParams& dp, uint8_t* planes,
                           int64_t rows_pad, int64_t k_pad, cudaStream_t st) {
-    dim3 grid(static_cast<unsigned>(k_pad / TH), static_cast<unsigned>(rows_pad / TR));
-#define OZ2_DIG(NM, I8_, SQ_)                                                                                      \
-    if (kmajor) k_digits<true, NM, I8_, SQ_><<<grid, 256, 0, st>>>(X, rows, k, ld, e, dp, planes, rows_pad, k_pad); \
-    else k_digits<false, NM, I8_, SQ_><<<grid, 256, 0, st>>>(X, rows, k, ld, e, dp, planes, rows_pad, k_pad);
-    if (dp.even_index != (dp.int8 ? 0 : 1)) {
+    // K tiles up to round_up(k, 128): beyond that the layout's padding is never read
+    dim3 grid(static_cast<unsigned>((k + TH - 1) / TH), static_cast<unsigned>(rows_pad / TR));
+#define OZ2_DIG_S(NM, I8_, SQ_, SUP)                                                                                    \
+    if (kmajor) k_digits<true, NM, I8_, SQ_, SUP><<<grid, 256, 0, st>>>(X, rows, k, ld, e, dp, planes, rows_pad, k_pad); \
+    else k_digits<false, NM, I8_, SQ_, SUP><<<grid, 256, 0, st>>>(X, rows, k, ld, e, dp, planes, rows_pad, k_pad);
+#define OZ2_DIG(NM, I8_, SQ_) OZ2_DIG_S(NM, I8_, SQ_, true)
+    if (super_bytes(k_pad) != kSuper) {
+        // k_pad < kSuper: one super-chunk of k_pad bytes per row, run-time plane pitch (the
+        // generic kernels; short-k conversions are a small part of such a call)
+        if (dp.int8) { OZ2_DIG_S(0, true, 0, false) }
+        else if (dp.num_squares == kNumSquares) { OZ2_DIG_S(0, false, kNumSquares, false) }
+        else { OZ2_DIG_S(0, false, 0, false) }
+    } else if (dp.even_index != (dp.int8 ? 0 : 1)) {
         // generic (never for the planner's families, whose even modulus is 256 / 1024 / 512)
         if (dp.int8) { OZ2_DIG(0, true, 0) } else { OZ2_DIG(0, false, 0) }
     } else if (dp.int8) {
@@ -670,6 +852,7 @@ cudaError_t launch_digits(const double* X, int64_t rows, int64_t k, int64_t ld, 
         OZ2_DIG(0, false, 0)       // generic: reads md.square per modulus
     }
 #undef OZ2_DIG
+#undef OZ2_DIG_S
     return cudaGetLastError();
 }
 

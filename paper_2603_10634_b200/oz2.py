@@ -29,7 +29,8 @@ _MODES = {"accurate": OZ2_MODE_ACCURATE, "fast": OZ2_MODE_FAST}
 TUNE = {
     "cta_group": 0, "sync_lead": 1, "sync_chunk": 2, "l2_promo": 3, "max_units": 4,
     "tma_hint_a": 5, "tma_hint_b": 6, "mod_split": 7, "fused_crt": 8, "sq_order": 9,
-    "crt_generic": 10, "host_blocks": 11, "kcat": 12,
+    "crt_generic": 10, "host_blocks": 11, "kcat": 12, "prescale_2read": 13,
+    "epi_sleep": 14,
 }
 
 _c_int64 = ctypes.c_int64
@@ -94,6 +95,7 @@ SIGNATURES = [
     ("oz2_version", ctypes.c_char_p, []),
     ("oz2_fp8_gemm_raw", ctypes.c_int, [_vp, _vp, _vp, _c_int64, _c_int64, _c_int64]),
     ("oz2_int8_gemm_raw", ctypes.c_int, [_vp, _vp, _vp, _c_int64, _c_int64, _c_int64]),
+    ("oz2_fp8_gemm_bound", ctypes.c_int, [_vp, _vp, _vp, _vp, _c_int64, _c_int64, _c_int64]),
 ]
 
 _lib = None
@@ -271,6 +273,10 @@ def oz2_fp8_gemm_raw(a, b, C32, m, n, k):
 
 def oz2_int8_gemm_raw(a, b, C32, m, n, k):
     return lib().oz2_int8_gemm_raw(a, b, C32, m, n, k)
+
+
+def oz2_fp8_gemm_bound(a, b, rmax, smax, m, n, k):
+    return lib().oz2_fp8_gemm_bound(a, b, rmax, smax, m, n, k)
 
 
 # ---- torch convenience (still only marshalling) ----------------------------------

@@ -100,6 +100,26 @@ def test_fp8_bound_rounding_within_R5(dev):
     assert np.abs(rel).max() < k * 2.0 ** -23
 
 
+def test_fp8_gemm_bound_entry_matches_raw(dev):
+    """oz2_fp8_gemm_bound (step 2's kernel on plain operands): its row / column maxima are
+    exactly the maxima of the raw FP32 accumulator of the same kernel family, ragged sizes."""
+    import torch
+    rng = np.random.default_rng(11)
+    m, n, k = 300, 520, 2048 + 128
+    codes_a = rng.integers(0x01, 0x79, size=(m, k)).astype(np.uint8)
+    codes_b = rng.integers(0x01, 0x79, size=(n, k)).astype(np.uint8)
+    c = _raw(dev, codes_a, codes_b)
+    a = torch.from_numpy(codes_a).cuda()
+    b = torch.from_numpy(codes_b).cuda()
+    rmax = torch.zeros(m, dtype=torch.int32, device="cuda")
+    smax = torch.zeros(n, dtype=torch.int32, device="cuda")
+    assert dev.oz2_fp8_gemm_bound(a.data_ptr(), b.data_ptr(), rmax.data_ptr(), smax.data_ptr(), m, n, k) == 0
+    torch.cuda.synchronize()
+    r = rmax.cpu().numpy().view(np.float32)
+    s = smax.cpu().numpy().view(np.float32)
+    assert np.array_equal(r, c.max(axis=1)) and np.array_equal(s, c.max(axis=0))
+
+
 # ------------------------------------------------------------------ full pipeline parity
 
 def _certified_pairs(Aint, BintT, P, rows, cols):

@@ -1,0 +1,103 @@
+"""Step 1 (prescale, eq. def:mu'nu') through the C ABI: the one-read form
+(chunk-local casts + rescale to the row exponent, the default) against the oracle and
+against the two-read form (row maxima, then the cast; OZ2_TUNE_PRESCALE_2READ = 1), on
+rows whose entries span the whole binary64 range -- so chunk exponents differ from the row
+exponent by 0 .. > 1000, rescaled codes land on every part of the E4M3 grid (normal,
+subnormal, the 2^-9 floor) -- with zero chunks, zero rows, NaN / Inf rows, both storage
+orders, k across the 2048-byte super-chunk boundary, and both FP8 and INT8 schemes."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from oracle import int8 as oint8
+from oracle import scheme
+from synth import gen_host
+
+
+def _wide(rows, k, seed):
+    """Entries (rand - 0.5) 2^t with t uniform in [-60, 60] per element, plus rows with
+    single huge / subnormal outliers and zero stretches longer than a 128-wide chunk."""
+    rng = np.random.default_rng(seed)
+    X = gen_host(rows, k, "uniform", seed=seed) * np.exp2(rng.integers(-60, 61, size=(rows, k)))
+    X[1, :] = 0.0                                   # zero row (R3)
+    X[2, 300:700] = 0.0                             # zero chunks inside a nonzero row
+    X[3, 5] = 2.0 ** 1000                           # one huge entry: every other chunk rescales by ~1000
+    X[4, :] *= 2.0 ** -1000                         # near the subnormal range ...
+    X[4, 7] = 2.0 ** -1070                          # ... and a subnormal
+    X[5, :] = 0.0
+    X[5, k - 1] = -3.0                              # a single nonzero, in the ragged last chunk
+    X[6, ::2] *= 2.0 ** -40                         # alternating magnitudes within each chunk
+    return X
+
+
+def _run(A, B, N, two_read, transa="N", transb="N", scheme_name="fp8"):
+    import paper_2603_10634_b200 as P
+    from gpu_helpers import run
+    assert P.oz2_set_tuning("prescale_2read", 1 if two_read else 0) == 0
+    try:
+        return run(A, B, N, transa=transa, transb=transb, want_residues=False, scheme=scheme_name)
+    finally:
+        P.oz2_reset_tuning()
+
+
+@pytest.mark.parametrize("transa,transb", [("N", "N"), ("T", "T")])
+@pytest.mark.parametrize("k", [2300, 700])
+def test_one_read_prescale_matches_oracle(transa, transb, k):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    m, n = 130, 70
+    A = _wide(m, k, 5)
+    B = _wide(n, k, 6).T.copy()
+    res = _run(A, B, 13, False, transa, transb)
+    epa, abar = scheme.prescale_rows(A)
+    epb, bbar = scheme.prescale_rows(B.T)
+    assert res["e_prime_a"].tolist() == epa and res["e_prime_b"].tolist() == epb
+    assert np.array_equal(res["abar"], abar) and np.array_equal(res["bbar"], bbar)
+    two = _run(A, B, 13, True, transa, transb)
+    for key in ("abar", "bbar", "e_prime_a", "e_prime_b", "rmax", "smax", "e_mu", "e_nu", "C"):
+        assert np.array_equal(res[key], two[key]), key
+
+
+def test_one_read_prescale_int8_matches_oracle():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    m, n, k = 96, 64, 2300
+    A = _wide(m, k, 7)
+    B = _wide(n, k, 8).T.copy()
+    res = _run(A, B, 15, False, scheme_name="int8")
+    epa, abar = oint8.prescale_rows(A)
+    epb, bbar = oint8.prescale_rows(B.T)
+    assert res["e_prime_a"].tolist() == epa and res["e_prime_b"].tolist() == epb
+    assert np.array_equal(res["abar"].astype(np.int64), abar)
+    assert np.array_equal(res["bbar"].astype(np.int64), bbar)
+    two = _run(A, B, 15, True, scheme_name="int8")
+    for key in ("abar", "bbar", "e_mu", "e_nu", "C"):
+        assert np.array_equal(res[key], two[key]), key
+
+
+@pytest.mark.parametrize("sch", ["fp8", "int8"])
+def test_one_read_prescale_nonfinite(sch):
+    """NaN / Inf rows and columns (R12): the same A-bar (zero bounds on those rows), status
+    and C as the two-read form."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    m, n, k = 70, 50, 2300
+    A = _wide(m, k, 9)
+    B = _wide(n, k, 10).T.copy()
+    A[8, 2000] = np.nan
+    A[9, 3] = np.inf
+    B[100, 4] = -np.inf
+    N = 15 if sch == "int8" else 13
+    one = _run(A, B, N, False, scheme_name=sch)
+    two = _run(A, B, N, True, scheme_name=sch)
+    assert one["status"] != 0 and two["status"] != 0
+    for key in ("abar", "bbar", "e_prime_a", "e_prime_b", "e_mu", "e_nu"):
+        assert np.array_equal(one[key], two[key]), key
+    assert np.all(one["abar"][8] == 0) and np.all(one["abar"][9] == 0)
+    assert np.array_equal(np.isnan(one["C"]), np.isnan(two["C"]))
+    fin = ~np.isnan(two["C"])
+    assert np.array_equal(one["C"][fin], two["C"][fin])

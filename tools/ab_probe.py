@@ -35,4 +35,7 @@ for v in vals:
     tot = statistics.median(x["total"] for x in res[v])
     g = statistics.median(x["residue_gemm"] for x in res[v])
     c = statistics.median(x["crt"] for x in res[v])
-    print(f"{var}={v}: total {tot:.3f} ms ({2.0*m*n*k/tot/1e9:.2f} TFLOP/s), residue_gemm {g:.3f}, crt {c:.3f}", flush=True)
+    ps = statistics.median(x["prescale"] for x in res[v])
+    dg = statistics.median(x["digits"] for x in res[v])
+    print(f"{var}={v}: total {tot:.3f} ms ({2.0*m*n*k/tot/1e9:.2f} TFLOP/s), residue_gemm {g:.3f}, "
+          f"prescale {ps:.3f}, digits {dg:.3f}, crt {c:.3f}", flush=True)

@@ -59,6 +59,14 @@ res.append(sustained("cublaslt_fp8_scaled_mm", lambda: torch._scaled_mm(a8, b8.t
 au, bu = a8.view(torch.uint8), b8.view(torch.uint8)
 res.append(sustained("oz2_fp8_gemm_raw_same_data",
                      lambda: P.oz2_fp8_gemm_raw(au.data_ptr(), bu.data_ptr(), c32.data_ptr(), n, n, n), 2.0 * n ** 3))
+# the same tcgen05 pipeline with step 2's near-empty epilogue (row / column maxima only)
+rmax = torch.zeros(n, dtype=torch.int32, device="cuda")
+smax = torch.zeros(n, dtype=torch.int32, device="cuda")
+res.append(sustained("oz2_fp8_gemm_bound_same_data",
+                     lambda: P.oz2_fp8_gemm_bound(au.data_ptr(), bu.data_ptr(), rmax.data_ptr(), smax.data_ptr(),
+                                                  n, n, n), 2.0 * n ** 3))
+res.append(sustained("cublaslt_fp8_scaled_mm_again", lambda: torch._scaled_mm(a8, b8.t(), scale_a=one, scale_b=one,
+                                                                               out_dtype=torch.bfloat16), 2.0 * n ** 3))
 del a8, b8, c32
 torch.cuda.empty_cache()
 A = gen_device(n, n, "phi", phi=1.0, seed=1)
