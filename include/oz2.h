@@ -246,11 +246,14 @@ int oz2_finalize(void);
  *   OZ2_TUNE_KCAT        0    square moduli: accumulate A1B2 + A2B1 in one TMEM
  *                             accumulator (K-concatenated) when k <= 2^15 (two
  *                             accumulator drains instead of three; measured slower)
- *   OZ2_TUNE_PRESCALE_2READ 0 accurate-mode step 1: 0 = one read of A and B (chunk-local
+ *   OZ2_TUNE_PRESCALE_2READ 1 accurate-mode step 1: 0 = one read of A and B (chunk-local
  *                             casts, then a rescale of A-bar/B-bar to the row exponent),
  *                             1 = row maxima then cast (two reads; fast mode always)
  *   OZ2_TUNE_EPI_SLEEP 1000   residue GEMM: ns the epilogue warps sleep between polls of a
  *                             filling accumulator (0 = spin on mbarrier.try_wait)
+ *   OZ2_TUNE_DIGITS_FMA  0    step 4: rows with |X'| < 2^52 (known from step 1's row maxima)
+ *                             scale and truncate with one fma.rz per element (0 = the general
+ *                             two-multiply path for every row)
  *
  * oz2_set_tuning returns -1 for an unknown knob, -2 for a value out of range;
  * oz2_get_tuning writes the current value. */
@@ -269,7 +272,8 @@ int oz2_finalize(void);
 #define OZ2_TUNE_KCAT        12
 #define OZ2_TUNE_PRESCALE_2READ 13
 #define OZ2_TUNE_EPI_SLEEP   14
-#define OZ2_TUNE_COUNT       15
+#define OZ2_TUNE_DIGITS_FMA  15
+#define OZ2_TUNE_COUNT       16
 int oz2_set_tuning(int knob, int value);
 int oz2_get_tuning(int knob, int* value);
 void oz2_reset_tuning(void);
@@ -298,6 +302,11 @@ int oz2_plan_query(int num_moduli, int64_t k, oz2_plan_info* out);
 
 /* "oz2 <version> sm_100a" */
 const char* oz2_version(void);
+
+/* The cudaError_t behind this thread's last OZ2_ERR_CUDA (0 if none yet); its name (e.g.
+ * "cudaErrorLaunchOutOfResources") is copied into name_out (cap bytes, NUL-terminated) when
+ * name_out is not NULL. */
+int oz2_last_cuda_error(char* name_out, int cap);
 
 /* ---- diagnostics ---------------------------------------------------------------- */
 

@@ -152,7 +152,7 @@ __device__ constexpr float2 kNM2 = {-12582912.0f, -12582912.0f};
 __device__ constexpr float2 kNM2b = {-8388608.0f, -8388608.0f};     // -2^23
 
 template <int MODE_, int CG, int FL, int MC>
-__global__ void __maxnreg__(200)   // 320 threads, one CTA per SM (launch_bounds would cap at 168 and spill)
+__global__ void __launch_bounds__(GEMM_THREADS, 1)   // 10 warps: 3 on one SM sub-partition -> <= 168 registers
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
             const __grid_constant__ GemmParams P) {
     // INT8 variants run the same pipeline on kind::i8 (S32 accumulators)
@@ -457,6 +457,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                             tmem_ld_32x32b_x32(taddr + c * 32, v);
                             tmem_ld_wait();
                             if (c == 3) release_slot(slot);   // the whole slot is in registers
+                            const bool chunk_full = row_ok && col0 + c * 32 + 32 <= P.n;
 #pragma unroll
                             for (int j = 0; j < 32; j += 2) {
                                 // packed FP32 pairs; x - p rint(x/p) by the 1.5 2^23 magic-number
@@ -489,14 +490,19 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                                 } else {
                                     // C'_l mod p stored as u in [0, p) (|acc| <= p/2 + 1 here);
                                     // the CRT consumes u directly, the debug output converts
-                                    // it back to the symmetric range (R2)
-#pragma unroll
-                                    for (int u = 0; u < 2; ++u) {
-                                        float r = acc[u];
-                                        if (r < 0.0f) r += p;
-                                        const int jj = c * 32 + j + u;
-                                        if (row_ok && col0 + jj < P.n)       // streamed: read once by the CRT
-                                            __stcs(out + static_cast<int64_t>(jj) * P.m, static_cast<short>(r));
+                                    // it back to the symmetric range (R2).  u + 2^23 holds u in
+                                    // its low bits (no float-to-int conversion).
+                                    const float2 u2 = __fadd2_rn(make_float2(acc[0] < 0.0f ? acc[0] + p : acc[0],
+                                                                             acc[1] < 0.0f ? acc[1] + p : acc[1]),
+                                                                 make_float2(8388608.0f, 8388608.0f));
+                                    const int jj = c * 32 + j;
+                                    int16_t* o = out + static_cast<int64_t>(jj) * P.m;   // streamed: read once by the CRT
+                                    if (chunk_full) {
+                                        __stcs(o, static_cast<short>(__float_as_int(u2.x)));
+                                        __stcs(o + P.m, static_cast<short>(__float_as_int(u2.y)));
+                                    } else if (row_ok) {
+                                        if (col0 + jj < P.n) __stcs(o, static_cast<short>(__float_as_int(u2.x)));
+                                        if (col0 + jj + 1 < P.n) __stcs(o + P.m, static_cast<short>(__float_as_int(u2.y)));
                                     }
                                 }
                             }

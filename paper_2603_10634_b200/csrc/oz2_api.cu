@@ -371,8 +371,9 @@ static const int kTuneDefault[OZ2_TUNE_COUNT] = {
     0,    // CRT_GENERIC
     4,    // HOST_BLOCKS
     0,    // KCAT (no measurable gain at 16384^3: profiles/round2_layout_ab.md)
-    0,    // PRESCALE_2READ
+    1,    // PRESCALE_2READ (one-read measured 0.1-0.4 ms slower in-step: profiles/round2_prescale_ab.md)
     1000, // EPI_SLEEP (ns)
+    0,    // DIGITS_FMA (fewer instructions, but 0.1-0.5 ms slower in-step: profiles/round2_digits_ab.md)
 };
 
 struct ThreadState {
@@ -627,9 +628,16 @@ static int read_timing(float* ms_out, int n) {   // phase times of the last time
     return OZ2_SUCCESS;
 }
 
-#define OZ2_CK(x)                                   \
-    do {                                            \
-        if ((x) != cudaSuccess) return OZ2_ERR_CUDA; \
+// the CUDA error behind the last OZ2_ERR_CUDA of this thread (oz2_last_cuda_error)
+static thread_local int t_last_cuda_error = 0;
+static int cuda_fail(cudaError_t e) {
+    t_last_cuda_error = static_cast<int>(e);
+    return OZ2_ERR_CUDA;
+}
+#define OZ2_CK(x)                                          \
+    do {                                                   \
+        const cudaError_t e_ = (x);                        \
+        if (e_ != cudaSuccess) return cuda_fail(e_);       \
     } while (0)
 
 // =================================================================================
@@ -738,8 +746,8 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
         if (!fast) {
             const int cg = cta_group(L.n_pad, i8);
             CUtensorMap ta, tb;
-            if (!make_map_planes(&ta, abar, gplanes, L.k_pad, L.m_pad, a_box_rows(cg))) return OZ2_ERR_CUDA;
-            if (!make_map_planes(&tb, bbar, gplanes, L.k_pad, L.n_pad, b_box_rows(cg))) return OZ2_ERR_CUDA;
+            if (!make_map_planes(&ta, abar, gplanes, L.k_pad, L.m_pad, a_box_rows(cg))) return cuda_fail(cudaErrorInvalidValue);
+            if (!make_map_planes(&tb, bbar, gplanes, L.k_pad, L.n_pad, b_box_rows(cg))) return cuda_fail(cudaErrorInvalidValue);
             GemmParams gp;
             std::memset(&gp, 0, sizeof(gp));
             gp.m = static_cast<int>(m); gp.n = static_cast<int>(n);
@@ -792,12 +800,16 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
         const int64_t nbj = std::min(L.nb, n - j0), nbj_pad = round_up(nbj, PAD_N);
         const double* Bj = b_kmajor ? B + j0 * ldb : B + j0;
         // ---- step 4: integers, residues, FP8 digits
-        OZ2_CK(launch_digits(Bj, nbj, k, ldb, b_kmajor, e_nu + j0, pl->dig, digB, nbj_pad, L.k_pad, st));
+        // row maxima of step 1 (not computed when the exponents are imported)
+        const unsigned long long* mx = (imported || !tune(OZ2_TUNE_DIGITS_FMA)) ? nullptr : maxbits;
+        OZ2_CK(launch_digits(Bj, nbj, k, ldb, b_kmajor, e_nu + j0, mx ? mx + m + j0 : nullptr, pl->dig, digB,
+                             nbj_pad, L.k_pad, st));
         for (int64_t i0 = 0; i0 < m; i0 += L.mb) {
             const int64_t mbi = std::min(L.mb, m - i0), mbi_pad = round_up(mbi, PAD_M);
             const double* Ai = a_kmajor ? A + i0 * lda : A + i0;
             if (j0 == 0 || L.mb < m)      // one row block: A's digits survive across column blocks
-                OZ2_CK(launch_digits(Ai, mbi, k, lda, a_kmajor, e_mu + i0, pl->dig, digA, mbi_pad, L.k_pad, st));
+                OZ2_CK(launch_digits(Ai, mbi, k, lda, a_kmajor, e_mu + i0, mx ? mx + i0 : nullptr, pl->dig, digA,
+                                     mbi_pad, L.k_pad, st));
             if (!L.blocked) {
                 if (opt && opt->digits_a && k)
                     for (int x = 0; x < pl->M; ++x)
@@ -812,8 +824,8 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             // ---- step 5: 3N exact FP8 GEMMs with the modular epilogue
             const int cg = cta_group(nbj_pad, i8);
             CUtensorMap ta, tb;
-            if (!make_map_planes(&ta, digA, pl->M, L.k_pad, mbi_pad, a_box_rows(cg))) return OZ2_ERR_CUDA;
-            if (!make_map_planes(&tb, digB, pl->M, L.k_pad, nbj_pad, b_box_rows(cg))) return OZ2_ERR_CUDA;
+            if (!make_map_planes(&ta, digA, pl->M, L.k_pad, mbi_pad, a_box_rows(cg))) return cuda_fail(cudaErrorInvalidValue);
+            if (!make_map_planes(&tb, digB, pl->M, L.k_pad, nbj_pad, b_box_rows(cg))) return cuda_fail(cudaErrorInvalidValue);
             // square moduli: A1 B2 + A2 B1 K-concatenated in one accumulator when the sum
             // stays in the FP32 exactness window (k <= 2^15; OZ2_TUNE_KCAT)
             const bool kcat = tune(OZ2_TUNE_KCAT) != 0 && !i8 && pl->nsq > 0 && k <= kMaxK / 2;
@@ -1141,6 +1153,17 @@ int oz2_get_timing(float* ms_out, int n) {
 }
 
 
+int oz2_last_cuda_error(char* name_out, int cap) {
+    const int e = t_last_cuda_error;
+    if (name_out && cap > 0) {
+        const char* nm = cudaGetErrorName(static_cast<cudaError_t>(e));
+        int i = 0;
+        for (; nm && nm[i] && i < cap - 1; ++i) name_out[i] = nm[i];
+        name_out[i] = 0;
+    }
+    return e;
+}
+
 int oz2_finalize(void) {
     if (g_ts.stream) cudaStreamSynchronize(g_ts.stream);
     g_ts.release_all();
@@ -1166,6 +1189,7 @@ int oz2_set_tuning(int knob, int value) {
         case OZ2_TUNE_PRESCALE_2READ: ok = value == 0 || value == 1; break;
         case OZ2_TUNE_HOST_BLOCKS: ok = value >= 1 && value <= 64; break;
         case OZ2_TUNE_EPI_SLEEP: ok = value >= 0 && value <= 100000; break;
+        case OZ2_TUNE_DIGITS_FMA: ok = value == 0 || value == 1; break;
         default: break;
     }
     if (!ok) return -2;
@@ -1247,8 +1271,8 @@ static int gemm_raw(int mode, const uint8_t* a, const uint8_t* b, float* C32, in
     if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15u) return OZ2_ERR_NOT_SUPPORTED;
     const int cg = cta_group(((n + BN - 1) / BN) * BN, mode == MODE_RAW_I8);
     CUtensorMap ta, tb;
-    if (!make_map_plain(&ta, a, k, m, k, a_box_rows(cg))) return OZ2_ERR_CUDA;
-    if (!make_map_plain(&tb, b, k, n, k, b_box_rows(cg))) return OZ2_ERR_CUDA;
+    if (!make_map_plain(&ta, a, k, m, k, a_box_rows(cg))) return cuda_fail(cudaErrorInvalidValue);
+    if (!make_map_plain(&tb, b, k, n, k, b_box_rows(cg))) return cuda_fail(cudaErrorInvalidValue);
     GemmParams gp;
     std::memset(&gp, 0, sizeof(gp));
     gp.m = static_cast<int>(m); gp.n = static_cast<int>(n);

@@ -169,8 +169,9 @@ cudaError_t launch_exps_fast(const unsigned long long* maxbits, const int32_t* e
 cudaError_t launch_exps(const unsigned long long* maxbits, const int32_t* eprime,
                         const uint32_t* rsmax, int64_t count, ExpParams ep, int32_t* e_out,
                         cudaStream_t st);
+// maxbits: step 1's row maxima of |X| (selects the one-FMA fast path per row), or nullptr
 cudaError_t launch_digits(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
-                          const int32_t* e, const DigitParams& dp, uint8_t* planes,
+                          const int32_t* e, const unsigned long long* maxbits, const DigitParams& dp, uint8_t* planes,
                           int64_t rows_pad, int64_t k_pad, cudaStream_t st);
 // plane x of the digit-plane layout (gplanes planes per super-chunk group) -> dst [rows][k]
 cudaError_t launch_unpack_plane(uint8_t* dst, const uint8_t* src, int gplanes, int x, int64_t rows, int64_t k,

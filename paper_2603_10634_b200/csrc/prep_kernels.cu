@@ -261,10 +261,11 @@ __global__ void __launch_bounds__(256) k_cast_local(const double* __restrict__ X
             const unsigned long long b = __double_as_longlong(fabs(x[q]));
             mx = b > mx ? b : mx;
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const unsigned long long v = __shfl_xor_sync(0xffffffffu, mx, o);
-            mx = v > mx ? v : mx;
+        {   // warp max of the 64-bit patterns: high words, then low words among the leaders
+            const uint32_t hi = static_cast<uint32_t>(mx >> 32);
+            const uint32_t hmax = __reduce_max_sync(0xffffffffu, hi);
+            const uint32_t lmax = __reduce_max_sync(0xffffffffu, hi == hmax ? static_cast<uint32_t>(mx) : 0u);
+            mx = (static_cast<unsigned long long>(hmax) << 32) | lmax;
         }
         const int e = eprime_of<I8>(mx);
         if (lane == 0 && r < rows) {
@@ -637,9 +638,10 @@ __device__ __forceinline__ void digits_paired(const DigitParams& dp, const doubl
 // SUP: the super-chunk is kSuper bytes (k_pad >= kSuper), so plane offsets are immediates;
 // otherwise S = k_pad (< kSuper, one super-chunk per row), a run-time pitch.
 template <bool KMAJOR, int NMOD, bool I8, int NSQ, bool SUP>
-__global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, int64_t rows,
+__global__ void __launch_bounds__(256, 6) k_digits(const double* __restrict__ X, int64_t rows,
                                                 int64_t k, int64_t ld,
                                                 const int32_t* __restrict__ e_scale,
+                                                const unsigned long long* __restrict__ maxbits,
                                                 const __grid_constant__ DigitParams dp,
                                                 uint8_t* __restrict__ planes, int64_t rows_pad,
                                                 int64_t k_pad) {
@@ -656,6 +658,7 @@ __global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, in
     const int64_t ks = SUP ? k_pad / kSuper : 1;
     // a lane owns kEPL consecutive k of one row: kLPR lanes per row, 32 / kLPR rows per warp
     constexpr int kLPR = TH / kEPL, kRPW = 32 / kLPR;
+    static_assert(kRPW == 1, "one row per warp: the per-row path choice below is warp-uniform");
     const int lrow = lane / kLPR, hl = (lane % kLPR) * kEPL;
 #pragma unroll 1
     for (int j = 0; j < TR / (8 * kRPW); ++j) {
@@ -663,6 +666,31 @@ __global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, in
         const int64_t r = r0 + rr;
         int e = (r < rows) ? e_scale[r] : 0;
         if (e == kExpNonFinite) e = 0;                    // NaN / Inf row: C gets NaN (R12)
+        // plane x of this (row, super-chunk) at out + x S: immediate store offsets (SUP)
+        uint8_t* out = planes + (r * ks + sc) * group + within + hl;
+        // Common case, decided per row from step 1's row maximum: |X'| < 2^52 and 2^e a
+        // normal double.  Then trunc(x 2^e) is ONE fused multiply-add rounded toward zero,
+        // fma.rz(x, 2^e, +-2^52) - (+-2^52) with the sign of x (|x 2^e| + 2^52 lies in
+        // [2^52, 2^53) where the ulp is 1), and |X'| < 2^52 < lim1 admits the paired residues.
+        {
+            const unsigned long long mb = !maxbits ? ~0ull : (r < rows ? maxbits[r] : 0ull);   // padding rows: zero
+            const bool fast = mb == 0ull || (mb < 0x7FF0000000000000ull && e >= -1022 && e <= 1023 &&
+                                             ilog2_bits(mb) + e <= 51);
+            if (fast && NMOD > 0) {
+                const double sc2 = pow2d(e);
+                double y[kEPL];
+#pragma unroll
+                for (int q = 0; q < kEPL; ++q) {
+                    const double x = tile[rr * TP + hl + q];
+                    const double m52 = __hiloint2double((__double2hiint(x) & 0x80000000) | 0x43300000, 0);
+                    double t;
+                    asm("fma.rz.f64 %0, %1, %2, %3;" : "=d"(t) : "d"(x), "d"(sc2), "d"(m52));
+                    y[q] = t - m52;                                                // exact (eq. def:A')
+                }
+                digits_paired<NMOD, I8, NSQ, I8 ? 0 : 1>(dp, y, out, pitch);
+                continue;
+            }
+        }
         const double s1 = pow2d(e >> 1), s2 = pow2d(e - (e >> 1));
         double y[kEPL], M[kEPL];
         int E[kEPL];
@@ -675,8 +703,6 @@ __global__ void __launch_bounds__(256) k_digits(const double* __restrict__ X, in
             y[q] = copysign(a, v);
             amax = fmax(amax, a);
         }
-        // plane x of this (row, super-chunk) at out + x S: immediate store offsets (SUP)
-        uint8_t* out = planes + (r * ks + sc) * group + within + hl;
         // warp-uniform choice of the reduction depth
         const bool need2 = __any_sync(0xffffffffu, amax >= dp.lim1);   // 2^50 p_min (~2^59 hybrid)
         const bool need0 = __any_sync(0xffffffffu, amax >= dp.lim2);   // 2^86 p_min
@@ -810,13 +836,13 @@ cudaError_t launch_exps(const unsigned long long* maxbits, const int32_t* eprime
 }
 
 cudaError_t launch_digits(const double* X, int64_t rows, int64_t k, int64_t ld, bool kmajor,
-                          const int32_t* e, const DigitParams& dp, uint8_t* planes,
+                          const int32_t* e, const unsigned long long* maxbits, const DigitParams& dp, uint8_t* planes,
                           int64_t rows_pad, int64_t k_pad, cudaStream_t st) {
     // K tiles up to round_up(k, 128): beyond that the layout's padding is never read
     dim3 grid(static_cast<unsigned>((k + TH - 1) / TH), static_cast<unsigned>(rows_pad / TR));
 #define OZ2_DIG_S(NM, I8_, SQ_, SUP)                                                                                    \
-    if (kmajor) k_digits<true, NM, I8_, SQ_, SUP><<<grid, 256, 0, st>>>(X, rows, k, ld, e, dp, planes, rows_pad, k_pad); \
-    else k_digits<false, NM, I8_, SQ_, SUP><<<grid, 256, 0, st>>>(X, rows, k, ld, e, dp, planes, rows_pad, k_pad);
+    if (kmajor) k_digits<true, NM, I8_, SQ_, SUP><<<grid, 256, 0, st>>>(X, rows, k, ld, e, maxbits, dp, planes, rows_pad, k_pad); \
+    else k_digits<false, NM, I8_, SQ_, SUP><<<grid, 256, 0, st>>>(X, rows, k, ld, e, maxbits, dp, planes, rows_pad, k_pad);
 #define OZ2_DIG(NM, I8_, SQ_) OZ2_DIG_S(NM, I8_, SQ_, true)
     if (super_bytes(k_pad) != kSuper) {
         // k_pad < kSuper: one super-chunk of k_pad bytes per row, run-time plane pitch (the

@@ -30,7 +30,7 @@ TUNE = {
     "cta_group": 0, "sync_lead": 1, "sync_chunk": 2, "l2_promo": 3, "max_units": 4,
     "tma_hint_a": 5, "tma_hint_b": 6, "mod_split": 7, "fused_crt": 8, "sq_order": 9,
     "crt_generic": 10, "host_blocks": 11, "kcat": 12, "prescale_2read": 13,
-    "epi_sleep": 14,
+    "epi_sleep": 14, "digits_fma": 15,
 }
 
 _c_int64 = ctypes.c_int64
@@ -96,6 +96,7 @@ SIGNATURES = [
     ("oz2_fp8_gemm_raw", ctypes.c_int, [_vp, _vp, _vp, _c_int64, _c_int64, _c_int64]),
     ("oz2_int8_gemm_raw", ctypes.c_int, [_vp, _vp, _vp, _c_int64, _c_int64, _c_int64]),
     ("oz2_fp8_gemm_bound", ctypes.c_int, [_vp, _vp, _vp, _vp, _c_int64, _c_int64, _c_int64]),
+    ("oz2_last_cuda_error", ctypes.c_int, [ctypes.c_char_p, ctypes.c_int]),
 ]
 
 _lib = None
@@ -273,6 +274,13 @@ def oz2_fp8_gemm_raw(a, b, C32, m, n, k):
 
 def oz2_int8_gemm_raw(a, b, C32, m, n, k):
     return lib().oz2_int8_gemm_raw(a, b, C32, m, n, k)
+
+
+def oz2_last_cuda_error():
+    """(code, name) of the CUDA error behind this thread's last OZ2_ERR_CUDA."""
+    buf = ctypes.create_string_buffer(128)
+    code = lib().oz2_last_cuda_error(buf, 128)
+    return code, buf.value.decode()
 
 
 def oz2_fp8_gemm_bound(a, b, rmax, smax, m, n, k):

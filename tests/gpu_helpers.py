@@ -77,7 +77,7 @@ def run(A, B, N, transa="N", transb="N", alpha=1.0, beta=0.0, C0=None, e_mu_in=N
     finally:
         oz2.oz2_set_mode("accurate")
         oz2.oz2_set_scheme("fp8")
-    assert rc == 0, rc
+    assert rc == 0, (rc, oz2.oz2_last_cuda_error())
     t.cuda.synchronize()
     res = {key: v.cpu().numpy() for key, v in out.items()}
     res["abar"] = res["abar"][: m * k].reshape(m, k)

@@ -101,3 +101,27 @@ def test_one_read_prescale_nonfinite(sch):
     assert np.array_equal(np.isnan(one["C"]), np.isnan(two["C"]))
     fin = ~np.isnan(two["C"])
     assert np.array_equal(one["C"][fin], two["C"][fin])
+
+
+@pytest.mark.parametrize("sch,N", [("fp8", 13), ("int8", 15), ("karatsuba", 13)])
+def test_digits_fma_fast_path_identical(sch, N):
+    """Step 4's one-FMA scale-and-truncate path (OZ2_TUNE_DIGITS_FMA = 1, chosen per row from
+    step 1's row maximum) gives the same digit planes, residues and C as the general path,
+    on rows that take either path (wide exponent spread, huge / subnormal outliers)."""
+    import torch
+    import paper_2603_10634_b200 as P
+    from gpu_helpers import run
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    m, n, k = 100, 90, 2300
+    A = _wide(m, k, 11)
+    B = _wide(n, k, 12).T.copy()
+    outs = []
+    for v in (0, 1):
+        assert P.oz2_set_tuning("digits_fma", v) == 0
+        try:
+            outs.append(run(A, B, N, want_digits=True, scheme=sch))
+        finally:
+            P.oz2_reset_tuning()
+    for key in ("digits_a", "digits_b", "residues", "e_mu", "e_nu", "C"):
+        assert np.array_equal(outs[0][key], outs[1][key]), key

@@ -28,5 +28,7 @@ torch.cuda.synchronize()
 ref = A @ B
 print(f"case m={m} n={n} k={k} N={N} cg={cg} fused={fused} {scheme} {mode}: rc={rc} "
       f"rel={(torch.linalg.norm(C - ref) / torch.linalg.norm(ref)).item():.2e}", flush=True)
+if rc != 0:
+    print("last CUDA error:", P.oz2_last_cuda_error(), flush=True)
 P.oz2_finalize()
 sys.exit(0 if rc == 0 else 1)
