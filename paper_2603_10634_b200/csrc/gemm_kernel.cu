@@ -519,7 +519,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 }
             } else {
                 const uint32_t slot = g & 1u, use = g >> 1;
-                mbar_wait(&tfull[slot], use & 1u);
+                if (P.epi_sleep_ns) mbar_wait_sleep(&tfull[slot], use & 1u, P.epi_sleep_ns);
+                else mbar_wait(&tfull[slot], use & 1u);
                 tc_fence_after();
                 const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + slot * BN + half * 128u;
                 // non-negative FP32 and S32 values both order like their bit patterns

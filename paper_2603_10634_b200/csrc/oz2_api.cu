@@ -474,7 +474,7 @@ struct Layout {
     int64_t m_pad, n_pad, k_pad, mb, nb, mb_pad, nb_pad;
     int M;
     bool blocked;
-    size_t maxbits, eprime, rsmax, sumsq, eexp, eloc, abar, bbar, digA, digB, res, total;
+    size_t maxbits, eprime, rsmax, sumsq, eexp, eloc, prog, abar, bbar, digA, digB, res, total;
 };
 
 static Layout make_layout(int64_t m, int64_t n, int64_t k, int N, int M, int64_t mb = 0, int64_t nb = 0) {
@@ -495,7 +495,8 @@ static Layout make_layout(int64_t m, int64_t n, int64_t k, int N, int M, int64_t
     L.rsmax = off;   off = align_up(off + 4 * mn, 256);
     L.sumsq = off;   off = align_up(off + 8 * mn, 256);
     L.eexp = off;    off = align_up(off + 4 * mn, 256);
-    L.eloc = off;    off = align_up(off + 2 * mn * static_cast<size_t>((k + BK - 1) / BK), 1024);   // chunk exponents
+    L.eloc = off;    off = align_up(off + 2 * mn * static_cast<size_t>((k + BK - 1) / BK), 256);   // chunk exponents
+    L.prog = off;    off = align_up(off + 8, 1024);           // GEMM progress counter (throttle)
     if (L.blocked) {
         L.abar = off; off = align_up(off + static_cast<size_t>(L.m_pad) * L.k_pad, 1024);
         L.bbar = off; off = align_up(off + static_cast<size_t>(L.n_pad) * L.k_pad, 1024);
@@ -708,6 +709,11 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
     int32_t* e_nu = eexp + m;
 
     const bool imported = opt && opt->e_mu_in && opt->e_nu_in;
+    int sync_chunk = 1;
+    {   // throttle chunks must tile the 512-block K segments: a power of two in [1, 512]
+        const int kc = tune(OZ2_TUNE_SYNC_CHUNK);
+        while (sync_chunk * 2 <= kc && sync_chunk * 2 <= 512) sync_chunk *= 2;
+    }
     g_ts.timed_last = false;
     phase_mark(0);
     OZ2_CK(cudaMemsetAsync(D().d_status, 0, sizeof(int32_t), st));
@@ -755,6 +761,15 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             gp.super_shift = super_shift_of(L.k_pad);
             gp.m_tiles = static_cast<int>(L.m_pad / tile_m(cg)); gp.n_tiles = static_cast<int>(L.n_pad / BN);
             gp.rmax = rsmax; gp.smax = rsmax + m;
+            // the residue GEMM's progress throttle and lazy epilogue wait apply here too
+            gp.sync_lead = sync_lead();
+            gp.sync_chunk = sync_chunk;
+            gp.epi_sleep_ns = static_cast<unsigned>(tune(OZ2_TUNE_EPI_SLEEP));
+            gp.max_units = tune(OZ2_TUNE_MAX_UNITS);
+            if (gp.sync_lead > 0) {
+                gp.progress = reinterpret_cast<unsigned long long*>(ws + L.prog);
+                OZ2_CK(cudaMemsetAsync(gp.progress, 0, 8, st));
+            }
             OZ2_CK(launch_gemm(i8 ? MODE_BOUND_I8 : MODE_BOUND, cg, 0, ta, tb, gp, D().num_sms, st));
         }
         if (opt && opt->rmax && !fast) OZ2_CK(cudaMemcpyAsync(opt->rmax, rsmax, 4 * m, cudaMemcpyDeviceToDevice, st));
@@ -788,11 +803,6 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
     const int fuse_env = tune(OZ2_TUNE_FUSED_CRT);
     const bool fuse_auto = i8 ? k >= 49152 : k >= 16384;
     const int fused = (pl->L <= 6 && k >= 8192 && (fuse_env > 0 || (fuse_env < 0 && fuse_auto))) ? pl->L : 0;
-    int sync_chunk = 1;
-    {   // chunks must tile the 512-block K segments: a power of two in [1, 512]
-        const int kc = tune(OZ2_TUNE_SYNC_CHUNK);
-        while (sync_chunk * 2 <= kc && sync_chunk * 2 <= 512) sync_chunk *= 2;
-    }
     // ---- steps 4-6 on blocks of C (one block when unblocked)
     phase_mark(3);
     if (L.blocked) phase_mark(4);     // blocked: the whole block loop counts as "residue GEMM"
@@ -870,7 +880,7 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
                 gp.hint_b = hint(tune(OZ2_TUNE_TMA_HINT_B));
             }
             if (gp.sync_lead > 0) {
-                gp.progress = reinterpret_cast<unsigned long long*>(maxbits);   // dead after step 3
+                gp.progress = reinterpret_cast<unsigned long long*>(ws + L.prog);
                 OZ2_CK(cudaMemsetAsync(gp.progress, 0, 8, st));
             }
             double* Cij = C + i0 + j0 * ldc;

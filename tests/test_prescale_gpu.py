@@ -1,6 +1,6 @@
 """Step 1 (prescale, eq. def:mu'nu') through the C ABI: the one-read form
-(chunk-local casts + rescale to the row exponent, the default) against the oracle and
-against the two-read form (row maxima, then the cast; OZ2_TUNE_PRESCALE_2READ = 1), on
+(chunk-local casts + rescale to the row exponent, OZ2_TUNE_PRESCALE_2READ = 0) against the
+oracle and against the two-read form (row maxima, then the cast; the default), on
 rows whose entries span the whole binary64 range -- so chunk exponents differ from the row
 exponent by 0 .. > 1000, rescaled codes land on every part of the E4M3 grid (normal,
 subnormal, the 2^-9 floor) -- with zero chunks, zero rows, NaN / Inf rows, both storage
@@ -125,3 +125,25 @@ def test_digits_fma_fast_path_identical(sch, N):
             P.oz2_reset_tuning()
     for key in ("digits_a", "digits_b", "residues", "e_mu", "e_nu", "C"):
         assert np.array_equal(outs[0][key], outs[1][key]), key
+
+
+def test_digits_fma_fast_path_blocked():
+    """The fast path reads step 1's row maxima in step 4; with m/n blocking (several row and
+    column blocks, so A's digits are recomputed after earlier blocks' GEMMs have run) C must
+    equal the unblocked general-path result bit for bit."""
+    import torch
+    import paper_2603_10634_b200 as P
+    from gpu_helpers import run
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    m, n, k = 600, 520, 2300
+    A = _wide(m, k, 13)
+    B = _wide(n, k, 14).T.copy()
+    ref = run(A, B, 13, want_residues=False)
+    assert P.oz2_set_tuning("digits_fma", 1) == 0 and P.oz2_set_blocking(256, 256) == 0
+    try:
+        blk = run(A, B, 13, want_residues=False)
+    finally:
+        P.oz2_reset_tuning()
+        P.oz2_set_blocking(0, 0)
+    assert np.array_equal(ref["C"], blk["C"])
