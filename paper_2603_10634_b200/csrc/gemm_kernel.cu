@@ -87,26 +87,26 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // 2-SM TMA: bytes land in this CTA's smem, completion is counted on the leader's barrier
-__device__ __forceinline__ void tma_load_4d_cg2(const CUtensorMap* m, uint32_t leader_bar, void* smem,
-                                                int32_t c0, int32_t c1, int32_t c2, int32_t c3,
+__device__ __forceinline__ void tma_load_5d_cg2(const CUtensorMap* m, uint32_t leader_bar, void* smem,
+                                                int32_t c0, int32_t c1, int32_t c2, int32_t c3, int32_t c4,
                                                 uint64_t cache_hint) {
     asm volatile(
-        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;"
+        "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;"
         ::"r"(smem_u32(smem)), "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar),
-          "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(cache_hint)
+          "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "l"(cache_hint)
         : "memory");
 }
 // 2-SM TMA multicast: the box lands at the same smem offset in every CTA of `mask`, and
 // each destination pair's leader barrier (same offset) counts the bytes
-__device__ __forceinline__ void tma_load_4d_cg2_mc(const CUtensorMap* m, uint32_t leader_bar, void* smem,
-                                                   int32_t c0, int32_t c1, int32_t c2, int32_t c3,
+__device__ __forceinline__ void tma_load_5d_cg2_mc(const CUtensorMap* m, uint32_t leader_bar, void* smem,
+                                                   int32_t c0, int32_t c1, int32_t c2, int32_t c3, int32_t c4,
                                                    uint16_t mask, uint64_t cache_hint) {
     asm volatile(
-        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
-        " [%0], [%1, {%4, %5, %6, %7}], [%2], %3, %8;"
+        "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+        " [%0], [%1, {%4, %5, %6, %7, %8}], [%2], %3, %9;"
         ::"r"(smem_u32(smem)), "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar), "h"(mask),
-          "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(cache_hint)
+          "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "l"(cache_hint)
         : "memory");
 }
 __device__ __forceinline__ void mma_f8f6f4_cg2(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
@@ -299,28 +299,32 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                             ++g;
                         }
                         mbar_wait(&empty[stage], phase ^ 1);
-                        // map coordinates {K byte in the super-chunk, plane, super-chunk, row}
-                        // (digit planes; a plain [rows][k] matrix for the
-                        // raw GEMM: shift 30, dimension 0 spans the row)
-                        const int c0 = (kb & ((1 << P.super_shift) - 1)) * BK, c2 = kb >> P.super_shift;
+                        // map coordinates {K byte in the super-chunk, row in the 128-row block,
+                        // plane, super-chunk, row block} (digit planes); a
+                        // plain [rows][k] matrix for the raw GEMM: {K byte, row, 0, 0, 0}
+                        const int c0 = (kb & ((1 << P.super_shift) - 1)) * BK, c3 = kb >> P.super_shift;
+                        const int ar1 = P.row_blocked ? (a_row & (kRowBlk - 1)) : a_row;
+                        const int ar4 = P.row_blocked ? (a_row >> 7) : 0;
+                        const int br1 = P.row_blocked ? (b_row & (kRowBlk - 1)) : b_row;
+                        const int br4 = P.row_blocked ? (b_row >> 7) : 0;
                         if (CG == 1) {
                             mbar_arrive_expect_tx(&full[stage], Cfg::A_STAGE + Cfg::B_STAGE);
-                            tma_load_4d(&tmA, &full[stage], sA + stage * Cfg::A_STAGE, c0, a_pl, c2, a_row, hint_a);
-                            tma_load_4d(&tmB, &full[stage], sB + stage * Cfg::B_STAGE, c0, b_pl, c2, b_row, hint_b);
+                            tma_load_5d(&tmA, &full[stage], sA + stage * Cfg::A_STAGE, c0, ar1, a_pl, c3, ar4, hint_a);
+                            tma_load_5d(&tmB, &full[stage], sB + stage * Cfg::B_STAGE, c0, br1, b_pl, c3, br4, hint_b);
                         } else {
                             const uint32_t lb = full0 + stage * 8u;
                             if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (Cfg::A_STAGE + Cfg::B_STAGE));
                             else mbar_arrive_cluster(full_leader + stage * 8u);
                             if (MC == 1) {
-                                tma_load_4d_cg2(&tmA, lb, sA + stage * Cfg::A_STAGE, c0, a_pl, c2, a_row, hint_a);
+                                tma_load_5d_cg2(&tmA, lb, sA + stage * Cfg::A_STAGE, c0, ar1, a_pl, c3, ar4, hint_a);
                             } else {
                                 // this CTA's half of the A tile, multicast to the CTA with the same
                                 // rank in the other pair (which loads the other half for both)
                                 const uint16_t amask = static_cast<uint16_t>((1u << rank) | (1u << (rank + CG)));
-                                tma_load_4d_cg2_mc(&tmA, lb, sA + stage * Cfg::A_STAGE + pairi * (Cfg::A_STAGE / 2),
-                                                   c0, a_pl, c2, a_row, amask, hint_a);
+                                tma_load_5d_cg2_mc(&tmA, lb, sA + stage * Cfg::A_STAGE + pairi * (Cfg::A_STAGE / 2),
+                                                   c0, ar1, a_pl, c3, ar4, amask, hint_a);
                             }
-                            tma_load_4d_cg2(&tmB, lb, sB + stage * Cfg::B_STAGE, c0, b_pl, c2, b_row, hint_b);
+                            tma_load_5d_cg2(&tmB, lb, sB + stage * Cfg::B_STAGE, c0, br1, b_pl, c3, br4, hint_b);
                         }
                         if (++stage == NS) { stage = 0; phase ^= 1; }
                     }

@@ -554,39 +554,44 @@ static PFN_encodeTiled_t encode_fn() {
     return fn;
 }
 
-// 4-D byte tensor maps, box {128 bytes of K, 1 plane, 1 super-chunk, box_rows rows}, 128B
-// swizzle (the smem tile is the same 128-byte x box_rows block as a 2-D box):
-//   make_map_planes: digit planes, byte (x, r, h) at ((r KS + h/S) M + x) S + h mod S
-//                    (S = super_bytes(k_pad), KS = k_pad/S super-chunks, M planes per group)
-//   make_map_plain:  a plain [rows][pitch] matrix with k bytes per row (the raw GEMM)
-static bool encode_map4(CUtensorMap* map, const void* base, const cuuint64_t (&dims)[4],
-                        const cuuint64_t (&strides)[3], uint32_t box_rows) {
+// 5-D byte tensor maps, 128B swizzle; the box is 128 bytes of K x box_rows rows, which lands
+// in shared memory exactly like the 2-D box of a plain K-major matrix:
+//   make_map_planes: digit planes (plane_offset): dims {S bytes, 128 rows,
+//                    M planes, KS super-chunks, row blocks}; a 256-row box takes two row
+//                    blocks ({128, 128, 1, 1, 2}: the blocks' 128-row slabs are stacked)
+//   make_map_plain:  a plain [rows][pitch] matrix with k bytes per row (the raw GEMM):
+//                    dims {k, rows, 1, 1, 1}
+static bool encode_map5(CUtensorMap* map, const void* base, const cuuint64_t (&dims)[5],
+                        const cuuint64_t (&strides)[4], const cuuint32_t (&box)[5]) {
     PFN_encodeTiled_t fn = encode_fn();
     if (!fn) return false;
-    cuuint32_t box[4] = {static_cast<cuuint32_t>(BK), 1, 1, box_rows};
-    cuuint32_t es[4] = {1, 1, 1, 1};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
     // L2 promotion of TMA misses (OZ2_TUNE_L2_PROMO: 0 none, 1 64B, 2 128B, 3 256B)
     const int promo = tune(OZ2_TUNE_L2_PROMO);
     const CUtensorMapL2promotion pr = promo == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
                                     : promo == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
                                     : promo == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
                                                  : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-    return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(base), dims, strides, box, es,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, pr,
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<void*>(base), dims, strides,
+              const_cast<cuuint32_t*>(box), es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, pr,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 static bool make_map_planes(CUtensorMap* map, const void* base, int M, uint64_t k_pad, uint64_t rows,
                             uint32_t box_rows) {
     const uint64_t S = static_cast<uint64_t>(super_bytes(static_cast<int64_t>(k_pad))), KS = k_pad / S;
-    const cuuint64_t dims[4] = {S, static_cast<cuuint64_t>(M), KS, rows};
-    const cuuint64_t strides[3] = {S, S * M, S * M * KS};
-    return encode_map4(map, base, dims, strides, box_rows);
+    const uint64_t RB = (rows + kRowBlk - 1) / kRowBlk;
+    const cuuint64_t dims[5] = {S, static_cast<cuuint64_t>(kRowBlk), static_cast<cuuint64_t>(M), KS, RB};
+    const cuuint64_t strides[4] = {S, S * kRowBlk, S * kRowBlk * M, S * kRowBlk * M * KS};
+    const cuuint32_t box[5] = {static_cast<cuuint32_t>(BK), box_rows > static_cast<uint32_t>(kRowBlk) ? kRowBlk : box_rows,
+                               1, 1, box_rows > static_cast<uint32_t>(kRowBlk) ? box_rows / kRowBlk : 1};
+    return encode_map5(map, base, dims, strides, box);
 }
 static bool make_map_plain(CUtensorMap* map, const void* base, uint64_t k, uint64_t rows, uint64_t pitch,
                            uint32_t box_rows) {
-    const cuuint64_t dims[4] = {k, 1, 1, rows};
-    const cuuint64_t strides[3] = {pitch, pitch, pitch};
-    return encode_map4(map, base, dims, strides, box_rows);
+    const cuuint64_t dims[5] = {k, rows, 1, 1, 1};
+    const cuuint64_t strides[4] = {pitch, pitch * rows, pitch * rows, pitch * rows};
+    const cuuint32_t box[5] = {static_cast<cuuint32_t>(BK), box_rows, 1, 1, 1};
+    return encode_map5(map, base, dims, strides, box);
 }
 
 static int super_shift_of(int64_t k_pad) {   // log2(S / BK) of the digit-plane layout
@@ -759,6 +764,7 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             gp.m = static_cast<int>(m); gp.n = static_cast<int>(n);
             gp.num_k_blocks = static_cast<int>((k + BK - 1) / BK);   // not the layout's padding
             gp.super_shift = super_shift_of(L.k_pad);
+            gp.row_blocked = 1;
             gp.m_tiles = static_cast<int>(L.m_pad / tile_m(cg)); gp.n_tiles = static_cast<int>(L.n_pad / BN);
             gp.rmax = rsmax; gp.smax = rsmax + m;
             // the residue GEMM's progress throttle and lazy epilogue wait apply here too
@@ -845,6 +851,7 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             gp.m = static_cast<int>(mbi); gp.n = static_cast<int>(nbj);
             gp.num_k_blocks = static_cast<int>((k + BK - 1) / BK);   // not the layout's padding
             gp.super_shift = super_shift_of(L.k_pad);
+            gp.row_blocked = 1;
             gp.kseg_blocks = kMaxK / BK;                                  // 2^16 per segment
             gp.num_kseg = (gp.num_k_blocks + gp.kseg_blocks - 1) / gp.kseg_blocks;
             gp.m_tiles = static_cast<int>(mbi_pad / tile_m(cg)); gp.n_tiles = static_cast<int>(nbj_pad / BN);

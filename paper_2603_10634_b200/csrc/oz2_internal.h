@@ -30,19 +30,28 @@ constexpr int GEMM_THREADS = 320;       // warp0 TMA, warp1 MMA, warps 2..9 epil
 constexpr int PAD_M = 256;       // row padding of operand planes (tile multiple)
 constexpr int PAD_N = 256;
 constexpr int PAD_K = 128;
-// Digit-plane layout: the K extent of every plane is cut into super-chunks
-// of kSuper bytes; byte (plane x, row r, k index h) lives at
-//   ((r KS + h / S) M + x) S + h mod S,   S = super_bytes(k_pad), KS = k_pad / S,
-// i.e. for one row and one super-chunk the S-byte runs of all M planes are adjacent.  Each
-// plane keeps S contiguous bytes of K per row (DRAM page / L2-promotion locality for the
-// GEMM's TMA loads: 128-byte runs cost 6 % of residue-GEMM time, measured), and a digit
-// kernel thread stores its planes at compile-time offsets x S from one address.
+// Digit-plane layout: rows in blocks of kRowBlk = 128, the K extent of
+// every plane cut into super-chunks of S = kSuper bytes; byte (plane x, row r, k index h) at
+//   (((r / 128) KS + h / S) M + x) 128 S + (r mod 128) S + h mod S,
+//   S = super_bytes(k_pad), KS = k_pad / S,
+// i.e. one (row block, super-chunk) holds the M planes one after the other, each a
+// contiguous 128-row x S-byte slab.  A GEMM TMA box (<= 128 rows x 128 bytes of one plane)
+// stays inside one 256 KB slab (TLB locality: a per-row stride of M k_pad bytes cost 22 % of
+// residue-GEMM time at k = 32768, measured), each plane keeps S contiguous bytes of K per
+// row (DRAM page / L2-promotion locality: 128-byte runs cost 6 % at k = 16384), and a digit
+// kernel thread stores its planes at compile-time offsets x 128 S from one address.
 constexpr int kSuper = 2048;
+constexpr int kRowBlk = 128;
 __host__ __device__ inline int64_t pad_k(int64_t k) {          // k_pad: 128 multiple up to kSuper, then kSuper multiple
     const int64_t k128 = (k + PAD_K - 1) / PAD_K * PAD_K;
     return k128 <= kSuper ? k128 : (k + kSuper - 1) / kSuper * kSuper;
 }
 __host__ __device__ inline int64_t super_bytes(int64_t k_pad) { return k_pad < kSuper ? k_pad : kSuper; }
+// byte offset of (plane x of gplanes, row r, k index h)
+__host__ __device__ inline int64_t plane_offset(int64_t r, int64_t h, int x, int gplanes, int64_t k_pad) {
+    const int64_t S = super_bytes(k_pad), KS = k_pad / S;
+    return ((((r / kRowBlk) * KS + h / S) * gplanes + x) * kRowBlk + (r % kRowBlk)) * S + h % S;
+}
 
 // FP8 (kind::f8f6f4, E4M3 -> FP32) modes, and the same three on the INT8 tensor path
 // (kind::i8, S8/U8 -> S32) of the INT8 Ozaki-II scheme (NEXT-3): MODE_X_I8 = MODE_X + 3
@@ -86,6 +95,8 @@ struct GemmParams {
     int super_shift;             // log2(S / BK): k-block kb sits in super-chunk kb >> shift at
                                  // byte (kb mod 2^shift) BK (digit planes);
                                  // 30 for a plain [rows][k] matrix (raw GEMM)
+    int row_blocked;             // 1: digit-plane maps {S, 128 rows, plane, super-chunk, row
+                                 // block}; 0: plain maps {k, rows, 1, 1, 1}
     int num_moduli;
     int tail_head;               // residue mode: tiles [0, head) tile-major, the rest as
                                  // (tile, modulus) items (no fused CRT unless head = all tiles)

@@ -92,6 +92,16 @@ __device__ __forceinline__ void tma_load_4d(const CUtensorMap* m, uint64_t* bar,
           "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(cache_hint)
         : "memory");
 }
+__device__ __forceinline__ void tma_load_5d(const CUtensorMap* m, uint64_t* bar, void* smem,
+                                            int32_t c0, int32_t c1, int32_t c2, int32_t c3, int32_t c4,
+                                            uint64_t cache_hint) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;"
+        ::"r"(smem_u32(smem)), "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)),
+          "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "l"(cache_hint)
+        : "memory");
+}
 // L2 cache-policy constants (createpolicy encodings used by CUTLASS)
 constexpr uint64_t kEvictNormal = 0x1000000000000000ull;
 constexpr uint64_t kEvictFirst  = 0x12F0000000000000ull;

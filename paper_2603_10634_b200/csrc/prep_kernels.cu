@@ -7,11 +7,10 @@
 //
 // An operand is seen as `rows` rows of length k (A: rows = i; B: rows = j of B^T).
 // Element (r, h) lives at X[r + h*ld] (MN-major: A with transa='N', B with 'T') or
-// X[h + r*ld] (K-major: A 'T', B 'N').  Outputs are K-major byte planes in the
-// super-chunk layout (oz2_internal.h): byte (plane x, row r, k index h) at
-// ((r KS + h/S) M + x) S + h mod S, S = super_bytes(k_pad), KS = k_pad/S, M planes per
-// group -- for each row and S-wide K super-chunk the runs of all M planes are adjacent, so
-// (S = kSuper) a thread's stores to its planes differ by compile-time multiples of S bytes.
+// X[h + r*ld] (K-major: A 'T', B 'N').  Outputs are K-major byte planes in the row-blocked
+// super-chunk layout (plane_offset in oz2_internal.h): per 128-row block
+// and S-wide K super-chunk, the M planes are consecutive 128-row x S-byte slabs, so (S =
+// kSuper) a thread's stores to its planes differ by compile-time multiples of 128 S bytes.
 // Zero in the padding.
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -128,12 +127,21 @@ __device__ __forceinline__ void load_tile(const double* __restrict__ X, int64_t 
     }
 }
 
-// byte offset of (row r, 128-byte chunk c) in the super-chunk layout with `gplanes` planes
-// per group (plane 0); S = kSuper (16 chunks per super-chunk) or S = k_pad (one super-chunk)
+// byte offset of (row r, 128-byte chunk c) of plane 0 in the layout with `gplanes` planes
+// per group; S = kSuper (16 chunks per super-chunk) or S = k_pad (one super-chunk)
 __device__ __forceinline__ int64_t chunk_offset(int64_t r, uint32_t c, int gplanes, int64_t k_pad) {
+    const int64_t rb = r >> 7, ri = r & (kRowBlk - 1);
     if (k_pad >= kSuper)
-        return (r * (k_pad / kSuper) + (c >> 4)) * gplanes * kSuper + (c & 15u) * TH;
-    return r * gplanes * k_pad + c * TH;
+        return ((rb * (k_pad / kSuper) + (c >> 4)) * gplanes * kRowBlk + ri) * kSuper + (c & 15u) * TH;
+    return (rb * gplanes * kRowBlk + ri) * k_pad + c * TH;
+}
+
+// the same for the digit planes (num_planes per group), S = kSuper known at compile time
+template <bool SUP>
+__device__ __forceinline__ int64_t chunk_offset_planes(int64_t r, uint32_t c, int planes, int64_t k_pad) {
+    const int64_t rb = r >> 7, ri = r & (kRowBlk - 1);
+    if (SUP) return ((rb * (k_pad / kSuper) + (c >> 4)) * planes * kRowBlk + ri) * kSuper + (c & 15u) * TH;
+    return (rb * planes * kRowBlk + ri) * k_pad + c * TH;
 }
 
 __device__ __forceinline__ double pow2d(int e) {          // 2^e, |e| <= 1022
@@ -651,11 +659,8 @@ __global__ void __launch_bounds__(256, 6) k_digits(const double* __restrict__ X,
     load_tile<KMAJOR>(X, rows, k, ld, r0, h0, tile);
     __syncthreads();
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const int pitch = SUP ? kSuper : static_cast<int>(k_pad);                 // S: bytes between planes
-    const int64_t group = static_cast<int64_t>(dp.num_planes) * pitch;       // bytes per (row, super-chunk)
-    constexpr int kCps = kSuper / TH;                                        // chunks per super-chunk (SUP)
-    const int64_t sc = SUP ? blockIdx.x / kCps : 0, within = SUP ? (blockIdx.x % kCps) * TH : blockIdx.x * TH;
-    const int64_t ks = SUP ? k_pad / kSuper : 1;
+    // plane pitch 128 S: a compile-time immediate for S = kSuper
+    const int pitch = kRowBlk * (SUP ? kSuper : static_cast<int>(k_pad));
     // a lane owns kEPL consecutive k of one row: kLPR lanes per row, 32 / kLPR rows per warp
     constexpr int kLPR = TH / kEPL, kRPW = 32 / kLPR;
     static_assert(kRPW == 1, "one row per warp: the per-row path choice below is warp-uniform");
@@ -667,7 +672,7 @@ __global__ void __launch_bounds__(256, 6) k_digits(const double* __restrict__ X,
         int e = (r < rows) ? e_scale[r] : 0;
         if (e == kExpNonFinite) e = 0;                    // NaN / Inf row: C gets NaN (R12)
         // plane x of this (row, super-chunk) at out + x S: immediate store offsets (SUP)
-        uint8_t* out = planes + (r * ks + sc) * group + within + hl;
+        uint8_t* out = planes + chunk_offset_planes<SUP>(r, blockIdx.x, dp.num_planes, k_pad) + hl;
         // Common case, decided per row from step 1's row maximum: |X'| < 2^52 and 2^e a
         // normal double.  Then trunc(x 2^e) is ONE fused multiply-add rounded toward zero,
         // fma.rz(x, 2^e, +-2^52) - (+-2^52) with the sign of x (|x 2^e| + 2^52 lies in
@@ -740,11 +745,11 @@ __global__ void k_scale(double* C, int64_t m, int64_t n, int64_t ldc, double bet
 // plane x of the super-chunk layout -> [rows][k] (debug outputs of oz2_dgemm_ex only)
 __global__ void k_unpack_plane(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, int gplanes, int x,
                                int64_t rows, int64_t k, int64_t k_pad) {
-    const int64_t S = super_bytes(k_pad), ks = k_pad / S;
+
     for (int64_t r = blockIdx.y; r < rows; r += gridDim.y)
         for (int64_t h = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; h < k;
              h += static_cast<int64_t>(gridDim.x) * blockDim.x)
-            dst[r * k + h] = src[((r * ks + h / S) * gplanes + x) * S + h % S];
+            dst[r * k + h] = src[plane_offset(r, h, x, gplanes, k_pad)];
 }
 
 // ---------------------------------------------------------------------------------
