@@ -128,11 +128,12 @@ __device__ __forceinline__ void load_tile(const double* __restrict__ X, int64_t 
 }
 
 // byte offset of (row r, 128-byte chunk c) of plane 0 in the layout with `gplanes` planes
-// per group; S = kSuper (16 chunks per super-chunk) or S = k_pad (one super-chunk)
+// per group; S = kSuper (kCps chunks per super-chunk) or S = k_pad (one super-chunk)
+constexpr uint32_t kCps = kSuper / TH;
 __device__ __forceinline__ int64_t chunk_offset(int64_t r, uint32_t c, int gplanes, int64_t k_pad) {
     const int64_t rb = r >> 7, ri = r & (kRowBlk - 1);
     if (k_pad >= kSuper)
-        return ((rb * (k_pad / kSuper) + (c >> 4)) * gplanes * kRowBlk + ri) * kSuper + (c & 15u) * TH;
+        return ((rb * (k_pad / kSuper) + c / kCps) * gplanes * kRowBlk + ri) * kSuper + (c % kCps) * TH;
     return (rb * gplanes * kRowBlk + ri) * k_pad + c * TH;
 }
 
@@ -140,7 +141,7 @@ __device__ __forceinline__ int64_t chunk_offset(int64_t r, uint32_t c, int gplan
 template <bool SUP>
 __device__ __forceinline__ int64_t chunk_offset_planes(int64_t r, uint32_t c, int planes, int64_t k_pad) {
     const int64_t rb = r >> 7, ri = r & (kRowBlk - 1);
-    if (SUP) return ((rb * (k_pad / kSuper) + (c >> 4)) * planes * kRowBlk + ri) * kSuper + (c & 15u) * TH;
+    if (SUP) return ((rb * (k_pad / kSuper) + c / kCps) * planes * kRowBlk + ri) * kSuper + (c % kCps) * TH;
     return (rb * planes * kRowBlk + ri) * k_pad + c * TH;
 }
 
