@@ -229,7 +229,7 @@ int oz2_finalize(void);
  *                             sharing A by TMA multicast (FP8 kinds; INT8 uses 2)
  *   OZ2_TUNE_SYNC_LEAD   1    progress throttle: chunks a pair may lead the chip-wide
  *                             average (0 = off)
- *   OZ2_TUNE_SYNC_CHUNK  8    k-blocks per throttle chunk (power of two, 1..512)
+ *   OZ2_TUNE_SYNC_CHUNK  4    k-blocks per throttle chunk (power of two, 1..512)
  *   OZ2_TUNE_L2_PROMO    3    L2 promotion of TMA misses: 0 none, 1 64 B, 2 128 B, 3 256 B
  *   OZ2_TUNE_MAX_UNITS   0    cap on persistent CTA pairs (0 = all; power-wall study)
  *   OZ2_TUNE_TMA_HINT_A  0    L2 policy of A's operand loads: 0 normal, 1 evict-last,

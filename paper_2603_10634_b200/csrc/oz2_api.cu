@@ -360,7 +360,7 @@ struct DevState {
 static const int kTuneDefault[OZ2_TUNE_COUNT] = {
     2,    // CTA_GROUP
     1,    // SYNC_LEAD
-    8,    // SYNC_CHUNK
+    4,    // SYNC_CHUNK (4 vs 8: -1.1 % residue GEMM at 16384^3, profiles/round2_knobs.md)
     3,    // L2_PROMO
     0,    // MAX_UNITS
     0,    // TMA_HINT_A
