@@ -213,6 +213,50 @@ def vendor_fp8_ceiling(torch, local_rank, size=16384, sustain_s=4.0):
     return out
 
 
+def vendor_int8_ceiling(torch, local_rank, size=16384, sustain_s=3.0):
+    """cuBLASLt INT8 (torch._int_mm, S8 x S8 -> S32) on the same box, burst and sustained
+    (back to back for `sustain_s` seconds, clocks sampled): the vendor's ceiling for the INT8
+    scheme's residue GEMMs.  Operands: random bytes in [-128, 127] (the INT8 residue planes)."""
+    out = {"kernel": "torch._int_mm (cuBLASLt) s8 x s8 -> s32", "shape": f"{size}^3"}
+    try:
+        g = torch.Generator(device="cuda")
+        g.manual_seed(6)
+        a = torch.randint(-128, 128, (size, size), generator=g, device="cuda", dtype=torch.int8)
+        b = torch.randint(-128, 128, (size, size), generator=g, device="cuda", dtype=torch.int8)
+        f = lambda: torch._int_mm(a, b.t())
+        flops = 2.0 * size ** 3
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(3):
+            f()
+        best = float("inf")
+        for _ in range(10):
+            e0.record()
+            f()
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        out["burst_tops"] = round(flops / (best * 1e-3) / 1e12, 1)
+        sampler = ClockSampler(local_rank)
+        sampler.start()
+        time.sleep(0.2)
+        reps, t0 = 0, time.perf_counter()
+        e0.record()
+        while time.perf_counter() - t0 < sustain_s:
+            for _ in range(10):
+                f()
+            reps += 10
+            torch.cuda.synchronize()
+        e1.record()
+        torch.cuda.synchronize()
+        out["sustained_tops"] = round(flops * reps / (e0.elapsed_time(e1) * 1e-3) / 1e12, 1)
+        out["sustained_clocks"] = sampler.stop()
+        del a, b
+        torch.cuda.empty_cache()
+    except Exception as e:            # report, never fail the bench on the probe
+        out["error"] = repr(e)[:300]
+    return out
+
+
 # ---------------------------------------------------------------------------------- oz2 arm
 
 def run_oz2(args, rank, world, local_rank):
@@ -484,6 +528,18 @@ def run_oz2(args, rank, world, local_rank):
                                   "host <-> device around the device-pointer oz2_dgemm" if world > 1
                                   else "pinned host (A, B, C through oz2_dgemm)")}
         del Ahost, Bhost, Chost
+    if rank == 0 and args.scheme == "int8":
+        # the INT8 MMA draws less power than FP8 under the same cap, so the bf16-derived proxy
+        # is no ceiling for it: measure cuBLASLt INT8 on the box and take the larger as peak
+        vi = vendor_int8_ceiling(torch, local_rank)
+        out["vendor_int8"] = vi
+        if vi.get("sustained_tops"):
+            rf = out["roofline"]
+            rf["frac_vs_vendor_int8_sustained"] = round(rf["achieved"] / vi["sustained_tops"], 4)
+            if vi["sustained_tops"] > rf["peak"]:
+                rf["peak"] = vi["sustained_tops"]
+                rf["frac"] = round(rf["achieved"] / rf["peak"], 4)
+                rf["peak_source"] = "measured on this box: cuBLASLt INT8 (torch._int_mm) sustained, 16384^3"
     if rank != 0 or args.no_extras:
         return out, None
 
