@@ -243,9 +243,9 @@ int oz2_finalize(void);
  *   OZ2_TUNE_CRT_GENERIC 0    1 = the generic standalone CRT kernel (A/B reference)
  *   OZ2_TUNE_HOST_BLOCKS 4    host-pointer calls with pinned C: column blocks of C whose
  *                             device-to-host copies overlap the GEMMs (1 = off)
- *   OZ2_TUNE_KCAT        0    square moduli: accumulate A1B2 + A2B1 in one TMEM
- *                             accumulator (K-concatenated) when k <= 2^15 (two
- *                             accumulator drains instead of three; measured slower)
+ *   OZ2_TUNE_KCAT       -1    square moduli: accumulate A1B2 + A2B1 in one TMEM
+ *                             accumulator (K-concatenated; two accumulator drains
+ *                             instead of three): -1 auto (k <= 2048), 0 off, 1 on (k <= 2^15)
  *   OZ2_TUNE_PRESCALE_2READ 1 accurate-mode step 1: 0 = one read of A and B (chunk-local
  *                             casts, then a rescale of A-bar/B-bar to the row exponent),
  *                             1 = row maxima then cast (two reads; fast mode always)

@@ -370,7 +370,7 @@ static const int kTuneDefault[OZ2_TUNE_COUNT] = {
     1,    // SQ_ORDER
     0,    // CRT_GENERIC
     4,    // HOST_BLOCKS
-    0,    // KCAT (no measurable gain at 16384^3: profiles/round2_layout_ab.md)
+    -1,   // KCAT: auto = on for k <= 2048 (profiles/round2_kcat_k.md)
     1,    // PRESCALE_2READ (one-read measured 0.1-0.4 ms slower in-step: profiles/round2_prescale_ab.md)
     1000, // EPI_SLEEP (ns)
     0,    // DIGITS_FMA (fewer instructions, but 0.1-0.5 ms slower in-step: profiles/round2_digits_ab.md)
@@ -601,6 +601,15 @@ static int super_shift_of(int64_t k_pad) {   // log2(S / BK) of the digit-plane 
     return s;
 }
 
+// Epilogue poll interval: the knob, but never more than ~8 ns per k-block of a product (an
+// accumulator fills in ~0.45 us per k-block at the capped clock; at small k the epilogue is
+// on the critical path and a long sleep would delay the slot hand-back)
+static unsigned epi_sleep_ns(int num_k_blocks) {
+    const int64_t cap = 8ll * num_k_blocks;
+    const int64_t v = tune(OZ2_TUNE_EPI_SLEEP);
+    return static_cast<unsigned>(v < cap ? v : cap);
+}
+
 static int sync_lead() {   // progress throttle of the residue GEMM (OZ2_TUNE_SYNC_LEAD)
     const int v = tune(OZ2_TUNE_SYNC_LEAD);
     return v < 0 ? 0 : v;
@@ -770,7 +779,7 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             // the residue GEMM's progress throttle and lazy epilogue wait apply here too
             gp.sync_lead = sync_lead();
             gp.sync_chunk = sync_chunk;
-            gp.epi_sleep_ns = static_cast<unsigned>(tune(OZ2_TUNE_EPI_SLEEP));
+            gp.epi_sleep_ns = epi_sleep_ns(gp.num_k_blocks);
             gp.max_units = tune(OZ2_TUNE_MAX_UNITS);
             if (gp.sync_lead > 0) {
                 gp.progress = reinterpret_cast<unsigned long long*>(ws + L.prog);
@@ -844,7 +853,11 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             if (!make_map_planes(&tb, digB, pl->M, L.k_pad, nbj_pad, b_box_rows(cg))) return cuda_fail(cudaErrorInvalidValue);
             // square moduli: A1 B2 + A2 B1 K-concatenated in one accumulator when the sum
             // stays in the FP32 exactness window (k <= 2^15; OZ2_TUNE_KCAT)
-            const bool kcat = tune(OZ2_TUNE_KCAT) != 0 && !i8 && pl->nsq > 0 && k <= kMaxK / 2;
+            // (auto: k <= 2048, where each product's MMAs are shorter than its accumulator drain
+            // and 33 drains per tile instead of 39 pay: +14 % at 16384^2 x 1024, +7.5 % at 2048;
+            // -1 to -2 % from k = 4096 on, profiles/round2_kcat_k.md)
+            const int kcat_knob = tune(OZ2_TUNE_KCAT);
+            const bool kcat = (kcat_knob > 0 || (kcat_knob < 0 && k <= 2048)) && !i8 && pl->nsq > 0 && k <= kMaxK / 2;
             GemmParams gp = kcat ? pl->gemm_mod_kcat : pl->gemm_mod;
             gp.prods_per_tile = 0;
             for (int l = 0; l < N; ++l) gp.prods_per_tile += gp.mod[l].nprod;
@@ -877,7 +890,7 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             gp.residues = res;
             gp.sync_lead = sync_lead();
             gp.sync_chunk = sync_chunk;
-            gp.epi_sleep_ns = static_cast<unsigned>(tune(OZ2_TUNE_EPI_SLEEP));
+            gp.epi_sleep_ns = epi_sleep_ns(gp.num_k_blocks);
             gp.max_units = tune(OZ2_TUNE_MAX_UNITS);
             {   // OZ2_TUNE_TMA_HINT_A / _B: 0 evict-normal (default), 1 evict-last, 2 evict-first
                 auto hint = [](int v) -> unsigned long long {
@@ -1202,7 +1215,7 @@ int oz2_set_tuning(int knob, int value) {
         case OZ2_TUNE_FUSED_CRT: ok = value >= -1 && value <= 1; break;
         case OZ2_TUNE_SQ_ORDER:
         case OZ2_TUNE_CRT_GENERIC:
-        case OZ2_TUNE_KCAT:
+        case OZ2_TUNE_KCAT: ok = value >= -1 && value <= 1; break;
         case OZ2_TUNE_PRESCALE_2READ: ok = value == 0 || value == 1; break;
         case OZ2_TUNE_HOST_BLOCKS: ok = value >= 1 && value <= 64; break;
         case OZ2_TUNE_EPI_SLEEP: ok = value >= 0 && value <= 100000; break;

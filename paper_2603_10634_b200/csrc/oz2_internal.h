@@ -42,9 +42,11 @@ constexpr int PAD_K = 128;
 // kernel thread stores its planes at compile-time offsets x 128 S from one address.
 constexpr int kSuper = 2048;
 constexpr int kRowBlk = 128;
-__host__ __device__ inline int64_t pad_k(int64_t k) {          // k_pad: 128 multiple up to kSuper, then kSuper multiple
-    const int64_t k128 = (k + PAD_K - 1) / PAD_K * PAD_K;
-    return k128 <= kSuper ? k128 : (k + kSuper - 1) / kSuper * kSuper;
+// k_pad: a multiple of kSuper, so every call takes the specialised digit kernels (compile-time
+// plane pitch); only ceil(k / 128) k-blocks are ever written or read, the rest of the last
+// super-chunk is untouched address space
+__host__ __device__ inline int64_t pad_k(int64_t k) {
+    return (k + kSuper - 1) / kSuper * kSuper;
 }
 __host__ __device__ inline int64_t super_bytes(int64_t k_pad) { return k_pad < kSuper ? k_pad : kSuper; }
 // byte offset of (plane x of gplanes, row r, k index h)

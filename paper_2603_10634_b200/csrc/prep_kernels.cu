@@ -873,11 +873,16 @@ cudaError_t launch_digits(const double* X, int64_t rows, int64_t k, int64_t ld, 
             default: OZ2_DIG(0, false, 0) break;
         }
     } else if (dp.num_squares == kNumSquares) {
-        switch (dp.num_moduli) {   // hybrid family, fully unrolled for the common moduli counts
+        switch (dp.num_moduli) {   // hybrid family, fully unrolled for config 2's sweep (12..20)
             case 12: OZ2_DIG(12, false, kNumSquares) break;
             case 13: OZ2_DIG(13, false, kNumSquares) break;
             case 14: OZ2_DIG(14, false, kNumSquares) break;
+            case 15: OZ2_DIG(15, false, kNumSquares) break;
             case 16: OZ2_DIG(16, false, kNumSquares) break;
+            case 17: OZ2_DIG(17, false, kNumSquares) break;
+            case 18: OZ2_DIG(18, false, kNumSquares) break;
+            case 19: OZ2_DIG(19, false, kNumSquares) break;
+            case 20: OZ2_DIG(20, false, kNumSquares) break;
             default: OZ2_DIG(0, false, kNumSquares) break;
         }
     } else {

@@ -1,6 +1,6 @@
 """A/B two sets of liboz2 tuning knobs in ONE process, alternating call by call.
 
-    python tools/ab_multi.py SIZE N "knob=v,knob=v" "knob=v" [rounds]
+    python tools/ab_multi.py SIZE N "knob=v,knob=v" "knob=v" [rounds] [k]
 
 An empty set ("-") means the defaults.  Prints medians of the per-phase CUDA-event timers."""
 import statistics
@@ -12,10 +12,11 @@ from synth import gen_device
 
 n = int(sys.argv[1]); N = int(sys.argv[2]); sets = sys.argv[3:5]
 rounds = int(sys.argv[5]) if len(sys.argv) > 5 else 8
-A = gen_device(n, n, "phi", phi=1.0, seed=1)
-B = gen_device(n, n, "phi", phi=1.0, seed=2)
+k = int(sys.argv[6]) if len(sys.argv) > 6 else n
+A = gen_device(n, k, "phi", phi=1.0, seed=1)
+B = gen_device(k, n, "phi", phi=1.0, seed=2)
 C = torch.empty((n, n), dtype=torch.float64, device="cuda").t()
-ws = torch.empty(P.oz2_workspace_size("N", "N", n, n, n, N), dtype=torch.uint8, device="cuda")
+ws = torch.empty(P.oz2_workspace_size("N", "N", n, n, k, N), dtype=torch.uint8, device="cuda")
 P.oz2_set_workspace(ws.data_ptr(), ws.numel())
 P.oz2_set_stream(torch.cuda.current_stream().cuda_stream)
 P.oz2_set_timing(True)
@@ -33,12 +34,12 @@ res = {s: [] for s in sets}
 for r in range(rounds + 1):
     for s in (sets if r % 2 == 0 else sets[::-1]):
         apply(s)
-        assert P.oz2_dgemm("N", "N", n, n, n, 1.0, A.data_ptr(), n, B.data_ptr(), n, 0.0, C.data_ptr(), n, N) == 0
+        assert P.oz2_dgemm("N", "N", n, n, k, 1.0, A.data_ptr(), n, B.data_ptr(), k, 0.0, C.data_ptr(), n, N) == 0
         t = P.oz2_get_timing()
         if r > 0:
             res[s].append(t)
 for s in sets:
     tot = statistics.median(x["total"] for x in res[s])
     g = statistics.median(x["residue_gemm"] for x in res[s])
-    b = statistics.median(x["bound_gemm"] for x in res[s])
-    print(f"[{s}]: total {tot:.3f} ms ({2.0*n**3/tot/1e9:.2f} TFLOP/s), residue_gemm {g:.3f}, bound_gemm {b:.3f}", flush=True)
+    ph = {key: round(statistics.median(x[key] for x in res[s]), 3) for key in res[s][0]}
+    print(f"[{s}]: {2.0*n*n*k/tot/1e9:.2f} TFLOP/s", ph, flush=True)
