@@ -254,6 +254,9 @@ int oz2_finalize(void);
  *   OZ2_TUNE_DIGITS_FMA  0    step 4: rows with |X'| < 2^52 (known from step 1's row maxima)
  *                             scale and truncate with one fma.rz per element (0 = the general
  *                             two-multiply path for every row)
+ *   OZ2_TUNE_TILE_N    256    residue-GEMM tile width with CTA pairs (FP8 schemes): 256, or
+ *                             512 (256 x 512 tiles: both 256-column TMEM accumulators hold
+ *                             one tile, A staged once for both halves)
  *
  * oz2_set_tuning returns -1 for an unknown knob, -2 for a value out of range;
  * oz2_get_tuning writes the current value. */
@@ -273,7 +276,8 @@ int oz2_finalize(void);
 #define OZ2_TUNE_PRESCALE_2READ 13
 #define OZ2_TUNE_EPI_SLEEP   14
 #define OZ2_TUNE_DIGITS_FMA  15
-#define OZ2_TUNE_COUNT       16
+#define OZ2_TUNE_TILE_N      16
+#define OZ2_TUNE_COUNT       17
 int oz2_set_tuning(int knob, int value);
 int oz2_get_tuning(int knob, int* value);
 void oz2_reset_tuning(void);

@@ -35,6 +35,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
 #include "oz2_internal.h"
@@ -43,14 +44,22 @@
 
 namespace oz2 {
 
-template <int CG>
+// W = 2 (CG = 2, residue mode only): a 256 x 512 tile per CTA pair -- two N = 256 MMAs per
+// K step share the staged A tile (25 % fewer operand bytes per MAC moved L2 -> SM), the two
+// 256-column accumulators are the L and R halves of the tile (no double buffer: the next
+// product's L half starts as soon as L is drained, see the MMA issuer), and each epilogue
+// thread keeps the partial residues of its 128 R columns in shared memory (kPartBytes).
+template <int CG, int W = 1>
 struct GemmCfg {
     static constexpr int TILE_M = BM * CG;            // output rows per (cluster) tile
-    static constexpr int B_ROWS = BN / CG;            // B^T rows staged per CTA
+    static constexpr int TILE_N = BN * W;             // output columns per tile
+    static constexpr int B_ROWS = TILE_N / CG;        // B^T rows staged per CTA
     static constexpr int A_STAGE = BM * BK;
     static constexpr int B_STAGE = B_ROWS * BK;
-    static constexpr int NSTAGE = CG == 1 ? STAGES : STAGES2;
-    static constexpr int SMEM = NSTAGE * (A_STAGE + B_STAGE) + 1024 + 256 + static_cast<int>(sizeof(CrtShared));
+    static constexpr int NSTAGE = W == 2 ? 3 : CG == 1 ? STAGES : STAGES2;
+    static constexpr int PART_BYTES = W == 2 ? 64 * 256 * 4 : 0;   // 64 half2 per epilogue thread
+    static constexpr int SMEM = NSTAGE * (A_STAGE + B_STAGE) + 1024 + 256 + static_cast<int>(sizeof(CrtShared)) +
+                                16 + PART_BYTES;
 };
 
 template <int G>
@@ -151,7 +160,7 @@ __device__ constexpr float2 kM2 = {12582912.0f, 12582912.0f};      // 1.5 2^23
 __device__ constexpr float2 kNM2 = {-12582912.0f, -12582912.0f};
 __device__ constexpr float2 kNM2b = {-8388608.0f, -8388608.0f};     // -2^23
 
-template <int MODE_, int CG, int FL, int MC>
+template <int MODE_, int CG, int FL, int MC, int W>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)   // 10 warps: 3 on one SM sub-partition -> <= 168 registers
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
             const __grid_constant__ GemmParams P) {
@@ -161,7 +170,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     // k-block passes per modulus: 3 (FP8: three products, or a K-concatenated pair + one)
     // or 1 (INT8); the number of accumulator drains is P.mod[l].nprod
     constexpr int NP = I8 ? 1 : 3;
-    using Cfg = GemmCfg<CG>;
+    using Cfg = GemmCfg<CG, W>;
+    static_assert(W == 1 || (CG == 2 && MC == 1 && MODE_ == MODE_RESIDUE), "256 x 512 tiles: FP8 residue pairs only");
     constexpr int NS = Cfg::NSTAGE;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -173,6 +183,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     CrtShared* crt_s = reinterpret_cast<CrtShared*>(smem + NS * (Cfg::A_STAGE + Cfg::B_STAGE) + 256);
+    // W = 2: partial residues of the R half, [64 pairs][256 epilogue threads] (conflict-free)
+    __half2* part_r = reinterpret_cast<__half2*>(
+        (reinterpret_cast<uintptr_t>(crt_s) + sizeof(CrtShared) + 15) & ~uintptr_t(15));
     if (FL > 0) crt_stage_constants(crt_s, P.crt, threadIdx.x, blockDim.x);
 
     const uint32_t warp = warp_id_uniform();
@@ -264,7 +277,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 tile_coords<16 / CG>(tile, P.m_tiles, n_super, tm, tn);
                 tn = tn * MC + static_cast<int>(pairi);
                 const int a_row = tm * Cfg::TILE_M + static_cast<int>(rank) * BM + (MC == 2 ? static_cast<int>(pairi) * (BM / 2) : 0);
-                const int b_row = tn * BN + static_cast<int>(rank) * Cfg::B_ROWS;
+                const int b_row = tn * Cfg::TILE_N + static_cast<int>(rank) * (BN / CG);
                 for (int l = l0; l < l1; ++l)
                 for (int x = 0; x < nprod_of(l); ++x)
                 for (int seg = 0; seg < nseg; ++seg)
@@ -325,6 +338,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                                                    c0, ar1, a_pl, c3, ar4, amask, hint_a);
                             }
                             tma_load_5d_cg2(&tmB, lb, sB + stage * Cfg::B_STAGE, c0, br1, b_pl, c3, br4, hint_b);
+                            if (W == 2) {   // this CTA's rows of the R half's B operand (row-blocked maps)
+                                const int b2 = b_row + BN;
+                                tma_load_5d_cg2(&tmB, lb, sB + stage * Cfg::B_STAGE + (BN / CG) * BK, c0,
+                                                b2 & (kRowBlk - 1), b_pl, c3, b2 >> 7, hint_b);
+                            }
                         }
                         if (++stage == NS) { stage = 0; phase ^= 1; }
                     }
@@ -342,7 +360,61 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        if (leader && elect_one()) {
+        if (W == 2 && leader && elect_one()) {
+            // 256 x 512 tiles: per K step one N = 256 MMA into each half (L: columns 0-255 of
+            // TMEM, R: 256-511), both reading the same staged A.  A product starts its L half as
+            // soon as the epilogue has drained L (tempty[0]) and runs it up to NS K steps ahead
+            // while R drains; R then catches up and both proceed in lockstep, so the tensor pipe
+            // idles only for the part of a drain longer than NS K steps of L MMAs.  tfull[0] is
+            // committed after the last L MMA, so L's drain overlaps R's last K steps.
+            constexpr uint32_t idesc = make_idesc_e4m3_f32(Cfg::TILE_M, BN);
+            uint32_t cnt = 0, g = 0;                 // K steps consumed (ring position), products
+            for (int it = unit; it < num_items; it += units) {
+                const int l0 = item_l0(it);
+                const int l1 = l0 + item_nmods(it);
+                for (int l = l0; l < l1; ++l)
+                for (int x = 0; x < nprod_of(l); ++x)
+                for (int seg = 0; seg < nseg; ++seg, ++g) {
+                    const int kb0 = seg * kseg, nk = min(nkb, kb0 + kseg) - kb0;
+                    const int nsteps = nparts_of(l, x) * nk;    // (part, k-block) steps
+                    auto issue = [&](int s, uint32_t half_col, uint32_t b_off) {
+                        const uint32_t q = cnt + static_cast<uint32_t>(s), st = q % NS;
+                        const uint64_t a0 = make_desc_k128_sw128(smem_u32(sA + st * Cfg::A_STAGE));
+                        const uint64_t b0 = make_desc_k128_sw128(smem_u32(sB + st * Cfg::B_STAGE + b_off));
+#pragma unroll
+                        for (int kk = 0; kk < BK / 32; ++kk)
+                            mma_f8f6f4_cg2(tmem_base + half_col, a0 + 2 * kk, b0 + 2 * kk, idesc,
+                                           (s > 0 || kk > 0) ? 1u : 0u);
+                    };
+                    auto wait_full = [&](int s) {
+                        const uint32_t q = cnt + static_cast<uint32_t>(s);
+                        mbar_wait(&full[q % NS], (q / NS) & 1u);
+                        tc_fence_after();
+                    };
+                    mbar_wait(&tempty[0], (g & 1u) ^ 1u);
+                    tc_fence_after();
+                    int sl = 0;
+                    for (const int ahead = min(NS, nsteps); sl < ahead; ++sl) {
+                        wait_full(sl);
+                        issue(sl, 0u, 0u);
+                    }
+                    if (sl == nsteps) mma_commit_cg2(&tfull[0], pair_mask);
+                    mbar_wait(&tempty[1], (g & 1u) ^ 1u);
+                    tc_fence_after();
+                    for (int sr = 0; sr < nsteps; ++sr) {
+                        issue(sr, static_cast<uint32_t>(BN), static_cast<uint32_t>((BN / CG) * BK));
+                        mma_commit_cg2(&empty[(cnt + static_cast<uint32_t>(sr)) % NS], pair_mask);
+                        if (sl == sr + 1 && sl < nsteps) {          // caught up: lockstep
+                            wait_full(sl);
+                            issue(sl, 0u, 0u);
+                            if (++sl == nsteps) mma_commit_cg2(&tfull[0], pair_mask);
+                        }
+                    }
+                    mma_commit_cg2(&tfull[1], pair_mask);
+                    cnt += static_cast<uint32_t>(nsteps);
+                }
+            }
+        } else if (W == 1 && leader && elect_one()) {
             constexpr uint32_t idesc = I8 ? make_idesc_i8_s32(Cfg::TILE_M, BN, MODE != MODE_BOUND)
                                           : make_idesc_e4m3_f32(Cfg::TILE_M, BN);
             uint32_t stage = 0, phase = 0, g = 0;
@@ -404,18 +476,21 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         // products of the next tile, crt_per_prod columns after each product, so its
         // residue loads never delay the release of an accumulator slot.  The N residues
         // of an element were written by this same thread (program order).
+        // A thread's columns of a tile: 128 (W = 1), or 128 of the L half and the same 128 of
+        // the R half, BN columns further (W = 2).
+        constexpr int TCOLS = 128 * W;
         int64_t crt_row = -1, crt_col0 = 0;
-        int crt_j = 128;
-        const int crt_per_prod = (MODE == MODE_RESIDUE) ? (128 + P.prods_per_tile * nseg - 1) / (P.prods_per_tile * nseg) + 1 : 0;
+        int crt_j = TCOLS;
+        const int crt_per_prod = (MODE == MODE_RESIDUE) ? (TCOLS + P.prods_per_tile * nseg - 1) / (P.prods_per_tile * nseg) + 1 : 0;
         auto crt_steps = [&](int ncols) {
-            if (FL == 0 || crt_j >= 128) return;
-            if (crt_row >= P.m) { crt_j = 128; return; }
+            if (FL == 0 || crt_j >= TCOLS) return;
+            if (crt_row >= P.m) { crt_j = TCOLS; return; }
             const int emu = P.e_mu[crt_row];
             const int64_t lstride = static_cast<int64_t>(P.n) * P.m;
 #pragma unroll 1
-            for (int s2 = 0; s2 < ncols && crt_j < 128; ++s2, ++crt_j) {
-                const int64_t col = crt_col0 + crt_j;
-                if (col >= P.n) { crt_j = 128; break; }
+            for (int s2 = 0; s2 < ncols && crt_j < TCOLS; ++s2, ++crt_j) {
+                const int64_t col = crt_col0 + crt_j + (W == 2 && crt_j >= 128 ? BN - 128 : 0);
+                if (col >= P.n) { crt_j = TCOLS; break; }   // (R columns lie right of L's)
                 const int enu = P.e_nu[col];
                 const double v = exps_finite(emu, enu)
                                      ? crt_element<(FL > 0 ? FL : 4)>(P.residues + col * P.m + crt_row, lstride,
@@ -425,6 +500,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             }
         };
         uint32_t g = 0;
+        const uint32_t et = threadIdx.x - 64u;    // epilogue thread index (W = 2 partials)
         for (int it = unit; it < num_items; it += units) {
             const int tile = item_tile(it);
             const int l0 = item_l0(it);
@@ -433,9 +509,84 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             tile_coords<16 / CG>(tile, P.m_tiles, n_super, tm, tn);
             tn = tn * MC + static_cast<int>(pairi);
             const int64_t row = static_cast<int64_t>(tm) * Cfg::TILE_M + row_in_tile;
-            const int64_t col0 = static_cast<int64_t>(tn) * BN + half * 128u;
+            const int64_t col0 = static_cast<int64_t>(tn) * Cfg::TILE_N + half * 128u;
             const bool row_ok = row < P.m;
-            if (MODE == MODE_RESIDUE) {
+            if (W == 2) {
+                // 256 x 512 tile: per product drain L (columns col0 + [0, 128)), release it,
+                // then R (col0 + BN + [0, 128)); partial residues of L in registers, of R in
+                // shared memory.  Same arithmetic as the W = 1 epilogue below.
+                for (int l = l0; l < l0 + mods_per_item; ++l) {
+                    const float p = P.mod[l].p, pinv = P.mod[l].pinv;
+                    __half2 part[64];
+                    int16_t* outL = P.residues + (static_cast<int64_t>(l) * P.n + col0) * P.m + row;
+                    const int npl = nprod_of(l);
+                    for (int x = 0; x < npl; ++x) {
+                      const float coef = P.mod[l].coef[x];
+                      for (int seg = 0; seg < nseg; ++seg, ++g) {
+                        const bool first = (x == 0) && (seg == 0);
+                        const bool last = (x == npl - 1) && (seg == nseg - 1);
+                        auto drain = [&](auto RIGHT) {
+                            constexpr bool R = decltype(RIGHT)::value;
+                            const uint32_t slot = R ? 1u : 0u;
+                            if (P.epi_sleep_ns) mbar_wait_sleep(&tfull[slot], g & 1u, P.epi_sleep_ns);
+                            else mbar_wait(&tfull[slot], g & 1u);
+                            tc_fence_after();
+                            const int64_t cb = col0 + (R ? BN : 0);
+                            int16_t* out = outL + (R ? static_cast<int64_t>(BN) * P.m : 0);
+                            const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + slot * BN + half * 128u;
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) {
+                                uint32_t v[32];
+                                tmem_ld_32x32b_x32(taddr + c * 32, v);
+                                tmem_ld_wait();
+                                if (c == 3) release_slot(slot);
+                                const bool chunk_full = row_ok && cb + c * 32 + 32 <= P.n;
+#pragma unroll
+                                for (int j = 0; j < 32; j += 2) {
+                                    const float2 f = make_float2(__uint_as_float(v[j]), __uint_as_float(v[j + 1]));
+                                    const float2 pinv2 = make_float2(pinv, pinv), np2 = make_float2(-p, -p);
+                                    float2 q = __fadd2_rn(__ffma2_rn(f, pinv2, kM2), kNM2);
+                                    float2 a2 = __ffma2_rn(q, np2, f);
+                                    const int idx = (c * 32 + j) >> 1;
+                                    const float2 cf = make_float2(coef, coef);
+                                    if (first) a2 = __fmul2_rn(a2, cf);
+                                    else a2 = __ffma2_rn(a2, cf, __half22float2(R ? part_r[idx * 256 + et] : part[idx]));
+                                    q = __fadd2_rn(__ffma2_rn(a2, pinv2, kM2), kNM2);
+                                    a2 = __ffma2_rn(q, np2, a2);
+                                    if (!last) {
+                                        const __half2 h = __floats2half2_rn(a2.x, a2.y);   // exact (|.| <= 546)
+                                        if (R) part_r[idx * 256 + et] = h;
+                                        else part[idx] = h;
+                                    } else {
+                                        const float2 u2 = __fadd2_rn(make_float2(a2.x < 0.0f ? a2.x + p : a2.x,
+                                                                                 a2.y < 0.0f ? a2.y + p : a2.y),
+                                                                     make_float2(8388608.0f, 8388608.0f));
+                                        const int jj = c * 32 + j;
+                                        int16_t* o = out + static_cast<int64_t>(jj) * P.m;
+                                        if (chunk_full) {
+                                            __stcs(o, static_cast<short>(__float_as_int(u2.x)));
+                                            __stcs(o + P.m, static_cast<short>(__float_as_int(u2.y)));
+                                        } else if (row_ok) {
+                                            if (cb + jj < P.n) __stcs(o, static_cast<short>(__float_as_int(u2.x)));
+                                            if (cb + jj + 1 < P.n) __stcs(o + P.m, static_cast<short>(__float_as_int(u2.y)));
+                                        }
+                                    }
+                                }
+                            }
+                        };
+                        drain(std::integral_constant<bool, false>());
+                        drain(std::integral_constant<bool, true>());
+                        crt_steps(crt_per_prod);
+                      }
+                    }
+                }
+                if (FL > 0) {
+                    crt_steps(TCOLS);
+                    crt_row = row;
+                    crt_col0 = col0;
+                    crt_j = 0;
+                }
+            } else if (MODE == MODE_RESIDUE) {
                 for (int l = l0; l < l0 + mods_per_item; ++l) {
                     const float p = P.mod[l].p, pinv = P.mod[l].pinv, w16 = P.mod[l].w16;
                     // running partial sum_x coef_x r_x, reduced mod p after every product
@@ -516,7 +667,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     }
                 }
                 if (FL > 0) {
-                    crt_steps(128);               // finish the previous tile if still pending
+                    crt_steps(TCOLS);             // finish the previous tile if still pending
                     crt_row = row;                // this tile's CRT is spread over the next tile
                     crt_col0 = col0;
                     crt_j = 0;
@@ -558,7 +709,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     atomicMax(P.rmax + row, rowmax);
             }
         }
-        crt_steps(128);                           // the last tile's CRT
+        crt_steps(TCOLS);                         // the last tile's CRT
     }
 
     tc_fence_before();
@@ -573,10 +724,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 
 constexpr int kMaxDevices = 64;
 
-template <int MODE, int CG, int FL, int MC>
+template <int MODE, int CG, int FL, int MC, int W = 1>
 static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& gp,
                               int num_sms, cudaStream_t st) {
-    using Cfg = GemmCfg<CG>;
+    using Cfg = GemmCfg<CG, W>;
     constexpr int CS = CG * MC;
     const int num_tiles = gp.m_tiles * (gp.n_tiles / MC);
     if (num_tiles == 0) return cudaSuccess;
@@ -592,10 +743,10 @@ static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, cons
     std::lock_guard<std::mutex> lk(mu);
     int& max_clusters = max_clusters_dev[dev];
     if (max_clusters == 0) {
-        cudaError_t err = cudaFuncSetAttribute(gemm_kernel<MODE, CG, FL, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+        cudaError_t err = cudaFuncSetAttribute(gemm_kernel<MODE, CG, FL, MC, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
         if (err != cudaSuccess) return err;
         if (CS > 1) {
-            err = cudaFuncSetAttribute(gemm_kernel<MODE, CG, FL, MC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+            err = cudaFuncSetAttribute(gemm_kernel<MODE, CG, FL, MC, W>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
             cudaLaunchConfig_t q = {};
             q.gridDim = dim3((num_sms / CS) * CS);
             q.blockDim = dim3(GEMM_THREADS);
@@ -608,7 +759,7 @@ static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, cons
             q.attrs = qa;
             q.numAttrs = 1;
             int nc = 0;
-            if (cudaOccupancyMaxActiveClusters(&nc, gemm_kernel<MODE, CG, FL, MC>, &q) != cudaSuccess || nc <= 0) {
+            if (cudaOccupancyMaxActiveClusters(&nc, gemm_kernel<MODE, CG, FL, MC, W>, &q) != cudaSuccess || nc <= 0) {
                 cudaGetLastError();
                 nc = num_sms / CS;
             }
@@ -636,7 +787,7 @@ static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, cons
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, CG, FL, MC>, ta, tb, gp);
+    return cudaLaunchKernelEx(&cfg, gemm_kernel<MODE, CG, FL, MC, W>, ta, tb, gp);
 }
 
 template <int CG, int MC>
@@ -667,11 +818,20 @@ static cudaError_t launch_cg(int mode, int fl, const CUtensorMap& ta, const CUte
 }
 
 // cg = 1: 128x256 single-CTA tiles; cg = 2: 256x256 CTA pairs; cg = 4: clusters of two
-// pairs on horizontally adjacent tiles sharing A by TMA multicast (needs even n_tiles)
+// pairs on horizontally adjacent tiles sharing A by TMA multicast (needs even n_tiles);
+// tile_n = 512 (cg = 2, FP8 residue mode): 256x512 CTA-pair tiles (gp.n_tiles in 512-column units)
 cudaError_t launch_gemm(int mode, int cg, int fused_limbs, const CUtensorMap& ta, const CUtensorMap& tb,
-                        const GemmParams& gp, int num_sms, cudaStream_t st) {
+                        const GemmParams& gp, int num_sms, cudaStream_t st, int tile_n) {
     cudaError_t err;
-    if (cg == 4 && mode < MODE_RESIDUE_I8) err = launch_cg<2, 2>(mode, fused_limbs, ta, tb, gp, num_sms, st);
+    if (tile_n == 512) {
+        if (cg != 2 || mode != MODE_RESIDUE) return cudaErrorInvalidValue;
+        switch (fused_limbs) {
+            case 4: err = launch_one<MODE_RESIDUE, 2, 4, 1, 2>(ta, tb, gp, num_sms, st); break;
+            case 5: err = launch_one<MODE_RESIDUE, 2, 5, 1, 2>(ta, tb, gp, num_sms, st); break;
+            case 6: err = launch_one<MODE_RESIDUE, 2, 6, 1, 2>(ta, tb, gp, num_sms, st); break;
+            default: err = launch_one<MODE_RESIDUE, 2, 0, 1, 2>(ta, tb, gp, num_sms, st); break;
+        }
+    } else if (cg == 4 && mode < MODE_RESIDUE_I8) err = launch_cg<2, 2>(mode, fused_limbs, ta, tb, gp, num_sms, st);
     else if (cg == 4) return cudaErrorInvalidValue;       // no multicast variant of the kind::i8 kernels
     else if (cg == 2) err = launch_cg<2, 1>(mode, fused_limbs, ta, tb, gp, num_sms, st);
     else err = launch_cg<1, 1>(mode, fused_limbs, ta, tb, gp, num_sms, st);

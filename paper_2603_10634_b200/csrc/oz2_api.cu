@@ -374,6 +374,7 @@ static const int kTuneDefault[OZ2_TUNE_COUNT] = {
     1,    // PRESCALE_2READ (one-read measured 0.1-0.4 ms slower in-step: profiles/round2_prescale_ab.md)
     1000, // EPI_SLEEP (ns)
     0,    // DIGITS_FMA (fewer instructions, but 0.1-0.5 ms slower in-step: profiles/round2_digits_ab.md)
+    256,  // TILE_N
 };
 
 struct ThreadState {
@@ -867,7 +868,10 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             gp.row_blocked = 1;
             gp.kseg_blocks = kMaxK / BK;                                  // 2^16 per segment
             gp.num_kseg = (gp.num_k_blocks + gp.kseg_blocks - 1) / gp.kseg_blocks;
-            gp.m_tiles = static_cast<int>(mbi_pad / tile_m(cg)); gp.n_tiles = static_cast<int>(nbj_pad / BN);
+            // OZ2_TUNE_TILE_N = 512: 256 x 512 CTA-pair tiles (FP8 schemes, CTA pairs)
+            const int tile_n = (tune(OZ2_TUNE_TILE_N) == 512 && cg == 2 && !i8) ? 512 : 256;
+            gp.m_tiles = static_cast<int>(mbi_pad / tile_m(cg));
+            gp.n_tiles = static_cast<int>((nbj_pad + tile_n - 1) / tile_n);
             gp.num_moduli = N;
             {   // work items (OZ2_TUNE_MOD_SPLIT: -1 auto, 0 tile-major, 1 all (tile, modulus),
                 // 2 hybrid): few tiles (< 8 per persistent unit) -> all split; otherwise
@@ -910,7 +914,7 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
                 gp.alpha = alpha; gp.beta = beta;
                 gp.C = Cij; gp.ldc = ldc;
             }
-            OZ2_CK(launch_gemm(i8 ? MODE_RESIDUE_I8 : MODE_RESIDUE, cg, fused_blk, ta, tb, gp, D().num_sms, st));
+            OZ2_CK(launch_gemm(i8 ? MODE_RESIDUE_I8 : MODE_RESIDUE, cg, fused_blk, ta, tb, gp, D().num_sms, st, tile_n));
             if (!L.blocked) {
                 if (opt && opt->residues)   // stored as u_l in [0, p_l): symmetric C'_l for the caller
                     OZ2_CK(launch_res_symmetric(opt->residues, res, m * n, pl->crt, st));
@@ -1220,6 +1224,7 @@ int oz2_set_tuning(int knob, int value) {
         case OZ2_TUNE_HOST_BLOCKS: ok = value >= 1 && value <= 64; break;
         case OZ2_TUNE_EPI_SLEEP: ok = value >= 0 && value <= 100000; break;
         case OZ2_TUNE_DIGITS_FMA: ok = value == 0 || value == 1; break;
+        case OZ2_TUNE_TILE_N: ok = value == 256 || value == 512; break;
         default: break;
     }
     if (!ok) return -2;

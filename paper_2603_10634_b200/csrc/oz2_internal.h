@@ -190,7 +190,7 @@ cudaError_t launch_digits(const double* X, int64_t rows, int64_t k, int64_t ld, 
 cudaError_t launch_unpack_plane(uint8_t* dst, const uint8_t* src, int gplanes, int x, int64_t rows, int64_t k,
                                 int64_t k_pad, cudaStream_t st);
 cudaError_t launch_gemm(int mode, int cg, int fused_limbs, const CUtensorMap& ta, const CUtensorMap& tb,
-                        const GemmParams& gp, int num_sms, cudaStream_t st);
+                        const GemmParams& gp, int num_sms, cudaStream_t st, int tile_n = 256);
 cudaError_t launch_res_symmetric(int16_t* out, const int16_t* in, int64_t per, const CrtParams& cp,
                                  cudaStream_t st);
 cudaError_t launch_crt(int limbs, const int16_t* res, int64_t m, int64_t n, const CrtParams& cp,

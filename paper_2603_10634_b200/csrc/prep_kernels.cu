@@ -163,72 +163,170 @@ __device__ __forceinline__ unsigned long long fp8_sq_units(uint32_t c) {   // co
 
 // I8 (INT8 scheme, R16): X-bar = ceil(|x| 2^e') in [0, 128] as U8 (exact upper bounds),
 // squares accumulated in units of 1.
-template <bool KMAJOR, bool FAST, bool I8>
+//
+// No shared-memory staging (round 3): a lane converts kCastH = 16 consecutive k of one row.
+//   MN-major (X[r + h ld]): lane = row, so each of the lane's 16 loads is one coalesced 256-byte
+//     run per warp; warp w of a block takes k in [h0 + 16 w, h0 + 16 w + 16): block = 32 rows x
+//     128 k (one 128-byte chunk of the layout), grid (rows_pad / 32, ceil(k / 128)).
+//   K-major (X[h + r ld]): warp = row, lane = 8 pairs of consecutive k 64 apart (eight coalesced
+//     16-byte loads when X is 16-byte aligned and ld even): block = 8 rows x 512 k, grid
+//     (rows_pad / 8, ceil(k / 512)).
+// The E4M3 round-up of the common element is four integer instructions on the high word of x
+// (cast_code); zeros, subnormal-range results and NaN / Inf rows take a warp-divergent slow
+// path.  Padding rows / k get zero codes.
+constexpr int kCastH = 16;
+
+struct CastRow {
+    uint32_t thr;        // |hi(x)| >= thr: the common path is exact (x normal, |x| 2^e >= 2^-6)
+    uint32_t add;        // ((e - 1016) << 20) + 0x1FFFF
+    int e;
+    bool bad;            // NaN / Inf row (R12): zero bounds, it cannot disturb other exponents
+};
+
+template <bool I8>
+__device__ __forceinline__ CastRow cast_row(unsigned long long mb) {
+    CastRow cr;
+    cr.e = eprime_of<I8>(mb);
+    cr.bad = mb >= 0x7FF0000000000000ull;
+    // y = |x| 2^e has binary64 exponent field ey = (hx >> 20) + e; the E4M3 normal range is
+    // y >= 2^-6, i.e. ey >= 1017, and x itself must be normal: hx >= max(1017 - e, 1) << 20
+    const int lo = 1017 - cr.e;
+    cr.thr = cr.bad ? 0xFFFFFFFFu : static_cast<uint32_t>(lo > 1 ? lo : 1) << 20;
+    cr.add = static_cast<uint32_t>((cr.e - 1016) * (1 << 20) + 0x1FFFF);
+    return cr;
+}
+
+// RU_e4m3(|x| 2^e) as a code for a common element (|hi(x)| >= thr): hy = hx + (e << 20) is the
+// high word of y; its top 3 significand bits rounded up (sticky = the other 49 bits, via +0x1FFFF
+// and min(lx, 1)) are (hy >> 17) - (1016 << 3) = (E + 7) 8 + M3, the code (R4).
+__device__ __forceinline__ uint32_t cast_code(uint32_t hx, uint32_t lx, uint32_t add) {
+    return (hx + add + min(lx, 1u)) >> 17;
+}
+
+template <bool I8>
+__device__ __forceinline__ uint32_t cast_code_slow(double x, const CastRow& cr) {
+    if (x == 0.0 || cr.bad) return 0u;
+    const double s1 = pow2d(cr.e >> 1), s2 = pow2d(cr.e - (cr.e >> 1));   // 2^e in two exact steps
+    if (I8) return static_cast<uint32_t>(ceil((fabs(x) * s1) * s2));     // exact: <= 2^7 scaled
+    const uint32_t c = fp8_ru_code((fabs(x) * s1) * s2);                  // E4M3 subnormal grid
+    return c ? c : 1u;            // an underflowed nonzero still rounds up to 2^-9
+}
+
+// the 16 codes of a lane (c), squares added to *sq (FAST)
+template <bool FAST, bool I8>
+__device__ __forceinline__ void cast16(const double (&x)[kCastH], const CastRow& cr, uint32_t (&c)[kCastH],
+                                       unsigned long long* sq) {
+    bool slow = false;
+#pragma unroll
+    for (int q = 0; q < kCastH; ++q) {
+        const uint32_t hx = static_cast<uint32_t>(__double2hiint(x[q])) & 0x7FFFFFFFu;
+        const uint32_t lx = static_cast<uint32_t>(__double2loint(x[q]));
+        c[q] = cast_code(hx, lx, cr.add);
+        slow |= I8 || hx < cr.thr;
+    }
+    if (slow) {
+#pragma unroll
+        for (int q = 0; q < kCastH; ++q) {
+            const uint32_t hx = static_cast<uint32_t>(__double2hiint(x[q])) & 0x7FFFFFFFu;
+            if (I8 || hx < cr.thr) c[q] = cast_code_slow<I8>(x[q], cr);
+        }
+    }
+    if (FAST) {
+        unsigned long long s = 0;
+#pragma unroll
+        for (int q = 0; q < kCastH; ++q) s += I8 ? static_cast<unsigned long long>(c[q] * c[q]) : fp8_sq_units(c[q]);
+        *sq += s;
+    }
+}
+
+template <bool KMAJOR, bool FAST, bool I8, bool VEC>
 __global__ void __launch_bounds__(256) k_cast(const double* __restrict__ X, int64_t rows, int64_t k,
                                               int64_t ld, const unsigned long long* __restrict__ maxbits,
                                               int32_t* __restrict__ eprime, uint8_t* __restrict__ xbar,
                                               int gplanes, int64_t k_pad,
                                               int32_t* __restrict__ status,
                                               unsigned long long* __restrict__ sumsq) {
-    __shared__ double tile[TR * TP];
-    const int64_t h0 = static_cast<int64_t>(blockIdx.x) * TH;
-    const int64_t r0 = static_cast<int64_t>(blockIdx.y) * TR;
-    load_tile<KMAJOR>(X, rows, k, ld, r0, h0, tile);
-    __syncthreads();
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    if (blockIdx.x == 0 && t < TR) {
-        const int64_t r = r0 + t;
-        if (r < rows) {
-            const unsigned long long mb = maxbits[r];
-            eprime[r] = eprime_of<I8>(mb);
-            if (mb >= 0x7FF0000000000000ull) atomicOr(status, 1);
+    // MN-major: the lane's row, its 16 consecutive k from h; K-major: the warp's row, the
+    // lane's 8 pairs of consecutive k at h + 64 j (each 16-byte load of the warp is one
+    // coalesced 512-byte run, each 2-byte store one 64-byte run)
+    int64_t r, h;
+    if (!KMAJOR) {
+        r = static_cast<int64_t>(blockIdx.x) * 32 + lane;
+        h = static_cast<int64_t>(blockIdx.y) * TH + w * kCastH;
+    } else {
+        r = static_cast<int64_t>(blockIdx.x) * 8 + w;
+        h = static_cast<int64_t>(blockIdx.y) * (32 * kCastH) + 2 * lane;
+    }
+    const unsigned long long mb = (r < rows) ? maxbits[r] : 0ull;
+    const CastRow cr = cast_row<I8>(mb);
+    if (blockIdx.y == 0 && (KMAJOR ? lane == 0 : w == 0) && r < rows) {
+        eprime[r] = cr.e;
+        if (cr.bad) atomicOr(status, 1);
+    }
+    double x[kCastH];
+    if (!KMAJOR) {
+        const double* p = X + r + h * ld;
+        if (r < rows && h + kCastH <= k) {
+#pragma unroll
+            for (int q = 0; q < kCastH; ++q) x[q] = __ldg(p + q * ld);
+        } else {
+#pragma unroll
+            for (int q = 0; q < kCastH; ++q) x[q] = (r < rows && h + q < k) ? __ldg(p + q * ld) : 0.0;
+        }
+    } else {
+        const double* p = X + r * ld + h;
+        if (VEC && r < rows && h + 64 * (kCastH / 2 - 1) + 2 <= k) {
+#pragma unroll
+            for (int j = 0; j < kCastH / 2; ++j) {
+                const double2 v = __ldg(reinterpret_cast<const double2*>(p + 64 * j));
+                x[2 * j] = v.x;
+                x[2 * j + 1] = v.y;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < kCastH / 2; ++j) {
+                const int64_t hj = h + 64 * j;
+                x[2 * j] = (r < rows && hj < k) ? __ldg(p + 64 * j) : 0.0;
+                x[2 * j + 1] = (r < rows && hj + 1 < k) ? __ldg(p + 64 * j + 1) : 0.0;
+            }
         }
     }
-    // warp w handles rows w, w+8, w+16, w+24; lane covers 4 consecutive h
-#pragma unroll
-    for (int j = 0; j < TR / 8; ++j) {
-        const int rr = w + 8 * j;
-        const int64_t r = r0 + rr;
-        const unsigned long long mbr = (r < rows) ? maxbits[r] : 0ull;
-        const int e = eprime_of<I8>(mbr);
-        const bool bad = mbr >= 0x7FF0000000000000ull;     // NaN / Inf row: zero bounds, so it
-                                                           // cannot disturb other rows' exponents (R12)
-        const double s1 = pow2d(e >> 1), s2 = pow2d(e - (e >> 1));   // 2^e in two exact steps
-        uint32_t word = 0;
-        unsigned long long sq = 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const double x = tile[rr * TP + lane * 4 + q];
-            uint32_t c = 0;
-            if (x != 0.0 && !bad) {
-                if (I8) {
-                    c = static_cast<uint32_t>(ceil((fabs(x) * s1) * s2));   // exact: < 2^7 scaled
-                } else {
-                    // RU_e4m3(|x| 2^e) on the integer pipes (no F2F): in the E4M3 normal range
-                    // y = |x| 2^e >= 2^-6 the scaling is an exponent-field add and the round-up
-                    // to 3 significand bits an add of the sticky bit at bit 49
-                    const uint32_t hx = static_cast<uint32_t>(__double2hiint(x)) & 0x7FFFFFFFu;
-                    const uint32_t lx = static_cast<uint32_t>(__double2loint(x));
-                    const int ey = static_cast<int>(hx >> 20) + e;
-                    if ((hx >> 20) != 0u && ey >= 1017) {
-                        const uint32_t hy = hx + (static_cast<uint32_t>(e) << 20);
-                        const uint32_t sticky = ((hy & 0x1FFFFu) | lx) != 0u ? 0x20000u : 0u;
-                        c = (((hy & ~0x1FFFFu) + sticky) >> 17) - 8128u;     // (E + 7) 8 + M3
-                    } else {
-                        c = fp8_ru_code((fabs(x) * s1) * s2);   // E4M3 subnormal grid (or tiny x)
-                        c = c ? c : 1u;           // an underflowed nonzero still rounds up to 2^-9
-                    }
-                }
-            }
-            if (FAST) sq += I8 ? static_cast<unsigned long long>(c * c) : fp8_sq_units(c);
-            else word |= c << (8 * q);
-        }
-        if (FAST) {
+    unsigned long long sq = 0;
+    uint32_t c[kCastH];
+    cast16<FAST, I8>(x, cr, c, &sq);
+    if (FAST) {
+        if (KMAJOR) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
             if (lane == 0 && sq && r < rows) atomicAdd(sumsq + r, sq);
         } else {
-            *reinterpret_cast<uint32_t*>(xbar + chunk_offset(r, blockIdx.x, gplanes, k_pad) + lane * 4) = word;
+            // the 8 warps share the block's 32 rows: one atomic per row and block
+            __shared__ unsigned long long part[8][32];
+            part[w][lane] = sq;
+            __syncthreads();
+            if (w == 0) {
+#pragma unroll
+                for (int v = 1; v < 8; ++v) sq += part[v][lane];
+                if (sq && r < rows) atomicAdd(sumsq + r, sq);
+            }
+        }
+    } else if (!KMAJOR) {
+        // 16 codes of one 128-byte chunk (h mod 128 is a multiple of 16), padding included:
+        // the buffer is reused across calls
+        uint4 word;
+        word.x = c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24);
+        word.y = c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24);
+        word.z = c[8] | (c[9] << 8) | (c[10] << 16) | (c[11] << 24);
+        word.w = c[12] | (c[13] << 8) | (c[14] << 16) | (c[15] << 24);
+        *reinterpret_cast<uint4*>(xbar + chunk_offset(r, static_cast<uint32_t>(h / TH), gplanes, k_pad) + (h % TH)) =
+            word;
+    } else {
+#pragma unroll
+        for (int j = 0; j < kCastH / 2; ++j) {
+            const int64_t hj = h + 64 * j;      // up to round_up(k, 512) <= k_pad (padding: zero codes)
+            *reinterpret_cast<uint16_t*>(xbar + chunk_offset(r, static_cast<uint32_t>(hj / TH), gplanes, k_pad) +
+                                         (hj % TH)) = static_cast<uint16_t>(c[2 * j] | (c[2 * j + 1] << 8));
         }
     }
 }
@@ -782,19 +880,23 @@ cudaError_t launch_cast(const double* X, int64_t rows, int64_t k, int64_t ld, bo
                         const unsigned long long* maxbits, int32_t* eprime, uint8_t* xbar, int gplanes,
                         int64_t rows_pad, int64_t k_pad, int32_t* status,
                         unsigned long long* sumsq, bool i8, cudaStream_t st) {
-    // K tiles up to round_up(k, 128): beyond that the layout's padding is never read
-    dim3 grid(static_cast<unsigned>((k + TH - 1) / TH), static_cast<unsigned>(rows_pad / TR));
-#define OZ2_CAST(KM, FA, I8_) k_cast<KM, FA, I8_><<<grid, 256, 0, st>>>(X, rows, k, ld, maxbits, eprime, xbar, gplanes, k_pad, status, sumsq)
-    const int sel = (kmajor ? 4 : 0) | (sumsq ? 2 : 0) | (i8 ? 1 : 0);
-    switch (sel) {
-        case 0: OZ2_CAST(false, false, false); break;
-        case 1: OZ2_CAST(false, false, true); break;
-        case 2: OZ2_CAST(false, true, false); break;
-        case 3: OZ2_CAST(false, true, true); break;
-        case 4: OZ2_CAST(true, false, false); break;
-        case 5: OZ2_CAST(true, false, true); break;
-        case 6: OZ2_CAST(true, true, false); break;
-        default: OZ2_CAST(true, true, true); break;
+    if (rows_pad == 0 || k == 0) return cudaSuccess;
+    // K tiles up to round_up(k, 128) (MN-major) or round_up(k, 512) (K-major, inside k_pad, a
+    // multiple of 2048): beyond round_up(k, 128) the layout's padding is never read
+    const bool vec = (reinterpret_cast<uintptr_t>(X) & 15u) == 0 && (ld & 1) == 0;
+    const dim3 grid = kmajor ? dim3(static_cast<unsigned>(rows_pad / 8), static_cast<unsigned>((k + 511) / 512))
+                             : dim3(static_cast<unsigned>(rows_pad / 32), static_cast<unsigned>((k + TH - 1) / TH));
+#define OZ2_CAST(KM, FA, I8_, V) k_cast<KM, FA, I8_, V><<<grid, 256, 0, st>>>(X, rows, k, ld, maxbits, eprime, xbar, gplanes, k_pad, status, sumsq)
+    const bool fa = sumsq != nullptr;
+    if (!kmajor) {
+        if (fa) { if (i8) OZ2_CAST(false, true, true, false); else OZ2_CAST(false, true, false, false); }
+        else { if (i8) OZ2_CAST(false, false, true, false); else OZ2_CAST(false, false, false, false); }
+    } else if (vec) {
+        if (fa) { if (i8) OZ2_CAST(true, true, true, true); else OZ2_CAST(true, true, false, true); }
+        else { if (i8) OZ2_CAST(true, false, true, true); else OZ2_CAST(true, false, false, true); }
+    } else {
+        if (fa) { if (i8) OZ2_CAST(true, true, true, false); else OZ2_CAST(true, true, false, false); }
+        else { if (i8) OZ2_CAST(true, false, true, false); else OZ2_CAST(true, false, false, false); }
     }
 #undef OZ2_CAST
     return cudaGetLastError();

@@ -30,7 +30,7 @@ TUNE = {
     "cta_group": 0, "sync_lead": 1, "sync_chunk": 2, "l2_promo": 3, "max_units": 4,
     "tma_hint_a": 5, "tma_hint_b": 6, "mod_split": 7, "fused_crt": 8, "sq_order": 9,
     "crt_generic": 10, "host_blocks": 11, "kcat": 12, "prescale_2read": 13,
-    "epi_sleep": 14, "digits_fma": 15,
+    "epi_sleep": 14, "digits_fma": 15, "tile_n": 16,
 }
 
 _c_int64 = ctypes.c_int64

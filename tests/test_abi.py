@@ -186,6 +186,8 @@ def test_tuning_knobs_host_only(oz2mod):
     assert P.oz2_set_tuning("cta_group", 3) == -2
     assert P.oz2_set_tuning(99, 1) == -1
     assert P.oz2_set_tuning("sync_chunk", 0) == -2
+    assert P.oz2_set_tuning("tile_n", 384) == -2 and P.oz2_set_tuning("tile_n", 128) == -2
+    assert len(P.TUNE) == 17 and P.TUNE["tile_n"] == 16
     assert P.oz2_set_tuning("cta_group", 1) == 0 and P.oz2_get_tuning("cta_group") == 1
     with P.tuning(mod_split=2, fused_crt=0):
         assert P.oz2_get_tuning("mod_split") == 2 and P.oz2_get_tuning("fused_crt") == 0

@@ -690,7 +690,9 @@ B = gen_device(k, n, "phi", phi=1.0, seed=92)
 C = torch.empty((n, m), dtype=torch.float64, device="cuda").t()
 P.oz2_set_stream(torch.cuda.current_stream().cuda_stream)
 assert P.oz2_set_scheme(sch) == 0
-assert P.oz2_set_tuning("cta_group", int(sys.argv[2])) == 0
+assert P.oz2_set_tuning("cta_group", int(sys.argv[2].rstrip("w"))) == 0
+if sys.argv[2].endswith("w"):      # 256 x 512 CTA-pair tiles (FP8 kinds; INT8 keeps 256)
+    assert P.oz2_set_tuning("tile_n", 512) == 0
 for split in ("0", "1", "2"):
     assert P.oz2_set_tuning("mod_split", int(split)) == 0
     assert P.oz2_dgemm("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0, C.data_ptr(), m, 13) == 0
@@ -702,7 +704,8 @@ for split in ("0", "1", "2"):
 @pytest.mark.parametrize("sch", ["fp8", "int8", "karatsuba"])
 def test_gemm_variants_identical(dev, sch):
     """CTA group 1 (128x256 CTAs), 2 (CTA pairs, default), 4 (two pairs multicasting A; FP8
-    kinds only, INT8 falls back to pairs) give identical C under all three work-item
+    kinds only, INT8 falls back to pairs), 2 with 256x512 tiles (OZ2_TUNE_TILE_N = 512; FP8
+    kinds, K-concatenated square products at this k) give identical C under all three work-item
     schedules, and that C is the oracle's on one sampled entry per 256 x 256 tile.  Each
     variant runs in a subprocess with a timeout, so a pipeline hang fails the test."""
     import hashlib
@@ -714,12 +717,12 @@ def test_gemm_variants_identical(dev, sch):
     from synth import gen_device
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = {}
-    for cg in ["1", "2", "4"]:
+    for cg in ["1", "2", "4", "2w"]:
         r = subprocess.run([sys.executable, "-c", _CG_SNIPPET, sch, cg], cwd=root,
                            capture_output=True, text=True, timeout=240)
         assert r.returncode == 0, r.stderr[-2000:]
         outs[cg] = r.stdout.split()
-    assert outs["1"] == outs["2"] == outs["4"]
+    assert outs["1"] == outs["2"] == outs["4"] == outs["2w"]
     assert outs["2"][1] == outs["2"][3] == outs["2"][5]   # tile-major, split and hybrid agree
     # the same problem in-process (default kernels) with exponent outputs -> the oracle
     m, n, k = 2560, 2560, 1024
@@ -806,3 +809,53 @@ def test_kcat_on_off_identical_many_tiles(dev, sch, knobs):
     for o in outs[1:]:
         assert np.array_equal(o["residues"], outs[0]["residues"])
         assert np.array_equal(o["C"], outs[0]["C"])
+
+
+_W512_SNIPPET = r"""
+import hashlib, sys
+import numpy as np, torch
+sys.path.insert(0, ".")
+import paper_2603_10634_b200 as P
+from synth import gen_device
+sch, m, n, k, N = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5])
+A = gen_device(m, k, "phi", phi=1.0, seed=93)
+B = gen_device(k, n, "phi", phi=1.0, seed=94)
+P.oz2_set_stream(torch.cuda.current_stream().cuda_stream)
+assert P.oz2_set_scheme(sch) == 0
+for tn in (256, 512):
+    assert P.oz2_set_tuning("tile_n", tn) == 0
+    for fused in (-1, 0):
+        assert P.oz2_set_tuning("fused_crt", fused) == 0
+        C = torch.full((n, m), 7.0, dtype=torch.float64, device="cuda").t()
+        res = torch.zeros(N * m * n, dtype=torch.int16, device="cuda")
+        opt = P.oz2_options()
+        opt.residues = res.data_ptr()
+        assert P.oz2_dgemm_ex("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.0,
+                              C.data_ptr(), m, N, opt) == 0
+        torch.cuda.synchronize()
+        h = hashlib.sha256(C.cpu().numpy().tobytes() + res.cpu().numpy().tobytes()).hexdigest()
+        print(tn, fused, h)
+"""
+
+
+@pytest.mark.parametrize("sch,m,n,k,N", [
+    ("fp8", 1000, 1300, 16500, 13),      # fused CRT (k >= 16384), ragged m, n, k; last R half partly outside n
+    ("fp8", 520, 700, 70000, 12),        # two 2^16 K segments per product
+    ("karatsuba", 777, 1536, 16384, 13),
+    ("fp8", 300, 2000, 1500, 20),        # K-concatenated square products (k <= 2048), 6-limb CRT
+])
+def test_tile_n512_identical(sch, m, n, k, N):
+    """256 x 512 CTA-pair tiles (OZ2_TUNE_TILE_N = 512) give the same residues and C as the
+    default 256 x 256 tiles, bit for bit, with the fused and the separate CRT (the default
+    tiles are pinned to the oracle by the tests above).  Subprocess with a timeout: a
+    pipeline hang fails the test instead of blocking the suite."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _W512_SNIPPET, sch, str(m), str(n), str(k), str(N)],
+                       cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln.split() for ln in r.stdout.strip().splitlines()]
+    assert len(lines) == 4
+    assert len({ln[2] for ln in lines}) == 1, lines

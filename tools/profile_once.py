@@ -1,4 +1,7 @@
-"""Run the pipeline a few times at one size (for ncu launch lists / captures)."""
+"""Run the pipeline a few times at one size (for ncu launch lists / captures).
+
+    python tools/profile_once.py [n] [N] [reps] [scheme] [mode] ["knob=v,knob=v"]
+"""
 import sys
 import torch
 sys.path.insert(0, ".")
@@ -10,6 +13,10 @@ N = int(sys.argv[2]) if len(sys.argv) > 2 else 13
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 scheme = sys.argv[4] if len(sys.argv) > 4 else "fp8"
 mode = sys.argv[5] if len(sys.argv) > 5 else "accurate"
+knobs = sys.argv[6] if len(sys.argv) > 6 else ""     # "knob=v,knob=v" (oz2_set_tuning)
+for kv in filter(None, knobs.split(",")):
+    kn, v = kv.split("=")
+    assert P.oz2_set_tuning(kn, int(v)) == 0, kv
 A = gen_device(n, n, "phi", phi=1.0, seed=1)
 B = gen_device(n, n, "phi", phi=1.0, seed=2)
 C = torch.empty((n, n), dtype=torch.float64, device="cuda").t()
