@@ -48,7 +48,8 @@ namespace oz2 {
 // K step share the staged A tile (25 % fewer operand bytes per MAC moved L2 -> SM), the two
 // 256-column accumulators are the L and R halves of the tile (no double buffer: the next
 // product's L half starts as soon as L is drained, see the MMA issuer), and each epilogue
-// thread keeps the partial residues of its 128 R columns in shared memory (kPartBytes).
+// thread keeps the partial residues of its 128 R columns in shared memory (PART_BYTES);
+// measured slower than W = 1 (profiles/round2_tile512.md), selected only by OZ2_TUNE_TILE_N.
 template <int CG, int W = 1>
 struct GemmCfg {
     static constexpr int TILE_M = BM * CG;            // output rows per (cluster) tile
