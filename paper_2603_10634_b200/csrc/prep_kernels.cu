@@ -764,20 +764,26 @@ __global__ void __launch_bounds__(256, 6) k_digits(const double* __restrict__ X,
     constexpr int kLPR = TH / kEPL, kRPW = 32 / kLPR;
     static_assert(kRPW == 1, "one row per warp: the per-row path choice below is warp-uniform");
     const int lrow = lane / kLPR, hl = (lane % kLPR) * kEPL;
+    // the block's 32 rows lie in one 128-row block of the layout (TR divides kRowBlk), so a
+    // row's slab offset is the tile's plus rr S (row stride S inside a plane slab)
+    static_assert(kRowBlk % TR == 0, "a conversion tile must not straddle 128-row blocks");
+    uint8_t* const out0 = planes + chunk_offset_planes<SUP>(r0, blockIdx.x, dp.num_planes, k_pad) + hl;
+    const int row_stride = SUP ? kSuper : static_cast<int>(k_pad);
+    const int rows_i = static_cast<int>(rows), r0i = static_cast<int>(r0);   // rows < 2^21 (kMaxRows)
 #pragma unroll 1
     for (int j = 0; j < TR / (8 * kRPW); ++j) {
         const int rr = (j * 8 + w) * kRPW + lrow;
-        const int64_t r = r0 + rr;
-        int e = (r < rows) ? e_scale[r] : 0;
+        const int r = r0i + rr;
+        int e = (r < rows_i) ? e_scale[r] : 0;
         if (e == kExpNonFinite) e = 0;                    // NaN / Inf row: C gets NaN (R12)
         // plane x of this (row, super-chunk) at out + x S: immediate store offsets (SUP)
-        uint8_t* out = planes + chunk_offset_planes<SUP>(r, blockIdx.x, dp.num_planes, k_pad) + hl;
+        uint8_t* out = out0 + rr * row_stride;
         // Common case, decided per row from step 1's row maximum: |X'| < 2^52 and 2^e a
         // normal double.  Then trunc(x 2^e) is ONE fused multiply-add rounded toward zero,
         // fma.rz(x, 2^e, +-2^52) - (+-2^52) with the sign of x (|x 2^e| + 2^52 lies in
         // [2^52, 2^53) where the ulp is 1), and |X'| < 2^52 < lim1 admits the paired residues.
         {
-            const unsigned long long mb = !maxbits ? ~0ull : (r < rows ? maxbits[r] : 0ull);   // padding rows: zero
+            const unsigned long long mb = !maxbits ? ~0ull : (r < rows_i ? maxbits[r] : 0ull);   // padding rows: zero
             const bool fast = mb == 0ull || (mb < 0x7FF0000000000000ull && e >= -1022 && e <= 1023 &&
                                              ilog2_bits(mb) + e <= 51);
             if (fast && NMOD > 0) {
@@ -795,21 +801,30 @@ __global__ void __launch_bounds__(256, 6) k_digits(const double* __restrict__ X,
                 continue;
             }
         }
-        const double s1 = pow2d(e >> 1), s2 = pow2d(e - (e >> 1));
         double y[kEPL], M[kEPL];
         int E[kEPL];
-        double amax = 0.0;
+        // X' = trunc(2^e x) (eq. def:A'): the scaling is exact (one multiply when 2^e is a
+        // normal double -- warp-uniform, the warp holds one row -- else two), the truncation
+        // one FRND.F64.TRUNC; the reduction depth is chosen from the largest high word (for
+        // non-negative doubles a >= lim iff hi(a) >= hi(lim) when lim's low word is zero, as
+        // for lim = 2^50 p_min and 2^86 p_min; otherwise the test is conservative)
+        uint32_t amax_hi = 0;
+        if (e >= -1022 && e <= 1023) {
+            const double sc = pow2d(e);
 #pragma unroll
-        for (int q = 0; q < kEPL; ++q) {
-            const double v = (tile[rr * TP + hl + q] * s1) * s2;           // exact (eq. def:A')
-            double a = fabs(v);
-            if (a < 4503599627370496.0) a = __dadd_rz(a, 4503599627370496.0) - 4503599627370496.0;  // trunc
-            y[q] = copysign(a, v);
-            amax = fmax(amax, a);
+            for (int q = 0; q < kEPL; ++q) y[q] = trunc(tile[rr * TP + hl + q] * sc);
+        } else {
+            const double s1 = pow2d(e >> 1), s2 = pow2d(e - (e >> 1));
+#pragma unroll
+            for (int q = 0; q < kEPL; ++q) y[q] = trunc((tile[rr * TP + hl + q] * s1) * s2);
         }
-        // warp-uniform choice of the reduction depth
-        const bool need2 = __any_sync(0xffffffffu, amax >= dp.lim1);   // 2^50 p_min (~2^59 hybrid)
-        const bool need0 = __any_sync(0xffffffffu, amax >= dp.lim2);   // 2^86 p_min
+#pragma unroll
+        for (int q = 0; q < kEPL; ++q)
+            amax_hi = max(amax_hi, static_cast<uint32_t>(__double2hiint(y[q])) & 0x7FFFFFFFu);
+        // warp-uniform choice of the reduction depth (a NaN / Inf row takes the deepest path;
+        // its entries of C are NaN whatever its digits, R12)
+        const bool need2 = __any_sync(0xffffffffu, amax_hi >= static_cast<uint32_t>(__double2hiint(dp.lim1)));
+        const bool need0 = __any_sync(0xffffffffu, amax_hi >= static_cast<uint32_t>(__double2hiint(dp.lim2)));
         if (need0) {
             // |X'| = M 2^E with M < 2^53 an integer (E = 0 below 2^53)
 #pragma unroll

@@ -147,3 +147,27 @@ def test_digits_fma_fast_path_blocked():
         P.oz2_reset_tuning()
         P.oz2_set_blocking(0, 0)
     assert np.array_equal(ref["C"], blk["C"])
+
+
+@pytest.mark.parametrize("transa,transb", [("N", "N"), ("T", "N"), ("N", "T"), ("T", "T")])
+@pytest.mark.parametrize("k", [701, 2300])
+@pytest.mark.parametrize("sch", ["fp8", "int8"])
+def test_two_read_cast_matches_oracle(transa, transb, k, sch):
+    """The default step 1 (k_rowmax, then k_cast: a lane casts 16 consecutive k of a row with
+    the integer E4M3 round-up; zeros, sub-2^-6 results and subnormal inputs on the slow path)
+    against the oracle's prescale: e' and A-bar / B-bar bit-exact for both storage orders of
+    both operands, k odd (K-major operands then have an odd leading dimension: scalar loads)
+    and even (16-byte loads), wide exponent spread with zero / huge / subnormal outliers."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    m, n = 97, 70
+    A = _wide(m, k, 15)
+    B = _wide(n, k, 16).T.copy()
+    res = _run(A, B, 13 if sch == "fp8" else 15, True, transa, transb, scheme_name=sch)
+    pre = scheme.prescale_rows if sch == "fp8" else oint8.prescale_rows
+    epa, abar = pre(A)
+    epb, bbar = pre(B.T)
+    assert res["e_prime_a"].tolist() == list(epa) and res["e_prime_b"].tolist() == list(epb)
+    assert np.array_equal(res["abar"].astype(np.int64), np.asarray(abar).astype(np.int64))
+    assert np.array_equal(res["bbar"].astype(np.int64), np.asarray(bbar).astype(np.int64))
