@@ -859,3 +859,67 @@ def test_tile_n512_identical(sch, m, n, k, N):
     lines = [ln.split() for ln in r.stdout.strip().splitlines()]
     assert len(lines) == 4
     assert len({ln[2] for ln in lines}) == 1, lines
+
+
+_CANARY_SNIPPET = r"""
+import sys
+import numpy as np, torch
+sys.path.insert(0, ".")
+import paper_2603_10634_b200 as P
+from synth import gen_device
+ta, tb, m, n, k, N, sch, mode, tile_n, blocked = sys.argv[1], sys.argv[2], *map(int, sys.argv[3:7]), sys.argv[7], sys.argv[8], int(sys.argv[9]), int(sys.argv[10])
+A = gen_device(m, k, "phi", phi=1.0, seed=71)
+B = gen_device(k, n, "phi", phi=1.0, seed=72)
+Ast, lda = (A.t().contiguous().t(), m) if ta == "N" else (A.contiguous(), k)
+Bst, ldb = (B.t().contiguous().t(), k) if tb == "N" else (B.contiguous(), n)
+ldc = m + 5
+Cbuf = torch.full((n, ldc), 3.25, dtype=torch.float64, device="cuda")
+assert P.oz2_set_scheme(sch) == 0 and P.oz2_set_mode(mode) == 0
+assert P.oz2_set_tuning("tile_n", tile_n) == 0
+need = P.oz2_workspace_size(ta, tb, m, n, k, N)
+if blocked:                                 # a third of the unblocked workspace: m/n blocking
+    need = need // 3
+GUARD = 1 << 20
+ws = torch.full((need + 2 * GUARD,), 0xA5, dtype=torch.uint8, device="cuda")
+P.oz2_set_workspace(ws.data_ptr() + GUARD, need)
+P.oz2_set_stream(torch.cuda.current_stream().cuda_stream)
+a0, b0 = Ast.clone(), Bst.clone()
+rc = P.oz2_dgemm(ta, tb, m, n, k, 1.0, Ast.data_ptr(), lda, Bst.data_ptr(), ldb, 0.0, Cbuf.data_ptr(), ldc, N)
+torch.cuda.synchronize()
+assert rc == 0, rc
+assert bool((ws[:GUARD] == 0xA5).all()), "workspace head guard written"
+assert bool((ws[GUARD + need:] == 0xA5).all()), "workspace tail guard written"
+assert torch.equal(Ast, a0) and torch.equal(Bst, b0), "inputs modified"
+assert bool((Cbuf[:, m:] == 3.25).all()), "ldc padding written"
+C = Cbuf[:, :m].t()
+ref = A @ B
+rel = (torch.linalg.norm(C - ref) / torch.linalg.norm(ref)).item()
+assert rel < 1e-14, rel
+print("ok", rel)
+"""
+
+
+@pytest.mark.parametrize("ta,tb,m,n,k,N,sch,mode,tile_n,blocked", [
+    ("N", "N", 300, 260, 701, 13, "fp8", "accurate", 256, 0),     # k_cast MN-major / K-major (odd ld: scalar loads)
+    ("T", "T", 300, 260, 701, 13, "fp8", "accurate", 256, 0),
+    ("T", "N", 300, 260, 2300, 13, "fp8", "accurate", 256, 0),    # 16-byte K-major loads, 2 super-chunks
+    ("N", "T", 300, 260, 701, 13, "fp8", "fast", 256, 0),         # sums of squares
+    ("T", "N", 300, 260, 701, 15, "int8", "accurate", 256, 0),
+    ("N", "N", 520, 700, 16500, 13, "fp8", "accurate", 512, 0),   # 256 x 512 tiles, fused CRT
+    ("N", "N", 1000, 900, 3000, 13, "fp8", "accurate", 256, 1),   # m/n blocking
+])
+def test_workspace_and_buffer_guards(ta, tb, m, n, k, N, sch, mode, tile_n, blocked):
+    """Bounds check of our own (compute-sanitizer is not available on the GPU pool): 1 MiB
+    guard bands of 0xA5 before and after a caller workspace of exactly the required size
+    stay untouched, the inputs are unmodified, the ldc padding of C is not written, and C
+    is accurate -- over the storage orders, odd / even k (scalar / vector loads of the
+    cast), fast mode, the INT8 scheme, 256 x 512 tiles and m/n blocking."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    args = [ta, tb, str(m), str(n), str(k), str(N), sch, mode, str(tile_n), str(blocked)]
+    r = subprocess.run([sys.executable, "-c", _CANARY_SNIPPET, *args], cwd=root,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-2000:]
+    assert r.stdout.startswith("ok")
