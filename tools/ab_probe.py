@@ -37,5 +37,6 @@ for v in vals:
     c = statistics.median(x["crt"] for x in res[v])
     ps = statistics.median(x["prescale"] for x in res[v])
     dg = statistics.median(x["digits"] for x in res[v])
+    bg = statistics.median(x["bound_gemm"] for x in res[v])
     print(f"{var}={v}: total {tot:.3f} ms ({2.0*m*n*k/tot/1e9:.2f} TFLOP/s), residue_gemm {g:.3f}, "
-          f"prescale {ps:.3f}, digits {dg:.3f}, crt {c:.3f}", flush=True)
+          f"prescale {ps:.3f}, bound_gemm {bg:.3f}, digits {dg:.3f}, crt {c:.3f}", flush=True)
