@@ -164,7 +164,7 @@ __device__ __forceinline__ unsigned long long fp8_sq_units(uint32_t c) {   // co
 // I8 (INT8 scheme, R16): X-bar = ceil(|x| 2^e') in [0, 128] as U8 (exact upper bounds),
 // squares accumulated in units of 1.
 //
-// No shared-memory staging (round 3): a lane converts kCastH = 16 consecutive k of one row.
+// No shared-memory staging (round 2, session 4): a lane converts kCastH = 16 consecutive k of a row.
 //   MN-major (X[r + h ld]): lane = row, so each of the lane's 16 loads is one coalesced 256-byte
 //     run per warp; warp w of a block takes k in [h0 + 16 w, h0 + 16 w + 16): block = 32 rows x
 //     128 k (one 128-byte chunk of the layout), grid (rows_pad / 32, ceil(k / 128)).
