@@ -82,6 +82,58 @@ __global__ void __launch_bounds__(256, 4) k_crt_n(const int16_t* __restrict__ re
     }
 }
 
+// CRT of whole tiles of the residue GEMM's tile order (the split tail of the hybrid schedule;
+// the other tiles' CRT is fused into the GEMM epilogue).  Block (x, y): tile t0 + x, thread =
+// one row of the tile, columns y, y + gridDim.y, ... of the tile.
+template <int L>
+__global__ void __launch_bounds__(256) k_crt_tiles(const int16_t* __restrict__ res, int64_t m, int64_t n,
+                                                   const __grid_constant__ CrtParams cp,
+                                                   const int32_t* __restrict__ e_mu,
+                                                   const int32_t* __restrict__ e_nu, double alpha, double beta,
+                                                   double* __restrict__ C, int64_t ldc, int t0, int G, int m_tiles,
+                                                   int n_tiles, int tile_rows, int tile_cols) {
+    __shared__ CrtShared s;
+    crt_stage_constants(&s, cp, threadIdx.x, blockDim.x);
+    __syncthreads();
+    int tm, tn;
+    tile_coords_g(t0 + static_cast<int>(blockIdx.x), G, m_tiles, n_tiles, tm, tn);
+    const int64_t lstride = n * m;
+    for (int rr = threadIdx.x; rr < tile_rows; rr += blockDim.x) {
+        const int64_t i = static_cast<int64_t>(tm) * tile_rows + rr;
+        if (i >= m) break;
+        const int emu = e_mu[i];
+        for (int jj = blockIdx.y; jj < tile_cols; jj += gridDim.y) {
+            const int64_t j = static_cast<int64_t>(tn) * tile_cols + jj;
+            if (j >= n) break;
+            const int enu = e_nu[j];
+            const double v = exps_finite(emu, enu) ? crt_element<L>(res + j * m + i, lstride, &s, cp, emu + enu, false)
+                                                   : __longlong_as_double(0x7FF8000000000000ll);
+            store_alpha_beta(C + i + j * ldc, v, alpha, beta);
+        }
+    }
+}
+
+cudaError_t launch_crt_tiles(int limbs, const int16_t* res, int64_t m, int64_t n, const CrtParams& cp,
+                             const int32_t* e_mu, const int32_t* e_nu, double alpha, double beta, double* C,
+                             int64_t ldc, int t0, int count, int G, int m_tiles, int n_tiles, int tile_rows,
+                             int tile_cols, cudaStream_t st) {
+    if (count <= 0 || m == 0 || n == 0) return cudaSuccess;
+    const dim3 grid(static_cast<unsigned>(count), 32u);
+#define OZ2_CRTT_CASE(LL)                                                                                     \
+    case LL:                                                                                                  \
+        k_crt_tiles<LL><<<grid, 256, 0, st>>>(res, m, n, cp, e_mu, e_nu, alpha, beta, C, ldc, t0, G, m_tiles, \
+                                              n_tiles, tile_rows, tile_cols);                                 \
+        break;
+    switch (limbs) {
+        OZ2_CRTT_CASE(4)
+        OZ2_CRTT_CASE(5)
+        OZ2_CRTT_CASE(6)
+        default: return cudaErrorInvalidValue;    // the fused CRT (hence this tail) needs <= 6 limbs
+    }
+#undef OZ2_CRTT_CASE
+    return cudaGetLastError();
+}
+
 // debug output: the stored u_l in [0, p_l) back to the symmetric range of C'_l (R2)
 __global__ void k_res_symmetric(int16_t* __restrict__ out, const int16_t* __restrict__ in, int64_t per,
                                 const __grid_constant__ CrtParams cp) {

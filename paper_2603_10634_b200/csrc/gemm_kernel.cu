@@ -65,15 +65,9 @@ struct GemmCfg {
 
 template <int G>
 __device__ __forceinline__ void tile_coords(int t, int m_tiles, int n_tiles, int& tm, int& tn) {
-    // groups of G tile-rows swept column by column: the ~148 concurrently running tiles
-    // cover a near-square 2048 x ~2300 block of C, so the A and B panels they stream are
-    // shared in L2 (G x TILE_M = 2048 rows for both CTA-group sizes)
-    const int group = t / (G * n_tiles);
-    const int first_m = group * G;
-    const int gm = min(G, m_tiles - first_m);
-    const int in = t - group * G * n_tiles;
-    tm = first_m + in % gm;
-    tn = in / gm;
+    // groups of G tile-rows swept column by column (oz2_internal.h): G x TILE_M = 2048 rows
+    // for both CTA-group sizes
+    tile_coords_g(t, G, m_tiles, n_tiles, tm, tn);
 }
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -581,7 +575,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                       }
                     }
                 }
-                if (FL > 0) {
+                if (FL > 0 && it < head) {   // split tail items: their CRT runs in k_crt_tiles
                     crt_steps(TCOLS);
                     crt_row = row;
                     crt_col0 = col0;
@@ -667,7 +661,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                       }
                     }
                 }
-                if (FL > 0) {
+                if (FL > 0 && it < head) {   // split tail items: their CRT runs in k_crt_tiles
                     crt_steps(TCOLS);             // finish the previous tile if still pending
                     crt_row = row;                // this tile's CRT is spread over the next tile
                     crt_col0 = col0;

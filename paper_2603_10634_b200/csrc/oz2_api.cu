@@ -883,14 +883,15 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
                 const int64_t waves = (tiles + units - 1) / units;
                 const bool ragged = full < tiles && static_cast<double>(waves * units - tiles) > 0.005 * waves * units;
                 int ms = tune(OZ2_TUNE_MOD_SPLIT);
-                // hybrid only where the CRT runs separately anyway: giving up the fused CRT
-                // for the tail costs more than the tail (A/B: FP8 16384^3 -1.5 %, 8192^3 +3.4 %)
-                if (ms < 0) ms = tiles < 8 * units ? 1 : (ragged && !fused ? 2 : 0);
+                // hybrid also with the fused CRT (round 2): the head tiles keep their fused CRT,
+                // the split tail's tiles get theirs from k_crt_tiles after the GEMM
+                if (ms < 0) ms = tiles < 8 * units ? 1 : (ragged ? 2 : 0);
                 gp.tail_head = static_cast<int>(ms == 1 ? 0 : ms == 2 ? full : tiles);
             }
-            // the fused CRT needs every modulus of a tile in one item
+            // the fused CRT needs every modulus of a tile in one item: it covers the tile-major
+            // head items [0, tail_head); the split tail's CRT runs in k_crt_tiles below
             const int n_tiles_blk = gp.m_tiles * gp.n_tiles / (cg == 4 ? 2 : 1);
-            const int fused_blk = gp.tail_head < n_tiles_blk ? 0 : fused;
+            const int fused_blk = gp.tail_head == 0 ? 0 : fused;
             gp.residues = res;
             gp.sync_lead = sync_lead();
             gp.sync_chunk = sync_chunk;
@@ -924,6 +925,10 @@ static int run_device(bool a_kmajor, bool b_kmajor, int64_t m, int64_t n, int64_
             if (!fused_blk)
                 OZ2_CK(launch_crt(pl->L, res, mbi, nbj, pl->crt, e_mu + i0, e_nu + j0, alpha, beta, Cij, ldc,
                                   tune(OZ2_TUNE_CRT_GENERIC) != 0, st));
+            else if (gp.tail_head < n_tiles_blk)
+                OZ2_CK(launch_crt_tiles(pl->L, res, mbi, nbj, pl->crt, e_mu + i0, e_nu + j0, alpha, beta, Cij, ldc,
+                                        gp.tail_head, n_tiles_blk - gp.tail_head, 16 / (cg == 1 ? 1 : 2), gp.m_tiles,
+                                        gp.n_tiles / (cg == 4 ? 2 : 1), tile_m(cg), tile_n * (cg == 4 ? 2 : 1), st));
         }
         if (hook && hook->done) {
             const int hr = hook->done(hook->ctx, j0, nbj);

@@ -55,6 +55,19 @@ __host__ __device__ inline int64_t plane_offset(int64_t r, int64_t h, int x, int
     return ((((r / kRowBlk) * KS + h / S) * gplanes + x) * kRowBlk + (r % kRowBlk)) * S + h % S;
 }
 
+// Persistent-GEMM tile order: groups of G tile-rows swept column by column (the ~148
+// concurrently running tiles cover a near-square block of C and share their A and B panels
+// in L2).  t -> (tile row tm, tile column tn) of a grid of m_tiles x n_tiles tiles.  Shared by
+// the GEMM kernels and the tail-tile CRT (k_crt_tiles) of the hybrid schedule.
+__host__ __device__ __forceinline__ void tile_coords_g(int t, int G, int m_tiles, int n_tiles, int& tm, int& tn) {
+    const int group = t / (G * n_tiles);
+    const int first_m = group * G;
+    const int gm = G < m_tiles - first_m ? G : m_tiles - first_m;
+    const int in = t - group * G * n_tiles;
+    tm = first_m + in % gm;
+    tn = in / gm;
+}
+
 // FP8 (kind::f8f6f4, E4M3 -> FP32) modes, and the same three on the INT8 tensor path
 // (kind::i8, S8/U8 -> S32) of the INT8 Ozaki-II scheme (NEXT-3): MODE_X_I8 = MODE_X + 3
 enum GemmMode : int {
@@ -197,5 +210,12 @@ cudaError_t launch_crt(int limbs, const int16_t* res, int64_t m, int64_t n, cons
                        const int32_t* e_mu, const int32_t* e_nu, double alpha, double beta,
                        double* C, int64_t ldc, bool generic, cudaStream_t st);
 cudaError_t launch_scale(double* C, int64_t m, int64_t n, int64_t ldc, double beta, cudaStream_t st);
+// CRT + inverse scaling of the tiles [t0, t0 + count) of the residue GEMM's tile order (the
+// split tail of the hybrid schedule when the CRT of the other tiles is fused): tile t covers
+// rows tm tile_rows .. and columns tn tile_cols .. (tile_coords_g with G)
+cudaError_t launch_crt_tiles(int limbs, const int16_t* res, int64_t m, int64_t n, const CrtParams& cp,
+                             const int32_t* e_mu, const int32_t* e_nu, double alpha, double beta, double* C,
+                             int64_t ldc, int t0, int count, int G, int m_tiles, int n_tiles, int tile_rows,
+                             int tile_cols, cudaStream_t st);
 
 }  // namespace oz2

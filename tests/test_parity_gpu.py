@@ -923,3 +923,46 @@ def test_workspace_and_buffer_guards(ta, tb, m, n, k, N, sch, mode, tile_n, bloc
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, (r.stdout + r.stderr)[-2000:]
     assert r.stdout.startswith("ok")
+
+
+_HYBRID_SNIPPET = r"""
+import hashlib, sys
+import numpy as np, torch
+sys.path.insert(0, ".")
+import paper_2603_10634_b200 as P
+from synth import gen_device
+sch, cg, tile_n = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
+m, n, k, N = 2560, 2560, 16384, 13 if sch != "int8" else 15
+A = gen_device(m, k, "phi", phi=1.0, seed=81)
+B = gen_device(k, n, "phi", phi=1.0, seed=82)
+C0 = gen_device(m, n, "uniform", seed=83)
+P.oz2_set_stream(torch.cuda.current_stream().cuda_stream)
+assert P.oz2_set_scheme(sch) == 0
+assert P.oz2_set_tuning("cta_group", cg) == 0 and P.oz2_set_tuning("tile_n", tile_n) == 0
+for split, fused in ((0, 1), (2, 1), (2, 0), (1, 0)):
+    assert P.oz2_set_tuning("mod_split", split) == 0 and P.oz2_set_tuning("fused_crt", fused) == 0
+    C = C0.clone()
+    assert P.oz2_dgemm("N", "N", m, n, k, 1.0, A.data_ptr(), m, B.data_ptr(), k, 0.5, C.data_ptr(), m, N) == 0
+    torch.cuda.synchronize()
+    print(split, fused, hashlib.sha256(C.cpu().numpy().tobytes()).hexdigest())
+"""
+
+
+@pytest.mark.parametrize("sch,cg,tile_n", [("fp8", 2, 256), ("fp8", 1, 256), ("fp8", 4, 256),
+                                           ("fp8", 2, 512), ("karatsuba", 2, 256), ("int8", 2, 256)])
+def test_hybrid_schedule_with_fused_crt(sch, cg, tile_n):
+    """The hybrid schedule with the fused CRT (tile-major head items keep the CRT in the
+    GEMM epilogue, the split tail's tiles get theirs from k_crt_tiles) gives the same C as
+    tile-major + fused, hybrid + separate CRT and all-split, bit for bit, with beta != 0 (a
+    tile whose CRT ran twice would apply beta twice).  2560^2 x 16384: 100 CTA-pair tiles,
+    74 in the head wave, a 26-tile tail.  Subprocess with a timeout."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _HYBRID_SNIPPET, sch, str(cg), str(tile_n)], cwd=root,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln.split() for ln in r.stdout.strip().splitlines()]
+    assert len(lines) == 4
+    assert len({ln[2] for ln in lines}) == 1, lines
