@@ -435,9 +435,10 @@ def run_oz2(args, rank, world, local_rank):
     hbm_phases["peak_gbs"] = hbm_peak
     hbm_phases["note"] = ("phase times are CUDA events around both operands' kernels inside the step, "
                           "at the power-capped clock; per-kernel ncu figures: profiles/round1_ncu_prep_16384.md")
-    # rowmax x2, cast x2, [bound GEMM], exps, digits x2, residue GEMM, [k_crt unless fused]
+    # rowmax x2, cast x2, [bound GEMM], exps, digits x2, residue GEMM, [one CRT launch: k_crt
+    # unless fused, or k_crt_tiles for the split tail of a fused hybrid schedule]
     # the library's work-item rule (oz2_api.cu): all split below 8 tiles per CTA pair, else
-    # tile-major, or hybrid (split tail wave, separate CRT) when the last wave is ragged
+    # tile-major, or hybrid (split tail wave) when the last wave is ragged
     tiles = ((m + 255) // 256) * ((n + 255) // 256)
     units = torch.cuda.get_device_properties(dev).multi_processor_count // 2
     waves = -(-tiles // units)
@@ -446,9 +447,10 @@ def run_oz2(args, rank, world, local_rank):
     fenv = P.oz2_get_tuning("fused_crt")
     fusable = (P.oz2_plan_query(N, k).num_limbs <= 6 and k >= 8192
                and (fenv > 0 or (fenv < 0 and k >= (49152 if args.scheme == "int8" else 16384))))
-    mod_split = (ms_env == 1 or ms_env == 2) or (ms_env < 0 and (tiles < 8 * units or (ragged and not fusable)))
-    fused = fusable and not mod_split
-    launches_per_step = (8 + (args.mode == "accurate") + (not fused)) * (panels if world > 1 else 1)
+    all_split = ms_env == 1 or (ms_env < 0 and tiles < 8 * units)
+    hybrid = not all_split and (ms_env == 2 or (ms_env < 0 and ragged))
+    crt_launch = all_split or hybrid or not fusable
+    launches_per_step = (8 + (args.mode == "accurate") + crt_launch) * (panels if world > 1 else 1)
 
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
